@@ -1,0 +1,222 @@
+/*
+ * pmsz.h -- C ABI of the B200-native pMSz correction loop.
+ *
+ * This is the drop-in boundary for the hot path named in BASELINE.json: the
+ * reference package `topocorrect` (Python/NumPy, /root/reference/pkg) exposes
+ * the path as Python functions, not as an FFI, so every entry point below is
+ * the C-level equivalent of one reference function, cited by file:line
+ * (paths relative to /root/reference/pkg/src/topocorrect/).  The Python
+ * mirror in paper_2601_01787_b200/ binds these symbols with ctypes (see
+ * INTEGRATION.md for the stub a maintainer would add on the reference side).
+ *
+ * Conventions
+ *  - Plain pointers and sizes only; no torch types.  Pointers suffixed _dev
+ *    are CUDA device pointers, _host are host pointers.  `stream` is a
+ *    cudaStream_t passed as void*.  NULL stream = legacy default stream.
+ *  - Fields are flat, x fastest: id = x + nx*(y + ny*z) (grid.py:9-13,85-89).
+ *  - Values are f64 (grid.py:57).  The original field f may be passed as f32
+ *    when the caller knows it is f32-exact (codec.py:86-87 promotion is exact).
+ *  - Every function returns a pmsz_status; details of the last error on the
+ *    calling thread are available from pmsz_last_error().
+ */
+#ifndef PMSZ_H
+#define PMSZ_H
+
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    PMSZ_OK = 0,
+    PMSZ_ERR_INVALID = 1,      /* ValueError: dims/config/grid (correction.py:54-55,77-91) */
+    PMSZ_ERR_BOUND = 2,        /* BoundViolationError (correction.py:33-45,52-60) */
+    PMSZ_ERR_MONOTONE = 3,     /* AssertionError "edit raised a value" (correction.py:240-241) */
+    PMSZ_ERR_CONVERGENCE = 4,  /* ConvergenceError (correction.py:48-49,417-429) */
+    PMSZ_ERR_CUDA = 5,         /* CUDA runtime failure */
+    PMSZ_ERR_NONFINITE = 6     /* ValueError "field values must all be finite" (grid.py:62-63) */
+} pmsz_status;
+
+/* ConvergenceError sub-kinds, reported in pmsz_result.convergence_kind. */
+enum {
+    PMSZ_CONV_NONE = 0,
+    PMSZ_CONV_CAP = 1,       /* "no zero-edit iteration within cap"        correction.py:417-419 */
+    PMSZ_CONV_BOUND = 2,     /* "corrected field escaped the error bound"  correction.py:422-423 */
+    PMSZ_CONV_RESIDUAL = 3   /* "distortions survived a zero-edit iteration" correction.py:424-426 */
+};
+
+/* Plan flags. */
+enum {
+    PMSZ_FLAG_INCREMENTAL = 1,   /* dirty-ring sweeps after the first (exact) */
+    PMSZ_FLAG_EXTREMA_ONLY = 2,  /* drop the two order kinds (BASELINE config 5) */
+    PMSZ_FLAG_F32_ORIGINAL = 4   /* f is passed as float32 (exact promotion) */
+};
+
+/* Distortion kinds, in the reference declaration order (correction.py:133-139). */
+enum {
+    PMSZ_KIND_FALSE_MAX = 0, PMSZ_KIND_MISSING_MAX = 1,
+    PMSZ_KIND_FALSE_MIN = 2, PMSZ_KIND_MISSING_MIN = 3,
+    PMSZ_KIND_ASC_ORDER = 4, PMSZ_KIND_DESC_ORDER = 5
+};
+
+/*
+ * One correction domain: the whole grid (run_correction) or one block's
+ * extended extent (parallel.py:43-82).  Centers are restricted to the core
+ * box [core_lo, core_hi) given in the domain's own coordinates
+ * (the reference's `center_mask`, correction.py:169-180, parallel.py:73-77).
+ * shared_lo/shared_hi give, per axis, the width (0 or 2) of the band at the
+ * low/high face whose vertices are replicated in a neighbouring block
+ * (`_replicated_mask_zyx`, parallel.py:228-234); edits there raise
+ * shared_dirty (parallel.py:249-250).
+ */
+typedef struct {
+    int64_t nx, ny, nz;
+    int64_t core_lo[3];
+    int64_t core_hi[3];
+    int32_t shared_lo[3];
+    int32_t shared_hi[3];
+    double xi;                 /* CorrectionConfig.xi_abs (correction.py:63-96) */
+    double tau;                /* CorrectionConfig.tau */
+    int64_t max_iterations;    /* CorrectionConfig.max_outer_iterations */
+    int32_t flags;             /* PMSZ_FLAG_* */
+    int32_t reserved;
+} pmsz_desc;
+
+typedef struct pmsz_plan pmsz_plan;
+
+/* Counters of one run / one iteration (all on the host after the call). */
+typedef struct {
+    int64_t iterations;            /* CorrectionResult.iterations */
+    int64_t edit_count;            /* |EditSet| */
+    int64_t max_vertex_edits;      /* CorrectionResult.max_vertex_edits */
+    int64_t bound_violations;      /* BoundViolationError.offenders */
+    int64_t bound_first_index;     /* BoundViolationError.index */
+    int64_t floor_violations;      /* fhat < f - xi (hazard H6) */
+    int64_t nonfinite;             /* non-finite inputs */
+    int64_t residual[6];           /* detections left by the final sweep, per kind */
+    int64_t convergence_kind;      /* PMSZ_CONV_* */
+    int64_t full_sweeps;           /* full-grid detection sweeps executed (incl. verify) */
+    int64_t sparse_sweeps;         /* dirty-ring sweeps executed */
+    int64_t shared_dirty;          /* block mode: an edit touched a replicated vertex */
+    int64_t last_edits;            /* edits of the last iteration */
+    int64_t last_detections;       /* centres with a detection in the last iteration */
+} pmsz_result;
+
+/* Error string of the last failing call on this thread. */
+const char* pmsz_last_error(void);
+/* Library version string. */
+const char* pmsz_version(void);
+/* Number of kernel launches issued by this library since load (evidence for bench). */
+int64_t pmsz_launch_count(void);
+
+/* ---- plans -------------------------------------------------------------- */
+pmsz_status pmsz_plan_create(const pmsz_desc* desc, pmsz_plan** out);
+void pmsz_plan_destroy(pmsz_plan* plan);
+/* Device bytes of scratch owned by the plan. */
+int64_t pmsz_plan_scratch_bytes(const pmsz_plan* plan);
+
+/*
+ * run_correction (correction.py:391-436) on device-resident buffers.
+ * f_dev: original (f64, or f32 with PMSZ_FLAG_F32_ORIGINAL); fhat_dev: f64;
+ * g_dev: f64 output (the corrected field; may alias fhat_dev for in-place).
+ * history_host: receives edits_per_iteration (capacity history_cap).
+ * Returns PMSZ_OK or the reference's failure (bound / monotone / convergence).
+ * The edit set is read afterwards with pmsz_edits_export.
+ */
+pmsz_status pmsz_run_correction(pmsz_plan* plan, const void* f_dev, const double* fhat_dev,
+                                double* g_dev, int64_t* history_host, int64_t history_cap,
+                                pmsz_result* result, void* stream);
+
+/*
+ * The same call with HOST buffers (the end-to-end drop-in): copies f and fhat
+ * in, runs, and writes the corrected field and the edit set back to the host.
+ * g_host may be NULL (edit set only); ids_host/vals_host receive up to
+ * edits_cap edits (EditSet.diff, correction.py:363-369).
+ */
+pmsz_status pmsz_run_correction_host(pmsz_plan* plan, const void* f_host, const double* fhat_host,
+                                     double* g_host, int64_t* ids_host, double* vals_host,
+                                     int64_t edits_cap, int64_t* history_host, int64_t history_cap,
+                                     pmsz_result* result, void* stream);
+
+/* Ascending ids where g != fhat and the corrected values (EditSet.diff). */
+pmsz_status pmsz_edits_export(pmsz_plan* plan, const double* g_dev, int64_t* ids_dev,
+                              double* vals_dev, int64_t cap, int64_t* count_out, void* stream);
+
+/* ---- stepwise interface (block-parallel engine, parallel.py:150-255) ---- */
+/* K0: validate the pair, build the f-code, g <- fhat (correction.py:52-60,118-122,404-405). */
+pmsz_status pmsz_prepare(pmsz_plan* plan, const void* f_dev, const double* fhat_dev,
+                         double* g_dev, pmsz_result* result, void* stream);
+/* One Jacobi iteration (_iterate_array, correction.py:232-242) over the core box.
+ * Returns edits / detections / shared_dirty in result->last_*.
+ * edited_mask_dev (optional, u8 per vertex) receives the iteration's edited mask. */
+pmsz_status pmsz_iterate(pmsz_plan* plan, const void* f_dev, double* g_dev,
+                         uint8_t* edited_mask_dev, pmsz_result* result, void* stream);
+/* Iterate to a local fixpoint (local_converge / relaxed _block_round, parallel.py:150-172,237-255);
+ * lockstep != 0 runs exactly one iteration.  iterations/edit totals are accumulated into result. */
+pmsz_status pmsz_block_round(pmsz_plan* plan, const void* f_dev, double* g_dev, int32_t lockstep,
+                             int64_t* round_edits, pmsz_result* result, void* stream);
+/* Mark the whole core box dirty again (after a ghost merge changed replicas). */
+pmsz_status pmsz_mark_all_dirty(pmsz_plan* plan, void* stream);
+/* Mark the dirty 1-ring of the given ext-local vertex ids (after a ghost merge). */
+pmsz_status pmsz_mark_dirty_ids(pmsz_plan* plan, const uint32_t* ids_dev, int64_t count, void* stream);
+/* Final full detection sweep; per-kind residuals into result->residual (correction.py:424-426). */
+pmsz_status pmsz_verify(pmsz_plan* plan, const double* g_dev, pmsz_result* result, void* stream);
+/* Dense bounds check L <= g <= U (BoundsField.admits, correction.py:124-125); count out. */
+pmsz_status pmsz_bounds_violations(pmsz_plan* plan, const void* f_dev, const double* g_dev,
+                                   int64_t* count_out, void* stream);
+
+/* ---- topology kernels ---------------------------------------------------- */
+/* scan_neighbors (topology.py:47-86): ids of the (value,id)-largest/smallest neighbour
+ * and extremum flags.  Outputs are device arrays of n entries. */
+pmsz_status pmsz_scan_neighbors(int64_t nx, int64_t ny, int64_t nz, const double* values_dev,
+                                int64_t* nmax_dev, int64_t* nmin_dev, uint8_t* is_max_dev,
+                                uint8_t* is_min_dev, void* stream);
+/* Packed 1-byte code per vertex: low nibble nmax direction rank (15 = maximum),
+ * high nibble nmin direction rank (15 = minimum). */
+pmsz_status pmsz_scan_codes(int64_t nx, int64_t ny, int64_t nz, const double* values_dev,
+                            uint8_t* code_dev, void* stream);
+
+/* ---- ghost exchange helpers (_merge_min, parallel.py:122-140) ------------ */
+/* Pack a sub-box [lo, hi) of a domain array into a contiguous buffer. */
+pmsz_status pmsz_box_pack(int64_t nx, int64_t ny, int64_t nz, const double* src_dev,
+                          const int64_t lo[3], const int64_t hi[3], double* buf_dev, void* stream);
+/* dst[box] = min(dst[box], buf); counts changed vertices into *changed_dev (u64, device). */
+pmsz_status pmsz_box_unpack_min(int64_t nx, int64_t ny, int64_t nz, double* dst_dev,
+                                const int64_t lo[3], const int64_t hi[3], const double* buf_dev,
+                                unsigned long long* changed_dev, void* stream);
+/* dst[box] = buf (owner broadcast); counts changed vertices. */
+pmsz_status pmsz_box_unpack_copy(int64_t nx, int64_t ny, int64_t nz, double* dst_dev,
+                                 const int64_t lo[3], const int64_t hi[3], const double* buf_dev,
+                                 unsigned long long* changed_dev, void* stream);
+/* After a merge: mark the 1-ring of every vertex of box [lo,hi) whose value differs
+ * from `before` as dirty for the next incremental sweep. */
+pmsz_status pmsz_box_mark_changed(pmsz_plan* plan, const int64_t lo[3], const int64_t hi[3],
+                                  const double* before_buf_dev, const double* g_dev, void* stream);
+
+/* ---- synthetic inputs (synth.py, quantizer.py) --------------------------- */
+/* Fractal Perlin noise of a sub-box [lo, lo+ext) of the global grid gdims, bit-exact with
+ * synth.perlin (synth.py:55-100).  perm512: the 512-entry table of synth._permutation. */
+pmsz_status pmsz_perlin(const int64_t gdims[3], const int64_t lo[3], const int64_t ext[3],
+                        const int32_t* perm512_host, double frequency, int32_t octaves,
+                        double* out_f64_dev, float* out_f32_dev, void* stream);
+/* min / max of n values (f32 or f64); result on the host. */
+pmsz_status pmsz_minmax(const void* values_dev, int32_t is_f32, int64_t n, double* mn, double* mx,
+                        void* stream);
+/* quantize (quantizer.py:122-154): recon = origin + code*(2 xi) with the ulp repair. */
+pmsz_status pmsz_quantize(const void* f_dev, int32_t is_f32, int64_t n, double origin, double xi,
+                          double* recon_dev, int64_t* max_code_out, void* stream);
+/* Seeded bounded noise fhat = clamp(f + xi*u, f - xi, f + xi), u in [-1,1) from a
+ * counter hash of (seed, global id); ids are global so blocks agree. */
+pmsz_status pmsz_bounded_noise(const void* f_dev, int32_t is_f32, int64_t nx, int64_t ny,
+                               int64_t nz, const int64_t gdims[3], const int64_t lo[3],
+                               double xi, uint64_t seed, double* out_dev, void* stream);
+/* Copy a sub-box of a global device array into a contiguous domain array (f64 or f32). */
+pmsz_status pmsz_box_extract(const int64_t gdims[3], const void* src_dev, int32_t is_f32,
+                             const int64_t lo[3], const int64_t ext[3], void* dst_dev, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PMSZ_H */

@@ -1,0 +1,158 @@
+"""ctypes binding of the C ABI in include/pmsz.h (libpmsz.so, sm_100a).
+
+There is no CPU fallback: importing this module works everywhere (so the
+CPU test suite can check the exported symbols), but every compute entry point
+raises if the library is absent or no CUDA device is visible.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+_HERE = Path(__file__).resolve().parent
+LIB_PATH = _HERE / "_lib" / "libpmsz.so"
+HEADER_PATH = _HERE.parent / "include" / "pmsz.h"
+
+PMSZ_OK = 0
+PMSZ_ERR_INVALID = 1
+PMSZ_ERR_BOUND = 2
+PMSZ_ERR_MONOTONE = 3
+PMSZ_ERR_CONVERGENCE = 4
+PMSZ_ERR_CUDA = 5
+PMSZ_ERR_NONFINITE = 6
+
+PMSZ_CONV_NONE = 0
+PMSZ_CONV_CAP = 1
+PMSZ_CONV_BOUND = 2
+PMSZ_CONV_RESIDUAL = 3
+
+FLAG_INCREMENTAL = 1
+FLAG_EXTREMA_ONLY = 2
+FLAG_F32_ORIGINAL = 4
+
+i64 = ctypes.c_int64
+i32 = ctypes.c_int32
+u64 = ctypes.c_uint64
+vp = ctypes.c_void_p
+dp = ctypes.POINTER(ctypes.c_double)
+i64p = ctypes.POINTER(ctypes.c_int64)
+
+
+class PmszDesc(ctypes.Structure):
+    _fields_ = [
+        ("nx", i64), ("ny", i64), ("nz", i64),
+        ("core_lo", i64 * 3), ("core_hi", i64 * 3),
+        ("shared_lo", i32 * 3), ("shared_hi", i32 * 3),
+        ("xi", ctypes.c_double), ("tau", ctypes.c_double),
+        ("max_iterations", i64),
+        ("flags", i32), ("reserved", i32),
+    ]
+
+
+class PmszResult(ctypes.Structure):
+    _fields_ = [
+        ("iterations", i64), ("edit_count", i64), ("max_vertex_edits", i64),
+        ("bound_violations", i64), ("bound_first_index", i64),
+        ("floor_violations", i64), ("nonfinite", i64),
+        ("residual", i64 * 6), ("convergence_kind", i64),
+        ("full_sweeps", i64), ("sparse_sweeps", i64), ("shared_dirty", i64),
+        ("last_edits", i64), ("last_detections", i64),
+    ]
+
+
+# name -> (restype, argtypes); every symbol declared in include/pmsz.h.
+SIGNATURES = {
+    "pmsz_last_error": (ctypes.c_char_p, []),
+    "pmsz_version": (ctypes.c_char_p, []),
+    "pmsz_launch_count": (i64, []),
+    "pmsz_plan_create": (i32, [ctypes.POINTER(PmszDesc), ctypes.POINTER(vp)]),
+    "pmsz_plan_destroy": (None, [vp]),
+    "pmsz_plan_scratch_bytes": (i64, [vp]),
+    "pmsz_run_correction": (i32, [vp, vp, vp, vp, i64p, i64, ctypes.POINTER(PmszResult), vp]),
+    "pmsz_run_correction_host": (i32, [vp, vp, vp, vp, vp, vp, i64, i64p, i64,
+                                       ctypes.POINTER(PmszResult), vp]),
+    "pmsz_edits_export": (i32, [vp, vp, vp, vp, i64, i64p, vp]),
+    "pmsz_prepare": (i32, [vp, vp, vp, vp, ctypes.POINTER(PmszResult), vp]),
+    "pmsz_iterate": (i32, [vp, vp, vp, vp, ctypes.POINTER(PmszResult), vp]),
+    "pmsz_block_round": (i32, [vp, vp, vp, i32, i64p, ctypes.POINTER(PmszResult), vp]),
+    "pmsz_mark_all_dirty": (i32, [vp, vp]),
+    "pmsz_mark_dirty_ids": (i32, [vp, vp, i64, vp]),
+    "pmsz_verify": (i32, [vp, vp, ctypes.POINTER(PmszResult), vp]),
+    "pmsz_bounds_violations": (i32, [vp, vp, vp, i64p, vp]),
+    "pmsz_scan_neighbors": (i32, [i64, i64, i64, vp, vp, vp, vp, vp, vp]),
+    "pmsz_scan_codes": (i32, [i64, i64, i64, vp, vp, vp]),
+    "pmsz_box_pack": (i32, [i64, i64, i64, vp, i64p, i64p, vp, vp]),
+    "pmsz_box_unpack_min": (i32, [i64, i64, i64, vp, i64p, i64p, vp, vp, vp]),
+    "pmsz_box_unpack_copy": (i32, [i64, i64, i64, vp, i64p, i64p, vp, vp, vp]),
+    "pmsz_box_mark_changed": (i32, [vp, i64p, i64p, vp, vp, vp]),
+    "pmsz_perlin": (i32, [i64p, i64p, i64p, ctypes.POINTER(i32), ctypes.c_double, i32, vp, vp, vp]),
+    "pmsz_minmax": (i32, [vp, i32, i64, dp, dp, vp]),
+    "pmsz_quantize": (i32, [vp, i32, i64, ctypes.c_double, ctypes.c_double, vp, i64p, vp]),
+    "pmsz_bounded_noise": (i32, [vp, i32, i64, i64, i64, i64p, i64p, ctypes.c_double, u64, vp, vp]),
+    "pmsz_box_extract": (i32, [i64p, vp, i32, i64p, i64p, vp, vp]),
+}
+
+
+class NativeLibraryMissing(RuntimeError):
+    """libpmsz.so is not built: there is deliberately no CPU fallback."""
+
+
+_lib = None
+
+
+def load(path: os.PathLike | None = None) -> ctypes.CDLL:
+    """Load libpmsz.so (without touching the GPU) and bind every symbol."""
+    global _lib
+    if _lib is not None and path is None:
+        return _lib
+    p = Path(path) if path is not None else LIB_PATH
+    if not p.exists():
+        raise NativeLibraryMissing(
+            f"{p} is missing; build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(the pMSz path has no CPU fallback)")
+    lib = ctypes.CDLL(str(p))
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if path is None:
+        _lib = lib
+    return lib
+
+
+def lib() -> ctypes.CDLL:
+    """The loaded library, after checking a CUDA device is present."""
+    import torch
+    if not torch.cuda.is_available():
+        raise RuntimeError("pMSz kernels need a CUDA device (sm_100a); none is visible")
+    return load()
+
+
+def last_error() -> str:
+    return load().pmsz_last_error().decode(errors="replace")
+
+
+def launch_count() -> int:
+    return int(load().pmsz_launch_count())
+
+
+def ivec(values) -> "ctypes.Array":
+    return (i64 * 3)(*[int(v) for v in values])
+
+
+def check(status: int, what: str) -> None:
+    """Raise RuntimeError for CUDA / argument failures (domain errors are mapped by callers)."""
+    if status != PMSZ_OK:
+        raise RuntimeError(f"{what} failed (status {status}): {last_error()}")
+
+
+def stream_handle(stream=None) -> int:
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+def ptr(t) -> int:
+    return int(t.data_ptr())

@@ -1,0 +1,130 @@
+// common.cuh -- stencil, total order and proposal primitives shared by the
+// pMSz kernels (sm_100a).
+//
+// Semantics follow /root/reference/pkg/src/topocorrect:
+//   * Freudenthal 14-stencil and (value, id) order: grid.py:24-32,111-118.
+//   * The neighbours of one centre are visited in ASCENDING ID ORDER, which is
+//     the lexicographic (dz, dy, dx) order of the offsets for every grid
+//     shape.  "rank" below is that position (0..13); the centre
+//     itself sorts between rank 6 (-x) and rank 7 (+x).  Visiting in rank
+//     order turns the reference's (value, id) tie-break into a plain ">="
+//     (running max keeps the later = larger id on ties) and "<" (running min
+//     keeps the earlier = smaller id), exactly topology.py:64-80.
+//   * Out-of-domain neighbours are padded with NaN: every ordered f64
+//     comparison with NaN is false, so they never win either chain.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace pmsz {
+
+// Offsets in ascending-id (rank) order.
+__host__ __device__ constexpr int rank_dx(int r) {
+    constexpr int t[14] = {-1, 0, -1, 0, -1, 0, -1, 1, 0, 1, 0, 1, 0, 1};
+    return t[r];
+}
+__host__ __device__ constexpr int rank_dy(int r) {
+    constexpr int t[14] = {-1, -1, 0, 0, -1, -1, 0, 0, 1, 1, 0, 0, 1, 1};
+    return t[r];
+}
+__host__ __device__ constexpr int rank_dz(int r) {
+    constexpr int t[14] = {-1, -1, -1, -1, 0, 0, 0, 0, 0, 0, 1, 1, 1, 1};
+    return t[r];
+}
+// Centre sorts above ranks 0..6 and below ranks 7..13.
+constexpr int kCenterBelow = 6;
+constexpr uint8_t kExtremum = 15;
+
+struct Dom {
+    int64_t nx, ny, nz;   // domain (ext) extents
+    int64_t sy, sz;       // strides: 1, nx, nx*ny
+    int64_t n;
+    int64_t lo[3], hi[3]; // core (centre) box
+    int32_t shl[3], shh[3]; // shared band widths (block mode)
+    double xi, tau;
+    int extrema_only;
+};
+
+__device__ __forceinline__ double nan64() { return __longlong_as_double(0x7ff8000000000000ll); }
+
+// Order-preserving 64-bit key of a finite double (min-merge by atomicMin).
+// Proposals are g[a] - tau with tau > 0, which is never -0.0.
+__device__ __forceinline__ unsigned long long okey(double v) {
+    unsigned long long b = (unsigned long long)__double_as_longlong(v);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double okey_inv(unsigned long long k) {
+    unsigned long long b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+    return __longlong_as_double((long long)b);
+}
+constexpr unsigned long long kNoProposal = 0xffffffffffffffffull;
+
+// Result of the steepest-neighbour scan of one centre.
+struct Scan {
+    double vc;        // centre value
+    double vmax;      // value of the (value,id)-largest neighbour
+    double vmin;      // value of the (value,id)-smallest neighbour
+    int rmax, rmin;   // their ranks
+    bool is_max, is_min;
+};
+
+__device__ __forceinline__ uint8_t scan_code(const Scan& s) {
+    uint8_t lo = s.is_max ? kExtremum : (uint8_t)s.rmax;
+    uint8_t hi = s.is_min ? kExtremum : (uint8_t)s.rmin;
+    return (uint8_t)(lo | (hi << 4));
+}
+
+// Fold 14 neighbour values (rank order, NaN = absent) into a Scan.
+__device__ __forceinline__ Scan fold_scan(double vc, const double (&nv)[14]) {
+    Scan s;
+    s.vc = vc;
+    double bmax = -__longlong_as_double(0x7ff0000000000000ll);  // -inf
+    double bmin = __longlong_as_double(0x7ff0000000000000ll);   // +inf
+    int rmax = 15, rmin = 15;
+#pragma unroll
+    for (int r = 0; r < 14; ++r) {
+        const double v = nv[r];
+        const bool tmax = v >= bmax;
+        bmax = tmax ? v : bmax;
+        rmax = tmax ? r : rmax;
+        const bool tmin = v < bmin;
+        bmin = tmin ? v : bmin;
+        rmin = tmin ? r : rmin;
+    }
+    s.vmax = bmax; s.vmin = bmin; s.rmax = rmax; s.rmin = rmin;
+    // topology.py:79-80
+    s.is_max = (bmax < vc) || (bmax == vc && rmax <= kCenterBelow);
+    s.is_min = (bmin > vc) || (bmin == vc && rmin > kCenterBelow);
+    return s;
+}
+
+__device__ __forceinline__ void coords(const Dom& d, int64_t c, int64_t& x, int64_t& y, int64_t& z) {
+    z = c / d.sz;
+    int64_t r = c - z * d.sz;
+    y = r / d.sy;
+    x = r - y * d.sy;
+}
+
+__device__ __forceinline__ bool in_dom(const Dom& d, int64_t x, int64_t y, int64_t z) {
+    return x >= 0 && x < d.nx && y >= 0 && y < d.ny && z >= 0 && z < d.nz;
+}
+
+__device__ __forceinline__ int64_t rank_off(const Dom& d, int r) {
+    return (int64_t)rank_dx(r) + (int64_t)rank_dy(r) * d.sy + (int64_t)rank_dz(r) * d.sz;
+}
+
+// Gather-based scan of centre (x,y,z) from global memory (sparse sweeps and
+// domain edges).
+__device__ __forceinline__ Scan gather_scan(const Dom& d, const double* __restrict__ g,
+                                            int64_t x, int64_t y, int64_t z) {
+    const int64_t c = x + y * d.sy + z * d.sz;
+    double nv[14];
+#pragma unroll
+    for (int r = 0; r < 14; ++r) {
+        const bool ok = in_dom(d, x + rank_dx(r), y + rank_dy(r), z + rank_dz(r));
+        nv[r] = ok ? __ldg(g + c + rank_off(d, r)) : nan64();
+    }
+    return fold_scan(__ldg(g + c), nv);
+}
+
+}  // namespace pmsz

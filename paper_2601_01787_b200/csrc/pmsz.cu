@@ -1,0 +1,976 @@
+// pmsz.cu -- B200 (sm_100a) correction loop of pMSz behind the C ABI of
+// include/pmsz.h.  One plan = one correction domain (the whole grid for
+// run_correction, one block's extended extent for the block-parallel engine).
+//
+// Device layout per plan (N = domain voxels):
+//   g      f64[N]   caller-owned corrected field (read-only inside K1, K2 writes)
+//   f      f32/f64  caller-owned original field (read by K0 and, sparsely, by K2)
+//   code   u8[N]    packed f-scan: nmax rank | nmin rank << 4, 15 = extremum
+//   prop   u64[N]   order-preserving proposal keys, all-ones when idle (the
+//                   invariant is restored by K2, so no per-iteration memset)
+//   work   u32[N]   targets of the current iteration
+//   act    u32[2][cap] + actbits u32[N/32]  dirty-centre lists (incremental mode)
+//   editbits u32[N/32]  ever-edited bitmap -> EditSet
+//   counts u16[N]   per-vertex edit counts (max_vertex_edits)
+#include <cuda_runtime.h>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+#include <atomic>
+#include <algorithm>
+
+#include "../../include/pmsz.h"
+#include "common.cuh"
+#include "sweep.cuh"
+#include "gen.cuh"
+#include "tiles.cuh"
+
+using namespace pmsz;
+
+namespace {
+
+thread_local std::string g_last_error;
+std::atomic<long long> g_launches{0};
+
+pmsz_status fail(pmsz_status st, const std::string& msg) {
+    g_last_error = msg;
+    return st;
+}
+
+#define CUDA_TRY(expr)                                                                        \
+    do {                                                                                      \
+        cudaError_t _e = (expr);                                                              \
+        if (_e != cudaSuccess)                                                                \
+            return fail(PMSZ_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));   \
+    } while (0)
+
+#define LAUNCHED() (g_launches.fetch_add(1, std::memory_order_relaxed))
+
+inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+int g_num_sms = 0;
+int num_sms() {
+    if (!g_num_sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+        if (g_num_sms <= 0) g_num_sms = 148;
+    }
+    return g_num_sms;
+}
+
+inline unsigned grid_for(long long n, int threads, int per_sm = 8) {
+    long long b = (n + threads - 1) / threads;
+    long long cap = (long long)num_sms() * per_sm;
+    if (b > cap) b = cap;
+    if (b < 1) b = 1;
+    return (unsigned)b;
+}
+
+// ---- K0: validation + f-code + g <- fhat ----------------------------------
+template <typename FT>
+__global__ void __launch_bounds__(256) k_prep(Dom d, const FT* __restrict__ f, const double* __restrict__ fh,
+                                              double* __restrict__ g, uint8_t* __restrict__ code,
+                                              DevCounters* ctr) {
+    const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t y = (int64_t)blockIdx.y * blockDim.y + threadIdx.y;
+    const int64_t z = blockIdx.z;
+    const bool live = x < d.nx && y < d.ny;
+    unsigned bound = 0, floorv = 0, upper = 0, nonfin = 0;
+    if (live) {
+        const int64_t c = x + y * d.sy + z * d.sz;
+        const double fv = (double)f[c];
+        const double hv = fh[c];
+        nonfin = (!isfinite(fv) || !isfinite(hv)) ? 1u : 0u;
+        // validate_error_bound (correction.py:56-60)
+        if (fabs(fv - hv) > d.xi) {
+            bound = 1;
+            atomicMin(&ctr->bound_first, (unsigned long long)c);
+        }
+        floorv = hv < fv - d.xi ? 1u : 0u;   // hazard H6
+        upper = hv > fv + d.xi ? 1u : 0u;
+        if (g != fh) g[c] = hv;
+        // field_scan(original) (correction.py:404)
+        double nv[14];
+#pragma unroll
+        for (int r = 0; r < 14; ++r) {
+            const bool ok = in_dom(d, x + rank_dx(r), y + rank_dy(r), z + rank_dz(r));
+            nv[r] = ok ? (double)f[c + rank_off(d, r)] : nan64();
+        }
+        code[c] = scan_code(fold_scan(fv, nv));
+    }
+    const unsigned b = __reduce_add_sync(0xffffffffu, bound);
+    const unsigned fl = __reduce_add_sync(0xffffffffu, floorv);
+    const unsigned up = __reduce_add_sync(0xffffffffu, upper);
+    const unsigned nf = __reduce_add_sync(0xffffffffu, nonfin);
+    if (((threadIdx.y * blockDim.x + threadIdx.x) & 31) == 0) {
+        if (b) atomicAdd(&ctr->bound_viol, (unsigned long long)b);
+        if (fl) atomicAdd(&ctr->floor_viol, (unsigned long long)fl);
+        if (up) atomicAdd(&ctr->upper_viol, (unsigned long long)up);
+        if (nf) atomicAdd(&ctr->nonfinite, (unsigned long long)nf);
+    }
+}
+
+// ---- standalone scan (topology.scan_neighbors) -----------------------------
+__global__ void __launch_bounds__(256) k_scan_full(Dom d, const double* __restrict__ v, int64_t* nmax,
+                                                   int64_t* nmin, uint8_t* ismax, uint8_t* ismin,
+                                                   uint8_t* code) {
+    const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t y = (int64_t)blockIdx.y * blockDim.y + threadIdx.y;
+    const int64_t z = blockIdx.z;
+    if (x >= d.nx || y >= d.ny) return;
+    const int64_t c = x + y * d.sy + z * d.sz;
+    const Scan s = gather_scan(d, v, x, y, z);
+    if (nmax) nmax[c] = c + rank_off(d, s.rmax);
+    if (nmin) nmin[c] = c + rank_off(d, s.rmin);
+    if (ismax) ismax[c] = s.is_max;
+    if (ismin) ismin[c] = s.is_min;
+    if (code) code[c] = scan_code(s);
+}
+
+// ---- bounds check (BoundsField.admits) ------------------------------------
+template <typename FT>
+__global__ void __launch_bounds__(256) k_bounds(int64_t n, const FT* __restrict__ f, const double* __restrict__ g,
+                                                double xi, unsigned long long* count) {
+    unsigned long long mine = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double fv = (double)f[i];
+        const double gv = g[i];
+        if (!(gv >= fv - xi && gv <= fv + xi)) ++mine;
+    }
+    mine = __reduce_add_sync(0xffffffffu, (unsigned)mine);
+    if ((threadIdx.x & 31) == 0 && mine) atomicAdd(count, mine);
+}
+
+// ---- edit-set compaction from the ever-edited bitmap -----------------------
+constexpr int kCompactThreads = 256;
+constexpr int kWordsPerThread = 8;
+constexpr int kWordsPerBlock = kCompactThreads * kWordsPerThread;
+
+__global__ void __launch_bounds__(kCompactThreads) k_bits_count(const uint32_t* __restrict__ bits, int64_t nwords,
+                                                                unsigned long long* block_counts) {
+    __shared__ unsigned long long warp_sums[kCompactThreads / 32];
+    const int64_t base = (int64_t)blockIdx.x * kWordsPerBlock;
+    unsigned c = 0;
+    for (int k = 0; k < kWordsPerThread; ++k) {
+        const int64_t wdx = base + (int64_t)k * kCompactThreads + threadIdx.x;
+        if (wdx < nwords) c += __popc(bits[wdx]);
+    }
+    c = __reduce_add_sync(0xffffffffu, c);
+    if ((threadIdx.x & 31) == 0) warp_sums[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long t = 0;
+        for (int i = 0; i < kCompactThreads / 32; ++i) t += warp_sums[i];
+        block_counts[blockIdx.x] = t;
+    }
+}
+
+__global__ void __launch_bounds__(1024) k_exclusive_scan(unsigned long long* v, int64_t n,
+                                                         unsigned long long* total) {
+    __shared__ unsigned long long carry;
+    __shared__ unsigned long long warp_tot[32];
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int64_t base = 0; base < n; base += blockDim.x) {
+        const int64_t i = base + threadIdx.x;
+        const unsigned long long x = i < n ? v[i] : 0ull;
+        // inclusive warp scan
+        unsigned long long s = x;
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long y = __shfl_up_sync(0xffffffffu, s, o);
+            if ((threadIdx.x & 31) >= o) s += y;
+        }
+        if ((threadIdx.x & 31) == 31) warp_tot[threadIdx.x >> 5] = s;
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            unsigned long long t = threadIdx.x < (blockDim.x >> 5) ? warp_tot[threadIdx.x] : 0ull;
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned long long y = __shfl_up_sync(0xffffffffu, t, o);
+                if (threadIdx.x >= o) t += y;
+            }
+            warp_tot[threadIdx.x] = t;   // inclusive over warps
+        }
+        __syncthreads();
+        const unsigned long long warp_off = (threadIdx.x >> 5) ? warp_tot[(threadIdx.x >> 5) - 1] : 0ull;
+        if (i < n) v[i] = carry + warp_off + s - x;
+        __syncthreads();
+        if (threadIdx.x == blockDim.x - 1) carry += warp_off + s;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *total = carry;
+}
+
+__global__ void __launch_bounds__(kCompactThreads) k_bits_write(const uint32_t* __restrict__ bits, int64_t nwords,
+                                                                int64_t n, const unsigned long long* block_offs,
+                                                                const double* __restrict__ g, int64_t* ids,
+                                                                double* vals, int64_t cap) {
+    __shared__ unsigned warp_sums[kCompactThreads / 32];
+    const int64_t base = (int64_t)blockIdx.x * kWordsPerBlock;
+    // Each thread owns kWordsPerThread CONSECUTIVE words so ids stay ascending.
+    const int64_t w0 = base + (int64_t)threadIdx.x * kWordsPerThread;
+    uint32_t wv[kWordsPerThread];
+    unsigned c = 0;
+    for (int k = 0; k < kWordsPerThread; ++k) {
+        wv[k] = (w0 + k < nwords) ? bits[w0 + k] : 0u;
+        c += __popc(wv[k]);
+    }
+    // exclusive scan of c across the block
+    unsigned s = c;
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned y = __shfl_up_sync(0xffffffffu, s, o);
+        if ((threadIdx.x & 31) >= o) s += y;
+    }
+    if ((threadIdx.x & 31) == 31) warp_sums[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        unsigned t = threadIdx.x < kCompactThreads / 32 ? warp_sums[threadIdx.x] : 0u;
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned y = __shfl_up_sync(0xffffffffu, t, o);
+            if (threadIdx.x >= o) t += y;
+        }
+        if (threadIdx.x < kCompactThreads / 32) warp_sums[threadIdx.x] = t;
+    }
+    __syncthreads();
+    const unsigned warp_off = (threadIdx.x >> 5) ? warp_sums[(threadIdx.x >> 5) - 1] : 0u;
+    int64_t pos = (int64_t)block_offs[blockIdx.x] + warp_off + s - c;
+    for (int k = 0; k < kWordsPerThread; ++k) {
+        uint32_t m = wv[k];
+        while (m) {
+            const int b = __ffs(m) - 1;
+            m &= m - 1;
+            const int64_t id = (w0 + k) * 32 + b;
+            if (id < n && pos < cap) {
+                ids[pos] = id;
+                vals[pos] = g[id];
+            }
+            ++pos;
+        }
+    }
+}
+
+// ---- ghost-box helpers -------------------------------------------------------
+struct Box {
+    int64_t nx, ny;
+    int64_t lo[3], ext[3];
+};
+
+__global__ void __launch_bounds__(256) k_box_pack(Box b, const double* __restrict__ src, double* __restrict__ buf) {
+    const int64_t n = b.ext[0] * b.ext[1] * b.ext[2];
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t z = i / (b.ext[0] * b.ext[1]), r = i - z * b.ext[0] * b.ext[1];
+        const int64_t y = r / b.ext[0], x = r - y * b.ext[0];
+        buf[i] = src[(b.lo[0] + x) + b.nx * ((b.lo[1] + y) + b.ny * (b.lo[2] + z))];
+    }
+}
+
+template <bool kMin>
+__global__ void __launch_bounds__(256) k_box_unpack(Box b, double* __restrict__ dst, const double* __restrict__ buf,
+                                                    unsigned long long* changed) {
+    const int64_t n = b.ext[0] * b.ext[1] * b.ext[2];
+    unsigned mine = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t z = i / (b.ext[0] * b.ext[1]), r = i - z * b.ext[0] * b.ext[1];
+        const int64_t y = r / b.ext[0], x = r - y * b.ext[0];
+        const int64_t o = (b.lo[0] + x) + b.nx * ((b.lo[1] + y) + b.ny * (b.lo[2] + z));
+        const double cur = dst[o], in = buf[i];
+        const double nv = kMin ? (in < cur ? in : cur) : in;
+        if (nv != cur) {
+            dst[o] = nv;
+            ++mine;
+        }
+    }
+    mine = __reduce_add_sync(0xffffffffu, mine);
+    if ((threadIdx.x & 31) == 0 && mine && changed) atomicAdd(changed, (unsigned long long)mine);
+}
+
+__global__ void __launch_bounds__(256) k_box_mark(Dom d, Work w, Box b, const double* __restrict__ before,
+                                                  const double* __restrict__ g, int nxt) {
+    const int64_t n = b.ext[0] * b.ext[1] * b.ext[2];
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t z = i / (b.ext[0] * b.ext[1]), r = i - z * b.ext[0] * b.ext[1];
+        const int64_t y = r / b.ext[0], x = r - y * b.ext[0];
+        const int64_t o = (b.lo[0] + x) + b.nx * ((b.lo[1] + y) + b.ny * (b.lo[2] + z));
+        if (g[o] != before[i]) mark_ring(d, w, o, nxt);
+    }
+}
+
+__global__ void __launch_bounds__(256) k_mark_ids(Dom d, Work w, const uint32_t* __restrict__ ids, int64_t n, int nxt) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        mark_ring(d, w, ids[i], nxt);
+}
+
+template <typename FT>
+__global__ void __launch_bounds__(256) k_box_extract(Box b, int64_t gny, const FT* __restrict__ src, FT* __restrict__ dst) {
+    const int64_t n = b.ext[0] * b.ext[1] * b.ext[2];
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t z = i / (b.ext[0] * b.ext[1]), r = i - z * b.ext[0] * b.ext[1];
+        const int64_t y = r / b.ext[0], x = r - y * b.ext[0];
+        dst[i] = src[(b.lo[0] + x) + b.nx * ((b.lo[1] + y) + gny * (b.lo[2] + z))];
+    }
+}
+
+}  // namespace
+
+// ============================================================================
+// Plan
+// ============================================================================
+struct pmsz_plan {
+    pmsz_desc desc;
+    Dom dom;
+    int64_t n = 0, nwords = 0;
+    Work w{};
+    DevCounters* ctr = nullptr;
+    DevCounters* hctr = nullptr;   // pinned mirror
+    unsigned long long* block_counts = nullptr;
+    int64_t nblocks_compact = 0;
+    int64_t scratch_bytes = 0;
+    int cur = 0;              // pending dirty list
+    bool next_full = true;    // next iteration must sweep the whole core box
+    bool last_full = true;
+    bool prepared = false;
+    int64_t floor_viol = 0, upper_viol = 0;
+    // block-round bookkeeping
+    int64_t iterations = 0, edit_total = 0;
+    int f32 = 0;
+};
+
+namespace {
+
+Dom make_dom(const pmsz_desc& d) {
+    Dom o{};
+    o.nx = d.nx; o.ny = d.ny; o.nz = d.nz;
+    o.sy = d.nx; o.sz = d.nx * d.ny; o.n = d.nx * d.ny * d.nz;
+    for (int a = 0; a < 3; ++a) {
+        o.lo[a] = d.core_lo[a]; o.hi[a] = d.core_hi[a];
+        o.shl[a] = d.shared_lo[a]; o.shh[a] = d.shared_hi[a];
+    }
+    o.xi = d.xi; o.tau = d.tau;
+    o.extrema_only = (d.flags & PMSZ_FLAG_EXTREMA_ONLY) ? 1 : 0;
+    return o;
+}
+
+pmsz_status sync_counters(pmsz_plan* p, cudaStream_t s) {
+    CUDA_TRY(cudaMemcpyAsync(p->hctr, p->ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    return PMSZ_OK;
+}
+
+// Reset the per-iteration counters (nwork, nedits, ndetect, shared_dirty, nact[nxt]).
+pmsz_status reset_iter(pmsz_plan* p, cudaStream_t s, int nxt) {
+    CUDA_TRY(cudaMemsetAsync(p->ctr, 0, offsetof(DevCounters, nact), s));
+    CUDA_TRY(cudaMemsetAsync(&p->ctr->nact[nxt], 0, sizeof(unsigned long long), s));
+    return PMSZ_OK;
+}
+
+template <typename FT>
+pmsz_status launch_apply(pmsz_plan* p, const void* f, double* g, cudaStream_t s, int nxt) {
+    k_apply<FT><<<grid_for(p->n, 256, 16), 256, 0, s>>>(p->dom, (const FT*)f, g, p->w, nxt);
+    LAUNCHED();
+    return PMSZ_OK;
+}
+
+// One Jacobi iteration (K1 full or sparse, then K2).  Leaves counters on host.
+pmsz_status iterate_once(pmsz_plan* p, const void* f, double* g, cudaStream_t s) {
+    const int nxt = p->cur ^ 1;
+    pmsz_status st = reset_iter(p, s, nxt);
+    if (st) return st;
+    const Dom& d = p->dom;
+    if (p->next_full || !p->w.incremental) {
+        if (p->w.incremental) CUDA_TRY(cudaMemsetAsync(p->w.actbits, 0, p->nwords * 4, s));
+        const int64_t cx = d.hi[0] - d.lo[0], cy = d.hi[1] - d.lo[1], cz = d.hi[2] - d.lo[2];
+        if (cx > 0 && cy > 0 && cz > 0) {
+            launch_sweep_full<false>(d, g, p->w, s);
+            LAUNCHED();
+        }
+        p->last_full = true;
+    } else {
+        k_sweep_sparse<<<grid_for(p->w.act_cap, 256, 16), 256, 0, s>>>(d, g, p->w, p->cur);
+        LAUNCHED();
+        p->last_full = false;
+    }
+    st = p->f32 ? launch_apply<float>(p, f, g, s, nxt) : launch_apply<double>(p, f, g, s, nxt);
+    if (st) return st;
+    CUDA_TRY(cudaGetLastError());
+    st = sync_counters(p, s);
+    if (st) return st;
+    // next mode
+    if (p->w.incremental) {
+        if (p->hctr->nact[nxt] > p->w.act_cap) {
+            p->next_full = true;
+        } else {
+            p->next_full = false;
+            p->cur = nxt;
+        }
+    }
+    return PMSZ_OK;
+}
+
+pmsz_status reset_run_state(pmsz_plan* p, cudaStream_t s) {
+    CUDA_TRY(cudaMemsetAsync(p->ctr, 0, sizeof(DevCounters), s));
+    CUDA_TRY(cudaMemsetAsync(&p->ctr->bound_first, 0xff, sizeof(unsigned long long), s));
+    CUDA_TRY(cudaMemsetAsync(p->w.editbits, 0, p->nwords * 4, s));
+    CUDA_TRY(cudaMemsetAsync(p->w.counts, 0, p->n * sizeof(uint16_t), s));
+    if (p->w.incremental) CUDA_TRY(cudaMemsetAsync(p->w.actbits, 0, p->nwords * 4, s));
+    p->cur = 0;
+    p->next_full = true;
+    p->iterations = 0;
+    p->edit_total = 0;
+    return PMSZ_OK;
+}
+
+// After an aborted run the proposal array may hold stale keys.
+pmsz_status restore_prop(pmsz_plan* p, cudaStream_t s) {
+    CUDA_TRY(cudaMemsetAsync(p->w.prop, 0xff, p->n * sizeof(unsigned long long), s));
+    return PMSZ_OK;
+}
+
+pmsz_status prep(pmsz_plan* p, const void* f, const double* fh, double* g, cudaStream_t s) {
+    pmsz_status st = reset_run_state(p, s);
+    if (st) return st;
+    const Dom& d = p->dom;
+    dim3 block(32, 8, 1);
+    dim3 grid((unsigned)((d.nx + 31) / 32), (unsigned)((d.ny + 7) / 8), (unsigned)d.nz);
+    if (p->f32)
+        k_prep<float><<<grid, block, 0, s>>>(d, (const float*)f, fh, g, p->w.code, p->ctr);
+    else
+        k_prep<double><<<grid, block, 0, s>>>(d, (const double*)f, fh, g, p->w.code, p->ctr);
+    LAUNCHED();
+    CUDA_TRY(cudaGetLastError());
+    st = sync_counters(p, s);
+    if (st) return st;
+    p->floor_viol = (int64_t)p->hctr->floor_viol;
+    p->upper_viol = (int64_t)p->hctr->upper_viol;
+    p->prepared = true;
+    return PMSZ_OK;
+}
+
+pmsz_status verify_sweep(pmsz_plan* p, const double* g, cudaStream_t s, int64_t kinds[6]) {
+    CUDA_TRY(cudaMemsetAsync(&p->ctr->kinds[0], 0, sizeof(p->ctr->kinds), s));
+    const Dom& d = p->dom;
+    const int64_t cx = d.hi[0] - d.lo[0], cy = d.hi[1] - d.lo[1], cz = d.hi[2] - d.lo[2];
+    if (cx > 0 && cy > 0 && cz > 0) {
+        launch_sweep_full<true>(d, g, p->w, s);
+        LAUNCHED();
+    }
+    CUDA_TRY(cudaGetLastError());
+    pmsz_status st = sync_counters(p, s);
+    if (st) return st;
+    for (int k = 0; k < 6; ++k) kinds[k] = (int64_t)p->hctr->kinds[k];
+    return PMSZ_OK;
+}
+
+pmsz_status count_bounds(pmsz_plan* p, const void* f, const double* g, cudaStream_t s, int64_t* out) {
+    CUDA_TRY(cudaMemsetAsync(&p->ctr->scratch[1], 0, sizeof(unsigned long long), s));
+    if (p->f32)
+        k_bounds<float><<<grid_for(p->n, 256), 256, 0, s>>>(p->n, (const float*)f, g, p->dom.xi, &p->ctr->scratch[1]);
+    else
+        k_bounds<double><<<grid_for(p->n, 256), 256, 0, s>>>(p->n, (const double*)f, g, p->dom.xi, &p->ctr->scratch[1]);
+    LAUNCHED();
+    CUDA_TRY(cudaGetLastError());
+    pmsz_status st = sync_counters(p, s);
+    if (st) return st;
+    *out = (int64_t)p->hctr->scratch[1];
+    return PMSZ_OK;
+}
+
+pmsz_status edit_count(pmsz_plan* p, cudaStream_t s, int64_t* count) {
+    k_bits_count<<<(unsigned)p->nblocks_compact, kCompactThreads, 0, s>>>(p->w.editbits, p->nwords, p->block_counts);
+    LAUNCHED();
+    k_exclusive_scan<<<1, 1024, 0, s>>>(p->block_counts, p->nblocks_compact, &p->ctr->scratch[2]);
+    LAUNCHED();
+    CUDA_TRY(cudaGetLastError());
+    pmsz_status st = sync_counters(p, s);
+    if (st) return st;
+    *count = (int64_t)p->hctr->scratch[2];
+    return PMSZ_OK;
+}
+
+void fill_result(pmsz_plan* p, pmsz_result* r) {
+    if (!r) return;
+    r->bound_violations = (int64_t)p->hctr->bound_viol;
+    r->bound_first_index = (int64_t)p->hctr->bound_first;
+    r->floor_violations = p->floor_viol;
+    r->nonfinite = (int64_t)p->hctr->nonfinite;
+    r->max_vertex_edits = (int64_t)p->hctr->maxcount;
+}
+
+}  // namespace
+
+// ============================================================================
+// C ABI
+// ============================================================================
+extern "C" {
+
+const char* pmsz_last_error(void) { return g_last_error.c_str(); }
+const char* pmsz_version(void) { return "pmsz-b200 0.1.0 (sm_100a)"; }
+int64_t pmsz_launch_count(void) { return (int64_t)g_launches.load(); }
+
+pmsz_status pmsz_plan_create(const pmsz_desc* desc, pmsz_plan** out) {
+    if (!desc || !out) return fail(PMSZ_ERR_INVALID, "null argument");
+    *out = nullptr;
+    const pmsz_desc& d = *desc;
+    if (d.nx < 1 || d.ny < 1 || d.nz < 1) return fail(PMSZ_ERR_INVALID, "dims must be positive");
+    const int64_t n = d.nx * d.ny * d.nz;
+    if (n >= (int64_t)0xffffffffll) return fail(PMSZ_ERR_INVALID, "domain too large for 32-bit ids");
+    if (!(d.xi > 0) || !(d.tau > 0) || !(d.tau < 2 * d.xi))
+        return fail(PMSZ_ERR_INVALID, "need xi > 0 and 0 < tau < 2 xi");
+    const int64_t ext[3] = {d.nx, d.ny, d.nz};
+    for (int a = 0; a < 3; ++a)
+        if (d.core_lo[a] < 0 || d.core_hi[a] > ext[a] || d.core_lo[a] > d.core_hi[a])
+            return fail(PMSZ_ERR_INVALID, "core box outside the domain");
+    pmsz_plan* p = new pmsz_plan();
+    p->desc = d;
+    p->dom = make_dom(d);
+    p->n = n;
+    p->nwords = (n + 31) / 32;
+    p->f32 = (d.flags & PMSZ_FLAG_F32_ORIGINAL) ? 1 : 0;
+    p->w.incremental = (d.flags & PMSZ_FLAG_INCREMENTAL) ? 1 : 0;
+    const int64_t ncore = (d.core_hi[0] - d.core_lo[0]) * (d.core_hi[1] - d.core_lo[1]) *
+                          (d.core_hi[2] - d.core_lo[2]);
+    p->w.act_cap = (unsigned long long)std::max<int64_t>(ncore / 4, 4096);
+    p->nblocks_compact = (p->nwords + kWordsPerBlock - 1) / kWordsPerBlock;
+    auto alloc = [&](void** ptr, size_t bytes) -> bool {
+        if (cudaMalloc(ptr, bytes) != cudaSuccess) return false;
+        p->scratch_bytes += (int64_t)bytes;
+        return true;
+    };
+    bool ok = alloc((void**)&p->w.prop, n * 8) && alloc((void**)&p->w.work, n * 4) &&
+              alloc((void**)&p->w.editbits, p->nwords * 4) && alloc((void**)&p->w.counts, n * 2) &&
+              alloc((void**)&p->w.code, n) && alloc((void**)&p->ctr, sizeof(DevCounters)) &&
+              alloc((void**)&p->block_counts, std::max<int64_t>(p->nblocks_compact, 1) * 8);
+    if (ok && p->w.incremental)
+        ok = alloc((void**)&p->w.actbits, p->nwords * 4) && alloc((void**)&p->w.act[0], p->w.act_cap * 4) &&
+             alloc((void**)&p->w.act[1], p->w.act_cap * 4);
+    if (ok) ok = cudaMallocHost((void**)&p->hctr, sizeof(DevCounters)) == cudaSuccess;
+    if (!ok) {
+        cudaGetLastError();
+        pmsz_plan_destroy(p);
+        return fail(PMSZ_ERR_CUDA, "device allocation failed");
+    }
+    p->w.ctr = p->ctr;
+    memset(p->hctr, 0, sizeof(DevCounters));
+    if (cudaMemset(p->w.prop, 0xff, n * 8) != cudaSuccess || cudaMemset(p->ctr, 0, sizeof(DevCounters)) != cudaSuccess ||
+        cudaDeviceSynchronize() != cudaSuccess) {
+        pmsz_plan_destroy(p);
+        return fail(PMSZ_ERR_CUDA, "plan initialisation failed");
+    }
+    *out = p;
+    return PMSZ_OK;
+}
+
+void pmsz_plan_destroy(pmsz_plan* p) {
+    if (!p) return;
+    cudaFree(p->w.prop); cudaFree(p->w.work); cudaFree(p->w.editbits); cudaFree(p->w.counts);
+    cudaFree(p->w.code); cudaFree(p->ctr); cudaFree(p->block_counts);
+    cudaFree(p->w.actbits); cudaFree(p->w.act[0]); cudaFree(p->w.act[1]);
+    if (p->hctr) cudaFreeHost(p->hctr);
+    delete p;
+}
+
+int64_t pmsz_plan_scratch_bytes(const pmsz_plan* p) { return p ? p->scratch_bytes : 0; }
+
+pmsz_status pmsz_prepare(pmsz_plan* p, const void* f, const double* fh, double* g, pmsz_result* r, void* stream) {
+    if (!p || !f || !fh || !g) return fail(PMSZ_ERR_INVALID, "null argument");
+    cudaStream_t s = S(stream);
+    pmsz_status st = prep(p, f, fh, g, s);
+    if (st) return st;
+    fill_result(p, r);
+    if (p->hctr->nonfinite) return fail(PMSZ_ERR_NONFINITE, "field values must all be finite");
+    if (p->hctr->bound_viol) return fail(PMSZ_ERR_BOUND, "error bound violated");
+    return PMSZ_OK;
+}
+
+pmsz_status pmsz_iterate(pmsz_plan* p, const void* f, double* g, uint8_t* edited_mask, pmsz_result* r,
+                         void* stream) {
+    if (!p || !p->prepared) return fail(PMSZ_ERR_INVALID, "plan not prepared");
+    cudaStream_t s = S(stream);
+    p->w.edited_mask = edited_mask;
+    if (edited_mask) CUDA_TRY(cudaMemsetAsync(edited_mask, 0, p->n, s));
+    pmsz_status st = iterate_once(p, f, g, s);
+    p->w.edited_mask = nullptr;
+    if (st) { restore_prop(p, s); return st; }
+    if (p->floor_viol > 0 && p->hctr->ndetect > 0) {
+        restore_prop(p, s);
+        return fail(PMSZ_ERR_MONOTONE, "edit raised a value; monotonicity broken");
+    }
+    ++p->iterations;
+    p->edit_total += (int64_t)p->hctr->nedits;
+    if (r) {
+        fill_result(p, r);
+        r->last_edits = (int64_t)p->hctr->nedits;
+        r->last_detections = (int64_t)p->hctr->ndetect;
+        r->shared_dirty = (int64_t)p->hctr->shared_dirty;
+        r->iterations = p->iterations;
+        r->edit_count = p->edit_total;
+        if (p->last_full) ++r->full_sweeps; else ++r->sparse_sweeps;
+    }
+    return PMSZ_OK;
+}
+
+pmsz_status pmsz_block_round(pmsz_plan* p, const void* f, double* g, int32_t lockstep, int64_t* round_edits,
+                             pmsz_result* r, void* stream) {
+    if (!p || !p->prepared) return fail(PMSZ_ERR_INVALID, "plan not prepared");
+    int64_t total = 0;
+    bool dirty = false;
+    for (int64_t it = 0; it < p->desc.max_iterations; ++it) {
+        pmsz_status st = pmsz_iterate(p, f, g, nullptr, r, stream);
+        if (st) return st;
+        const int64_t e = (int64_t)p->hctr->nedits;
+        total += e;
+        dirty = dirty || p->hctr->shared_dirty;
+        if (lockstep || e == 0) {
+            if (round_edits) *round_edits = total;
+            if (r) r->shared_dirty = dirty;
+            return PMSZ_OK;
+        }
+    }
+    return fail(PMSZ_ERR_CONVERGENCE, "block found no zero-edit iteration within the cap");
+}
+
+pmsz_status pmsz_mark_all_dirty(pmsz_plan* p, void* stream) {
+    (void)stream;
+    if (!p) return fail(PMSZ_ERR_INVALID, "null plan");
+    p->next_full = true;
+    return PMSZ_OK;
+}
+
+pmsz_status pmsz_mark_dirty_ids(pmsz_plan* p, const uint32_t* ids, int64_t count, void* stream) {
+    if (!p) return fail(PMSZ_ERR_INVALID, "null plan");
+    if (!p->w.incremental || p->next_full || count <= 0) return PMSZ_OK;
+    cudaStream_t s = S(stream);
+    k_mark_ids<<<grid_for(count, 256), 256, 0, s>>>(p->dom, p->w, ids, count, p->cur);
+    LAUNCHED();
+    CUDA_TRY(cudaGetLastError());
+    pmsz_status st = sync_counters(p, s);
+    if (st) return st;
+    if (p->hctr->nact[p->cur] > p->w.act_cap) p->next_full = true;
+    return PMSZ_OK;
+}
+
+pmsz_status pmsz_box_mark_changed(pmsz_plan* p, const int64_t lo[3], const int64_t hi[3], const double* before,
+                                  const double* g, void* stream) {
+    if (!p) return fail(PMSZ_ERR_INVALID, "null plan");
+    if (!p->w.incremental || p->next_full) return PMSZ_OK;
+    cudaStream_t s = S(stream);
+    Box b{p->dom.nx, p->dom.ny, {lo[0], lo[1], lo[2]}, {hi[0] - lo[0], hi[1] - lo[1], hi[2] - lo[2]}};
+    const int64_t n = b.ext[0] * b.ext[1] * b.ext[2];
+    if (n <= 0) return PMSZ_OK;
+    k_box_mark<<<grid_for(n, 256), 256, 0, s>>>(p->dom, p->w, b, before, g, p->cur);
+    LAUNCHED();
+    CUDA_TRY(cudaGetLastError());
+    pmsz_status st = sync_counters(p, s);
+    if (st) return st;
+    if (p->hctr->nact[p->cur] > p->w.act_cap) p->next_full = true;
+    return PMSZ_OK;
+}
+
+pmsz_status pmsz_verify(pmsz_plan* p, const double* g, pmsz_result* r, void* stream) {
+    if (!p || !p->prepared) return fail(PMSZ_ERR_INVALID, "plan not prepared");
+    int64_t kinds[6];
+    pmsz_status st = verify_sweep(p, g, S(stream), kinds);
+    if (st) return st;
+    if (r) {
+        for (int k = 0; k < 6; ++k) r->residual[k] = kinds[k];
+        ++r->full_sweeps;
+    }
+    return PMSZ_OK;
+}
+
+pmsz_status pmsz_bounds_violations(pmsz_plan* p, const void* f, const double* g, int64_t* out, void* stream) {
+    if (!p || !out) return fail(PMSZ_ERR_INVALID, "null argument");
+    return count_bounds(p, f, g, S(stream), out);
+}
+
+pmsz_status pmsz_run_correction(pmsz_plan* p, const void* f, const double* fh, double* g, int64_t* history,
+                                int64_t history_cap, pmsz_result* r, void* stream) {
+    if (!p || !f || !fh || !g) return fail(PMSZ_ERR_INVALID, "null argument");
+    cudaStream_t s = S(stream);
+    pmsz_result local{};
+    if (!r) r = &local;
+    memset(r, 0, sizeof(*r));
+    pmsz_status st = pmsz_prepare(p, f, fh, g, r, stream);
+    if (st) return st;
+    bool converged = false;
+    int64_t it = 0;
+    for (; it < p->desc.max_iterations; ++it) {
+        st = pmsz_iterate(p, f, g, nullptr, r, stream);
+        if (st) return st;
+        const int64_t e = (int64_t)p->hctr->nedits;
+        if (history && it < history_cap) history[it] = e;
+        if (e == 0) { converged = true; ++it; break; }
+    }
+    r->iterations = it;
+    fill_result(p, r);
+    if (!converged) {
+        r->convergence_kind = PMSZ_CONV_CAP;
+        restore_prop(p, s);
+        return fail(PMSZ_ERR_CONVERGENCE, "no zero-edit iteration within the iteration cap");
+    }
+    // bounds.admits(g) (correction.py:422-423): only vertices whose fhat was
+    // outside [L, U] can fail, so the dense check runs only if K0 saw one.
+    if (p->floor_viol > 0 || p->upper_viol > 0) {
+        int64_t bad = 0;
+        st = count_bounds(p, f, g, s, &bad);
+        if (st) return st;
+        if (bad) {
+            r->convergence_kind = PMSZ_CONV_BOUND;
+            return fail(PMSZ_ERR_CONVERGENCE, "corrected field escaped the error bound");
+        }
+    }
+    // re-scan + _kind_masks must be empty (correction.py:424-426)
+    st = pmsz_verify(p, g, r, stream);
+    if (st) return st;
+    int64_t residual = 0;
+    for (int k = 0; k < 6; ++k) residual += r->residual[k];
+    if (residual) {
+        r->convergence_kind = PMSZ_CONV_RESIDUAL;
+        return fail(PMSZ_ERR_CONVERGENCE, "distortions survived a zero-edit iteration");
+    }
+    int64_t count = 0;
+    st = edit_count(p, s, &count);
+    if (st) return st;
+    r->edit_count = count;
+    return PMSZ_OK;
+}
+
+pmsz_status pmsz_edits_export(pmsz_plan* p, const double* g, int64_t* ids, double* vals, int64_t cap,
+                              int64_t* count_out, void* stream) {
+    if (!p || !g) return fail(PMSZ_ERR_INVALID, "null argument");
+    cudaStream_t s = S(stream);
+    int64_t count = 0;
+    pmsz_status st = edit_count(p, s, &count);
+    if (st) return st;
+    if (count_out) *count_out = count;
+    if (ids && vals && cap > 0 && count > 0) {
+        k_bits_write<<<(unsigned)p->nblocks_compact, kCompactThreads, 0, s>>>(p->w.editbits, p->nwords, p->n,
+                                                                             p->block_counts, g, ids, vals, cap);
+        LAUNCHED();
+        CUDA_TRY(cudaGetLastError());
+    }
+    return PMSZ_OK;
+}
+
+pmsz_status pmsz_run_correction_host(pmsz_plan* p, const void* f_host, const double* fh_host, double* g_host,
+                                     int64_t* ids_host, double* vals_host, int64_t edits_cap, int64_t* history,
+                                     int64_t history_cap, pmsz_result* r, void* stream) {
+    if (!p || !f_host || !fh_host) return fail(PMSZ_ERR_INVALID, "null argument");
+    cudaStream_t s = S(stream);
+    const size_t fbytes = p->n * (p->f32 ? 4 : 8), gbytes = p->n * 8;
+    void* f = nullptr;
+    double* g = nullptr;
+    int64_t* ids = nullptr;
+    double* vals = nullptr;
+    pmsz_status st = PMSZ_OK;
+    CUDA_TRY(cudaMallocAsync(&f, fbytes, s));
+    CUDA_TRY(cudaMallocAsync((void**)&g, gbytes, s));
+    CUDA_TRY(cudaMemcpyAsync(f, f_host, fbytes, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemcpyAsync(g, fh_host, gbytes, cudaMemcpyHostToDevice, s));
+    st = pmsz_run_correction(p, f, g, g, history, history_cap, r, stream);
+    if (st == PMSZ_OK) {
+        if (g_host) CUDA_TRY(cudaMemcpyAsync(g_host, g, gbytes, cudaMemcpyDeviceToHost, s));
+        if (ids_host && vals_host && edits_cap > 0 && r && r->edit_count > 0) {
+            const int64_t m = std::min(edits_cap, r->edit_count);
+            CUDA_TRY(cudaMallocAsync((void**)&ids, m * 8, s));
+            CUDA_TRY(cudaMallocAsync((void**)&vals, m * 8, s));
+            st = pmsz_edits_export(p, g, ids, vals, m, nullptr, stream);
+            if (st == PMSZ_OK) {
+                CUDA_TRY(cudaMemcpyAsync(ids_host, ids, m * 8, cudaMemcpyDeviceToHost, s));
+                CUDA_TRY(cudaMemcpyAsync(vals_host, vals, m * 8, cudaMemcpyDeviceToHost, s));
+            }
+            cudaFreeAsync(ids, s);
+            cudaFreeAsync(vals, s);
+        }
+    }
+    cudaFreeAsync(f, s);
+    cudaFreeAsync(g, s);
+    CUDA_TRY(cudaStreamSynchronize(s));
+    return st;
+}
+
+// ---- topology -------------------------------------------------------------
+static Dom whole_dom(int64_t nx, int64_t ny, int64_t nz) {
+    pmsz_desc d{};
+    d.nx = nx; d.ny = ny; d.nz = nz;
+    d.core_hi[0] = nx; d.core_hi[1] = ny; d.core_hi[2] = nz;
+    d.xi = 1; d.tau = 0.5;
+    return make_dom(d);
+}
+
+pmsz_status pmsz_scan_neighbors(int64_t nx, int64_t ny, int64_t nz, const double* v, int64_t* nmax, int64_t* nmin,
+                                uint8_t* ismax, uint8_t* ismin, void* stream) {
+    if (nx < 1 || ny < 1 || nz < 1 || !v) return fail(PMSZ_ERR_INVALID, "bad arguments");
+    Dom d = whole_dom(nx, ny, nz);
+    dim3 block(32, 8, 1), grid((unsigned)((nx + 31) / 32), (unsigned)((ny + 7) / 8), (unsigned)nz);
+    k_scan_full<<<grid, block, 0, S(stream)>>>(d, v, nmax, nmin, ismax, ismin, nullptr);
+    LAUNCHED();
+    CUDA_TRY(cudaGetLastError());
+    return PMSZ_OK;
+}
+
+pmsz_status pmsz_scan_codes(int64_t nx, int64_t ny, int64_t nz, const double* v, uint8_t* code, void* stream) {
+    if (nx < 1 || ny < 1 || nz < 1 || !v || !code) return fail(PMSZ_ERR_INVALID, "bad arguments");
+    Dom d = whole_dom(nx, ny, nz);
+    dim3 block(32, 8, 1), grid((unsigned)((nx + 31) / 32), (unsigned)((ny + 7) / 8), (unsigned)nz);
+    k_scan_full<<<grid, block, 0, S(stream)>>>(d, v, nullptr, nullptr, nullptr, nullptr, code);
+    LAUNCHED();
+    CUDA_TRY(cudaGetLastError());
+    return PMSZ_OK;
+}
+
+// ---- ghost boxes ------------------------------------------------------------
+static bool make_box(int64_t nx, int64_t ny, int64_t nz, const int64_t lo[3], const int64_t hi[3], Box& b) {
+    const int64_t ext[3] = {nx, ny, nz};
+    for (int a = 0; a < 3; ++a)
+        if (lo[a] < 0 || hi[a] > ext[a] || lo[a] > hi[a]) return false;
+    b = Box{nx, ny, {lo[0], lo[1], lo[2]}, {hi[0] - lo[0], hi[1] - lo[1], hi[2] - lo[2]}};
+    return true;
+}
+
+pmsz_status pmsz_box_pack(int64_t nx, int64_t ny, int64_t nz, const double* src, const int64_t lo[3],
+                          const int64_t hi[3], double* buf, void* stream) {
+    Box b;
+    if (!make_box(nx, ny, nz, lo, hi, b)) return fail(PMSZ_ERR_INVALID, "box outside the domain");
+    const int64_t n = b.ext[0] * b.ext[1] * b.ext[2];
+    if (n == 0) return PMSZ_OK;
+    k_box_pack<<<grid_for(n, 256), 256, 0, S(stream)>>>(b, src, buf);
+    LAUNCHED();
+    CUDA_TRY(cudaGetLastError());
+    return PMSZ_OK;
+}
+
+pmsz_status pmsz_box_unpack_min(int64_t nx, int64_t ny, int64_t nz, double* dst, const int64_t lo[3],
+                                const int64_t hi[3], const double* buf, unsigned long long* changed, void* stream) {
+    Box b;
+    if (!make_box(nx, ny, nz, lo, hi, b)) return fail(PMSZ_ERR_INVALID, "box outside the domain");
+    const int64_t n = b.ext[0] * b.ext[1] * b.ext[2];
+    if (n == 0) return PMSZ_OK;
+    k_box_unpack<true><<<grid_for(n, 256), 256, 0, S(stream)>>>(b, dst, buf, changed);
+    LAUNCHED();
+    CUDA_TRY(cudaGetLastError());
+    return PMSZ_OK;
+}
+
+pmsz_status pmsz_box_unpack_copy(int64_t nx, int64_t ny, int64_t nz, double* dst, const int64_t lo[3],
+                                 const int64_t hi[3], const double* buf, unsigned long long* changed, void* stream) {
+    Box b;
+    if (!make_box(nx, ny, nz, lo, hi, b)) return fail(PMSZ_ERR_INVALID, "box outside the domain");
+    const int64_t n = b.ext[0] * b.ext[1] * b.ext[2];
+    if (n == 0) return PMSZ_OK;
+    k_box_unpack<false><<<grid_for(n, 256), 256, 0, S(stream)>>>(b, dst, buf, changed);
+    LAUNCHED();
+    CUDA_TRY(cudaGetLastError());
+    return PMSZ_OK;
+}
+
+pmsz_status pmsz_box_extract(const int64_t gdims[3], const void* src, int32_t is_f32, const int64_t lo[3],
+                             const int64_t ext[3], void* dst, void* stream) {
+    int64_t hi[3] = {lo[0] + ext[0], lo[1] + ext[1], lo[2] + ext[2]};
+    Box b;
+    if (!make_box(gdims[0], gdims[1], gdims[2], lo, hi, b)) return fail(PMSZ_ERR_INVALID, "box outside the grid");
+    const int64_t n = ext[0] * ext[1] * ext[2];
+    if (n == 0) return PMSZ_OK;
+    if (is_f32)
+        k_box_extract<float><<<grid_for(n, 256), 256, 0, S(stream)>>>(b, gdims[1], (const float*)src, (float*)dst);
+    else
+        k_box_extract<double><<<grid_for(n, 256), 256, 0, S(stream)>>>(b, gdims[1], (const double*)src, (double*)dst);
+    LAUNCHED();
+    CUDA_TRY(cudaGetLastError());
+    return PMSZ_OK;
+}
+
+// ---- generators ---------------------------------------------------------------
+pmsz_status pmsz_perlin(const int64_t gdims[3], const int64_t lo[3], const int64_t ext[3], const int32_t* perm512,
+                        double frequency, int32_t octaves, double* out64, float* out32, void* stream) {
+    if (!gdims || !lo || !ext || !perm512 || octaves < 1) return fail(PMSZ_ERR_INVALID, "bad arguments");
+    cudaStream_t s = S(stream);
+    PerlinArgs a{};
+    for (int i = 0; i < 3; ++i) { a.gdims[i] = gdims[i]; a.lo[i] = lo[i]; a.ext[i] = ext[i]; }
+    a.frequency = frequency;
+    a.octaves = octaves;
+    int* perm = nullptr;
+    CUDA_TRY(cudaMallocAsync((void**)&perm, 512 * sizeof(int), s));
+    CUDA_TRY(cudaMemcpyAsync(perm, perm512, 512 * sizeof(int), cudaMemcpyHostToDevice, s));
+    const int64_t n = ext[0] * ext[1] * ext[2];
+    k_perlin<<<grid_for(n, 256, 16), 256, 0, s>>>(a, perm, out64, out32);
+    LAUNCHED();
+    cudaFreeAsync(perm, s);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaStreamSynchronize(s));   // perm512 is a host buffer owned by the caller
+    return PMSZ_OK;
+}
+
+pmsz_status pmsz_minmax(const void* v, int32_t is_f32, int64_t n, double* mn, double* mx, void* stream) {
+    if (!v || n < 1 || !mn || !mx) return fail(PMSZ_ERR_INVALID, "bad arguments");
+    cudaStream_t s = S(stream);
+    unsigned long long* k = nullptr;
+    CUDA_TRY(cudaMallocAsync((void**)&k, 16, s));
+    unsigned long long init[2] = {0xffffffffffffffffull, 0ull};
+    CUDA_TRY(cudaMemcpyAsync(k, init, 16, cudaMemcpyHostToDevice, s));
+    if (is_f32)
+        k_minmax<float><<<grid_for(n, 256, 16), 256, 0, s>>>((const float*)v, n, k, k + 1);
+    else
+        k_minmax<double><<<grid_for(n, 256, 16), 256, 0, s>>>((const double*)v, n, k, k + 1);
+    LAUNCHED();
+    unsigned long long out[2];
+    CUDA_TRY(cudaMemcpyAsync(out, k, 16, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    cudaFreeAsync(k, s);
+    auto inv = [](unsigned long long key) {
+        unsigned long long b = (key >> 63) ? (key & 0x7fffffffffffffffull) : ~key;
+        double d;
+        memcpy(&d, &b, 8);
+        return d;
+    };
+    *mn = inv(out[0]);
+    *mx = inv(out[1]);
+    return PMSZ_OK;
+}
+
+pmsz_status pmsz_quantize(const void* f, int32_t is_f32, int64_t n, double origin, double xi, double* recon,
+                          int64_t* max_code, void* stream) {
+    if (!f || !recon || n < 1 || !(xi > 0)) return fail(PMSZ_ERR_INVALID, "bad arguments");
+    cudaStream_t s = S(stream);
+    unsigned long long* k = nullptr;
+    CUDA_TRY(cudaMallocAsync((void**)&k, 16, s));
+    CUDA_TRY(cudaMemsetAsync(k, 0, 16, s));
+    const double two_xi = 2.0 * xi;
+    if (is_f32)
+        k_quantize<float><<<grid_for(n, 256, 16), 256, 0, s>>>((const float*)f, n, origin, xi, two_xi, recon, k, k + 1);
+    else
+        k_quantize<double><<<grid_for(n, 256, 16), 256, 0, s>>>((const double*)f, n, origin, xi, two_xi, recon, k, k + 1);
+    LAUNCHED();
+    unsigned long long out[2];
+    CUDA_TRY(cudaMemcpyAsync(out, k, 16, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    cudaFreeAsync(k, s);
+    if (max_code) *max_code = (int64_t)out[0];
+    if (out[1]) return fail(PMSZ_ERR_INVALID, "quantizer failed to meet its own bound");
+    return PMSZ_OK;
+}
+
+pmsz_status pmsz_bounded_noise(const void* f, int32_t is_f32, int64_t nx, int64_t ny, int64_t nz,
+                               const int64_t gdims[3], const int64_t lo[3], double xi, uint64_t seed, double* out,
+                               void* stream) {
+    if (!f || !out || !(xi > 0)) return fail(PMSZ_ERR_INVALID, "bad arguments");
+    cudaStream_t s = S(stream);
+    const int64_t n = nx * ny * nz;
+    if (is_f32)
+        k_bounded_noise<float><<<grid_for(n, 256, 16), 256, 0, s>>>((const float*)f, nx, ny, nz, gdims[0], gdims[1],
+                                                                   lo[0], lo[1], lo[2], xi, seed, out);
+    else
+        k_bounded_noise<double><<<grid_for(n, 256, 16), 256, 0, s>>>((const double*)f, nx, ny, nz, gdims[0],
+                                                                    gdims[1], lo[0], lo[1], lo[2], xi, seed, out);
+    LAUNCHED();
+    CUDA_TRY(cudaGetLastError());
+    return PMSZ_OK;
+}
+
+}  // extern "C"

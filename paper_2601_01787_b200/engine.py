@@ -1,0 +1,197 @@
+"""Device plans: one correction domain bound to libpmsz (host side of the C ABI).
+
+A :class:`DomainPlan` owns the device scratch of one domain (the whole grid,
+or one block's extended extent) and drives the kernels K0 (prepare), K1/K2
+(iterate), K4 (verify) and K5 (edit export).  Device buffers are torch CUDA
+tensors; only raw pointers cross the C ABI.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as N
+
+
+class BoundViolationError(ValueError):
+    """The decompressed field strays beyond the stated error bound
+    (correction.py:33-45: same fields and message)."""
+
+    def __init__(self, index, original, decompressed, xi_abs, offenders):
+        self.index = int(index)
+        self.original = float(original)
+        self.decompressed = float(decompressed)
+        self.xi_abs = float(xi_abs)
+        self.offenders = int(offenders)
+        super().__init__(
+            f"error bound violated at vertex {self.index}: "
+            f"|{self.original!r} - {self.decompressed!r}| > {self.xi_abs!r} "
+            f"(first of {self.offenders} offending vertices)")
+
+
+class ConvergenceError(RuntimeError):
+    """Correction failed to reach a distortion-free state (correction.py:48-49)."""
+
+
+@dataclass(frozen=True)
+class DomainSpec:
+    dims: tuple[int, int, int]
+    core_lo: tuple[int, int, int]
+    core_hi: tuple[int, int, int]
+    shared_lo: tuple[int, int, int] = (0, 0, 0)
+    shared_hi: tuple[int, int, int] = (0, 0, 0)
+
+    @staticmethod
+    def whole(dims) -> "DomainSpec":
+        d = tuple(int(v) for v in dims)
+        return DomainSpec(d, (0, 0, 0), d)
+
+
+class DomainPlan:
+    """One pmsz_plan (see include/pmsz.h)."""
+
+    def __init__(self, spec: DomainSpec, xi: float, tau: float, max_iterations: int,
+                 *, incremental: bool = True, extrema_only: bool = False,
+                 f32_original: bool = False):
+        self.lib = N.lib()
+        self.spec = spec
+        self.xi, self.tau, self.max_iterations = float(xi), float(tau), int(max_iterations)
+        self.f32_original = bool(f32_original)
+        d = N.PmszDesc()
+        d.nx, d.ny, d.nz = spec.dims
+        for a in range(3):
+            d.core_lo[a] = spec.core_lo[a]
+            d.core_hi[a] = spec.core_hi[a]
+            d.shared_lo[a] = spec.shared_lo[a]
+            d.shared_hi[a] = spec.shared_hi[a]
+        d.xi, d.tau, d.max_iterations = self.xi, self.tau, self.max_iterations
+        d.flags = ((N.FLAG_INCREMENTAL if incremental else 0)
+                   | (N.FLAG_EXTREMA_ONLY if extrema_only else 0)
+                   | (N.FLAG_F32_ORIGINAL if f32_original else 0))
+        h = ctypes.c_void_p()
+        st = self.lib.pmsz_plan_create(ctypes.byref(d), ctypes.byref(h))
+        if st == N.PMSZ_ERR_INVALID:
+            raise ValueError(N.last_error())
+        N.check(st, "pmsz_plan_create")
+        self.handle = h
+        self.n = spec.dims[0] * spec.dims[1] * spec.dims[2]
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self.lib.pmsz_plan_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def scratch_bytes(self) -> int:
+        return int(self.lib.pmsz_plan_scratch_bytes(self.handle))
+
+    # -- whole run -----------------------------------------------------------
+    def run(self, f: torch.Tensor, fhat: torch.Tensor, g: torch.Tensor, stream=None):
+        """pmsz_run_correction; returns (status, PmszResult, history list)."""
+        cap = self.max_iterations
+        hist = (ctypes.c_int64 * cap)()
+        res = N.PmszResult()
+        st = self.lib.pmsz_run_correction(self.handle, N.ptr(f), N.ptr(fhat), N.ptr(g), hist, cap,
+                                          ctypes.byref(res), N.stream_handle(stream))
+        n_hist = min(int(res.iterations), cap)
+        return st, res, [int(hist[i]) for i in range(n_hist)]
+
+    def export_edits(self, g: torch.Tensor, stream=None) -> tuple[torch.Tensor, torch.Tensor]:
+        cnt = ctypes.c_int64()
+        N.check(self.lib.pmsz_edits_export(self.handle, N.ptr(g), None, None, 0, ctypes.byref(cnt),
+                                           N.stream_handle(stream)), "pmsz_edits_export")
+        m = int(cnt.value)
+        ids = torch.empty(m, dtype=torch.int64, device=g.device)
+        vals = torch.empty(m, dtype=torch.float64, device=g.device)
+        if m:
+            N.check(self.lib.pmsz_edits_export(self.handle, N.ptr(g), N.ptr(ids), N.ptr(vals), m,
+                                               ctypes.byref(cnt), N.stream_handle(stream)),
+                    "pmsz_edits_export")
+        return ids, vals
+
+    # -- stepwise (block engine) ---------------------------------------------
+    def prepare(self, f, fhat, g, stream=None) -> N.PmszResult:
+        res = N.PmszResult()
+        st = self.lib.pmsz_prepare(self.handle, N.ptr(f), N.ptr(fhat), N.ptr(g), ctypes.byref(res),
+                                   N.stream_handle(stream))
+        return st, res
+
+    def iterate(self, f, g, edited_mask=None, stream=None):
+        res = N.PmszResult()
+        st = self.lib.pmsz_iterate(self.handle, N.ptr(f), N.ptr(g),
+                                   N.ptr(edited_mask) if edited_mask is not None else None,
+                                   ctypes.byref(res), N.stream_handle(stream))
+        return st, res
+
+    def block_round(self, f, g, lockstep: bool, stream=None):
+        res = N.PmszResult()
+        e = ctypes.c_int64()
+        st = self.lib.pmsz_block_round(self.handle, N.ptr(f), N.ptr(g), int(bool(lockstep)),
+                                       ctypes.byref(e), ctypes.byref(res), N.stream_handle(stream))
+        return st, int(e.value), res
+
+    def verify(self, g, stream=None):
+        res = N.PmszResult()
+        st = self.lib.pmsz_verify(self.handle, N.ptr(g), ctypes.byref(res), N.stream_handle(stream))
+        N.check(st, "pmsz_verify")
+        return [int(res.residual[k]) for k in range(6)]
+
+    def bounds_violations(self, f, g, stream=None) -> int:
+        out = ctypes.c_int64()
+        N.check(self.lib.pmsz_bounds_violations(self.handle, N.ptr(f), N.ptr(g), ctypes.byref(out),
+                                                N.stream_handle(stream)), "pmsz_bounds_violations")
+        return int(out.value)
+
+    def mark_all_dirty(self):
+        N.check(self.lib.pmsz_mark_all_dirty(self.handle, None), "pmsz_mark_all_dirty")
+
+    def mark_box_changed(self, lo, hi, before: torch.Tensor, g: torch.Tensor, stream=None):
+        N.check(self.lib.pmsz_box_mark_changed(self.handle, N.ivec(lo), N.ivec(hi), N.ptr(before),
+                                               N.ptr(g), N.stream_handle(stream)),
+                "pmsz_box_mark_changed")
+
+
+def raise_for(status: int, res: N.PmszResult, f_host_values=None, fhat_host_values=None,
+              xi: float | None = None, f_dev=None, fhat_dev=None):
+    """Map a pmsz_status to the reference's exception (correction.py:33-60,417-429)."""
+    if status == N.PMSZ_OK:
+        return
+    msg = N.last_error()
+    if status == N.PMSZ_ERR_BOUND:
+        i = int(res.bound_first_index)
+        if f_host_values is not None:
+            fo, fd = f_host_values[i], fhat_host_values[i]
+        else:
+            fo, fd = float(f_dev[i].item()), float(fhat_dev[i].item())
+        raise BoundViolationError(i, fo, fd, xi, int(res.bound_violations))
+    if status == N.PMSZ_ERR_MONOTONE:
+        raise AssertionError("edit raised a value; monotonicity broken")
+    if status == N.PMSZ_ERR_CONVERGENCE:
+        raise ConvergenceError(msg)
+    if status in (N.PMSZ_ERR_INVALID, N.PMSZ_ERR_NONFINITE):
+        raise ValueError(msg)
+    raise RuntimeError(f"pMSz device failure (status {status}): {msg}")
+
+
+def default_cap(xi: float, tau: float) -> int:
+    return 10 * math.ceil(2.0 * xi / tau)
+
+
+def as_device_f64(values: np.ndarray, device) -> torch.Tensor:
+    """Host f64 array -> device tensor without an extra host copy (the source
+    may be a frozen ScalarField array; it is only read)."""
+    import warnings
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore", UserWarning)
+        return torch.from_numpy(np.ascontiguousarray(values, dtype=np.float64)).to(device)

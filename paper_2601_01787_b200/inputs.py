@@ -1,0 +1,112 @@
+"""Synthetic benchmark inputs generated on the GPU.
+
+* ``perlin`` -- synth.perlin (synth.py:83-100), bit-exact (kernel built with
+  --fmad=false, same evaluation order); the permutation table is
+  synth._permutation (RandomState(seed).permutation(256), synth.py:33-37),
+  computed here on the host with NumPy exactly as the reference does.
+* ``quantize`` -- quantizer.quantize (quantizer.py:122-154), the bounded-error
+  stand-in for SZ3.
+* ``bounded_noise`` -- BASELINE config 1's seeded bounded-noise decompressed
+  field (no reference counterpart; the oracle restates the same hash).
+* ``relative_to_absolute`` -- quantizer.py:99-113 from a device min/max.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as N
+
+
+@dataclass(frozen=True)
+class NoiseSpec:
+    dims: tuple[int, int, int]
+    seed: int
+    frequency: float = 4.0
+    octaves: int = 3
+
+    def __post_init__(self):
+        d = tuple(int(v) for v in self.dims)
+        object.__setattr__(self, "dims", d if len(d) == 3 else (d[0], d[1], 1))
+        if self.octaves < 1:
+            raise ValueError("octaves must be >= 1")
+        if not self.frequency > 0:
+            raise ValueError("frequency must be positive")
+
+
+def permutation_table(seed: int) -> np.ndarray:
+    table = np.random.RandomState(seed & 0xFFFFFFFF).permutation(256)
+    return np.concatenate([table, table]).astype(np.int32)
+
+
+def perlin_device(spec: NoiseSpec, *, lo=(0, 0, 0), ext=None, f32: bool = False,
+                  device=None) -> torch.Tensor:
+    """Perlin values of the sub-box [lo, lo+ext) of the global grid spec.dims
+    (float64, or float32 = the reference's f32 cast)."""
+    ext = tuple(spec.dims) if ext is None else tuple(int(v) for v in ext)
+    dev = device or torch.device("cuda", torch.cuda.current_device())
+    n = ext[0] * ext[1] * ext[2]
+    out = torch.empty(n, dtype=torch.float32 if f32 else torch.float64, device=dev)
+    perm = permutation_table(spec.seed)
+    permp = perm.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+    N.check(N.lib().pmsz_perlin(N.ivec(spec.dims), N.ivec(lo), N.ivec(ext), permp,
+                                float(spec.frequency), int(spec.octaves),
+                                None if f32 else N.ptr(out), N.ptr(out) if f32 else None,
+                                N.stream_handle()), "pmsz_perlin")
+    return out
+
+
+def minmax_device(values: torch.Tensor) -> tuple[float, float]:
+    mn, mx = ctypes.c_double(), ctypes.c_double()
+    N.check(N.lib().pmsz_minmax(N.ptr(values), int(values.dtype == torch.float32), values.numel(),
+                                ctypes.byref(mn), ctypes.byref(mx), N.stream_handle()), "pmsz_minmax")
+    return float(mn.value), float(mx.value)
+
+
+def relative_to_absolute_range(lo: float, hi: float, eb_rel: float) -> float:
+    """quantizer.relative_to_absolute (quantizer.py:99-113) given min/max."""
+    if not (eb_rel > 0 and np.isfinite(eb_rel)):
+        raise ValueError(f"relative error bound must be positive, got {eb_rel}")
+    if hi > lo:
+        return eb_rel * (hi - lo)
+    if hi != 0.0:
+        return eb_rel * abs(hi)
+    raise ValueError("relative bound undefined for an all-zero field")
+
+
+def relative_to_absolute_device(values: torch.Tensor, eb_rel: float) -> float:
+    lo, hi = minmax_device(values)
+    return relative_to_absolute_range(lo, hi, eb_rel)
+
+
+def quantize_device(f: torch.Tensor, xi: float, origin: float | None = None,
+                    fmax: float | None = None) -> torch.Tensor:
+    """Reconstructed field of quantizer.quantize (float64 tensor)."""
+    if not (xi > 0 and np.isfinite(xi)):
+        raise ValueError(f"absolute error bound must be positive, got {xi}")
+    if origin is None or fmax is None:
+        origin, fmax = minmax_device(f)
+    if (fmax - origin) / (2.0 * xi) > 2.0 ** 53:
+        raise ValueError("error bound too small for the field's value range")
+    out = torch.empty(f.numel(), dtype=torch.float64, device=f.device)
+    mc = ctypes.c_int64()
+    st = N.lib().pmsz_quantize(N.ptr(f), int(f.dtype == torch.float32), f.numel(), float(origin),
+                               float(xi), N.ptr(out), ctypes.byref(mc), N.stream_handle())
+    if st != N.PMSZ_OK:
+        raise AssertionError(N.last_error())
+    return out
+
+
+def bounded_noise_device(f: torch.Tensor, dims, xi: float, seed: int, *, gdims=None,
+                         lo=(0, 0, 0)) -> torch.Tensor:
+    nx, ny, nz = dims
+    gd = tuple(gdims) if gdims is not None else (nx, ny, nz)
+    out = torch.empty(f.numel(), dtype=torch.float64, device=f.device)
+    N.check(N.lib().pmsz_bounded_noise(N.ptr(f), int(f.dtype == torch.float32), nx, ny, nz,
+                                       N.ivec(gd), N.ivec(lo), float(xi), int(seed) & (2**64 - 1),
+                                       N.ptr(out), N.stream_handle()), "pmsz_bounded_noise")
+    return out

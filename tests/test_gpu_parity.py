@@ -1,0 +1,247 @@
+"""GPU parity: the sm_100a kernels against the reference's golden outputs and
+the CPU oracle on identical inputs.  Bit-exact throughout (integer/index work
+and f64 compare/subtract only)."""
+
+import hashlib
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2601_01787_b200 as pm
+from conftest import golden_inputs
+from oracle import oracle as orc
+from paper_2601_01787_b200 import _native as N
+from paper_2601_01787_b200 import inputs as gen
+from paper_2601_01787_b200.topology import scan_codes_device
+
+pytestmark = pytest.mark.gpu
+
+DEV = "cuda"
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def sf(dims, v):
+    return pm.ScalarField(dims, v)
+
+
+def test_scan_bit_exact_against_reference(golden):
+    meta, arrays = golden
+    for case in meta["scans"]:
+        k = case["key"]
+        s = pm.scan_neighbors(arrays[k + "_v"], case["dims"])
+        assert np.array_equal(s.nmax, arrays[k + "_nmax"]), k
+        assert np.array_equal(s.nmin, arrays[k + "_nmin"]), k
+        assert np.array_equal(s.is_max, arrays[k + "_ismax"]), k
+        assert np.array_equal(s.is_min, arrays[k + "_ismin"]), k
+
+
+@pytest.mark.parametrize("dims", [(64, 48, 40), (33, 17, 9), (128, 128, 1), (5, 300, 3)])
+def test_codes_bit_exact_against_oracle(dims):
+    rng = np.random.default_rng(sum(dims))
+    n = int(np.prod(dims))
+    for v in (rng.standard_normal(n), rng.integers(0, 3, n).astype(np.float64),
+              orc.quantize(orc.perlin(dims, 5), 0.01)):
+        code = scan_codes_device(torch.from_numpy(v).to(DEV), dims).cpu().numpy()
+        assert np.array_equal(code, orc.codes(v, dims))
+
+
+@pytest.mark.parametrize("incremental", [True, False])
+def test_run_correction_matches_reference(golden, incremental):
+    meta, arrays = golden
+    for run in meta["runs"]:
+        f, fh, dims = golden_inputs(run, arrays)
+        cfg = pm.CorrectionConfig(xi_abs=run["xi"], tau=run["tau"], max_outer_iterations=run["cap"])
+        res = pm.run_correction(sf(dims, f), sf(dims, fh), cfg, incremental=incremental)
+        assert res.iterations == run["iterations"], run["name"]
+        assert list(res.edits_per_iteration) == run["edits_per_iteration"], run["name"]
+        assert res.max_vertex_edits == run["max_vertex_edits"], run["name"]
+        assert sha(res.corrected.values) == run["corrected_sha256"], run["name"]
+        assert np.array_equal(res.edits.ids, arrays[run["name"] + "_ids"])
+        assert np.array_equal(res.edits.values, arrays[run["name"] + "_vals"])
+        assert res.verification.is_clean
+
+
+def test_golden_edits_file(golden):
+    meta, arrays = golden
+    run = next(r for r in meta["runs"] if r["name"] == "golden8")
+    f, fh, dims = golden_inputs(run, arrays)
+    res = pm.run_correction(sf(dims, f), sf(dims, fh), pm.CorrectionConfig(xi_abs=run["xi"]))
+    blob = pm.encode_edits(res.edits, run["xi"], run["tau"])
+    assert hashlib.sha256(blob).hexdigest() == meta["golden_edits_sha256"]
+
+
+def test_iterate_trajectory_matches_reference(golden):
+    meta, _ = golden
+    for case in meta["iterate"]:
+        dims = (8, 8, 8)
+        f = orc.perlin(dims, case["seed"])
+        g = orc.quantize(f, case["xi"])
+        for step in case["trajectory"]:
+            g, ed = pm.iterate_array(dims, f, g, case["xi"], case["tau"])
+            assert int(ed.sum()) == step["edits"]
+            assert sha(g) == step["g_sha256"]
+            assert sha(ed) == step["edited_sha256"]
+
+
+def test_bound_violation_error(golden):
+    meta, arrays = golden
+    bv = meta["bound_violation"]
+    with pytest.raises(pm.BoundViolationError) as err:
+        pm.run_correction(sf((8, 8), arrays["bound_f"]), sf((8, 8), arrays["bound_fhat"]),
+                          pm.CorrectionConfig(xi_abs=bv["xi"]))
+    assert err.value.index == bv["index"] and err.value.offenders == bv["offenders"]
+    assert err.value.original == arrays["bound_f"][bv["index"]]
+
+
+def test_iteration_cap_raises_convergence_error(golden):
+    f = orc.perlin((8, 8, 8), 42)
+    xi = orc.relative_to_absolute(f, 1e-1)
+    with pytest.raises(pm.ConvergenceError):
+        pm.run_correction(sf((8, 8, 8), f), sf((8, 8, 8), orc.quantize(f, xi)),
+                          pm.CorrectionConfig(xi_abs=xi, max_outer_iterations=3))
+
+
+# --- hand-built KATs (test_correction.py:15-43, test_parallel.py:21-31) -------
+DESC_F = [0.15, 0.10, 0.40, 0.50, 0.60, 0.70, 0.90, 0.80, 0.95]
+DESC_G = [0.08, 0.10, 0.40, 0.50, 0.60, 0.70, 0.90, 0.80, 0.95]
+ASC_F = [0.02, 0.08, 0.12, 0.00, 0.20, 0.30, 0.05, 0.10, 0.25]
+ASC_G = [0.02, 0.08, 0.12, 0.00, 0.20, 0.30, 0.05, 0.10, 0.40]
+
+
+def test_kat_desc_clamps_to_lower():
+    g1, ed = pm.iterate_array((3, 3), np.array(DESC_F), np.array(DESC_G), 0.1, 0.1)
+    assert ed.tolist() == [False, True] + [False] * 7
+    assert g1[1] == 0.0
+    res = pm.run_correction(sf((3, 3), DESC_F), sf((3, 3), DESC_G), pm.CorrectionConfig(xi_abs=0.1, tau=0.1))
+    assert res.edits.count == 1 and res.iterations == 2
+
+
+def test_kat_asc_hits_proposal():
+    g1, ed = pm.iterate_array((3, 3), np.array(ASC_F), np.array(ASC_G), 0.3, 0.05)
+    assert np.flatnonzero(ed).tolist() == [8]
+    assert g1[8] == 0.30 - 0.05
+    res = pm.run_correction(sf((3, 3), ASC_F), sf((3, 3), ASC_G), pm.CorrectionConfig(xi_abs=0.3, tau=0.05))
+    assert res.edits.count == 1 and res.iterations == 2
+
+
+def ramp_with_dip():
+    xs = np.arange(8, dtype=np.float64)
+    ys = 0.1 * np.arange(4, dtype=np.float64)
+    f = (xs[None, :] + ys[:, None]).reshape(-1)
+    g = f.copy()
+    g[5] = 2.5
+    return sf((8, 4), f), sf((8, 4), g), pm.CorrectionConfig(xi_abs=3.0, tau=0.25)
+
+
+def test_kat_cross_block_repair():
+    f, g, cfg = ramp_with_dip()
+    res = pm.run_correction(f, g, cfg)
+    assert res.edits.ids.tolist() == [3, 4] and res.iterations == 2
+    assert res.corrected.values[3] == 2.5 - 0.25
+    r2, st = pm.run_parallel(f, g, cfg, (2, 1, 1), pm.SyncStrategy.RELAXED)
+    assert np.array_equal(r2.corrected.values, res.corrected.values)
+    assert (st.rounds, st.syncs, st.per_block_edit_totals) == (2, 1, (0, 2))
+    r3, st3 = pm.run_parallel(f, g, cfg, (2, 1, 1), pm.SyncStrategy.LOCKSTEP)
+    assert np.array_equal(r3.corrected.values, res.corrected.values)
+    assert (st3.rounds, st3.syncs) == (2, 2)
+
+
+def test_identity_input_is_one_clean_iteration():
+    f = orc.perlin((8, 8, 4), 3)
+    res = pm.run_correction(sf((8, 8, 4), f), sf((8, 8, 4), f), pm.CorrectionConfig(xi_abs=0.05))
+    assert res.edits.count == 0 and res.iterations == 1 and res.edits_per_iteration == (0,)
+
+
+@pytest.mark.parametrize("idx", range(18))
+def test_run_parallel_matches_reference(golden, idx):
+    meta, _ = golden
+    case = meta["parallel"][idx]
+    dims = tuple(case["dims"])
+    f = orc.perlin(dims, case["seed"])
+    fh = orc.quantize(f, case["xi"])
+    res, st = pm.run_parallel(sf(dims, f), sf(dims, fh), pm.CorrectionConfig(xi_abs=case["xi"]),
+                              tuple(case["grid"]), pm.SyncStrategy(case["strategy"]))
+    d = st.to_dict()
+    d.pop("timings")
+    ref = dict(case["stats"])
+    assert d == ref, case["name"]
+    assert res.edits_per_iteration == tuple(case["edits_per_iteration"])
+    assert res.iterations == case["iterations"] and res.max_vertex_edits == case["max_vertex_edits"]
+    assert sha(res.corrected.values) == case["corrected_sha256"], case["name"]
+
+
+# --- input generators --------------------------------------------------------
+def test_perlin_and_quantize_bit_exact(golden):
+    meta, _ = golden
+    for p in meta["perlin"]:
+        spec = gen.NoiseSpec(tuple(p["dims"]) if len(p["dims"]) == 3 else (*p["dims"], 1), p["seed"],
+                             p["frequency"], p["octaves"])
+        f = gen.perlin_device(spec)
+        assert sha(f.cpu().numpy()) == p["sha256"]
+        f32 = gen.perlin_device(spec, f32=True)
+        assert sha(f32.cpu().numpy()) == p["f32_sha256"]
+        xi = gen.relative_to_absolute_device(f, 1e-3)
+        assert xi == p["xi_rel_1e-3"]
+        assert sha(gen.quantize_device(f, xi).cpu().numpy()) == p["quantized_sha256"]
+
+
+def test_perlin_sub_box_and_noise_match_oracle():
+    dims = (40, 36, 30)
+    spec = gen.NoiseSpec(dims, 8)
+    part = gen.perlin_device(spec, lo=(5, 7, 3), ext=(20, 11, 9)).cpu().numpy()
+    assert np.array_equal(part, orc.perlin(dims, 8, lo=(5, 7, 3), ext=(20, 11, 9)))
+    f = gen.perlin_device(spec, f32=True)
+    xi = gen.relative_to_absolute_device(f, 1e-3)
+    fh = gen.bounded_noise_device(f, dims, xi, 5).cpu().numpy()
+    assert np.array_equal(fh, orc.bounded_noise(f.cpu().numpy().astype(np.float64), dims, xi, 5))
+
+
+# --- larger sizes against the oracle -----------------------------------------
+@pytest.mark.parametrize("n,rel,noise", [(96, 1e-3, True), (128, 1e-4, False), (160, 1e-3, False)])
+def test_device_path_matches_oracle_at_scale(n, rel, noise):
+    dims = (n, n, n)
+    spec = gen.NoiseSpec(dims, 0)
+    f32 = gen.perlin_device(spec, f32=True)
+    xi = gen.relative_to_absolute_device(f32, rel)
+    fh = gen.bounded_noise_device(f32, dims, xi, 0) if noise else gen.quantize_device(f32, xi)
+    cfg = pm.CorrectionConfig(xi_abs=xi)
+    out = pm.run_correction_device(f32, fh, dims, cfg)
+    f_h = f32.cpu().numpy().astype(np.float64)
+    ref = orc.run_correction(dims, f_h, fh.cpu().numpy(), xi, check_segmentation=False)
+    assert ref.status == orc.ORC_OK
+    assert out.edits_per_iteration == ref.edits_per_iteration
+    assert out.max_vertex_edits == ref.max_vertex_edits
+    g = out.corrected.cpu().numpy()
+    assert np.array_equal(g, ref.corrected)
+    ids = np.flatnonzero(ref.corrected != fh.cpu().numpy())
+    assert np.array_equal(out.edit_ids.cpu().numpy(), ids)
+    assert np.array_equal(out.edit_values.cpu().numpy(), ref.corrected[ids])
+    assert np.abs(g - f_h).max() <= xi
+
+
+def test_plan_is_reusable_and_restores_invariants():
+    dims = (64, 64, 64)
+    f32 = gen.perlin_device(gen.NoiseSpec(dims, 2), f32=True)
+    xi = gen.relative_to_absolute_device(f32, 1e-3)
+    fh = gen.quantize_device(f32, xi)
+    cfg = pm.CorrectionConfig(xi_abs=xi)
+    a = pm.run_correction_device(f32, fh, dims, cfg)
+    b = pm.run_correction_device(f32, fh, dims, cfg)
+    assert torch.equal(a.corrected, b.corrected) and a.edits_per_iteration == b.edits_per_iteration
+    assert torch.equal(a.edit_ids, b.edit_ids)
+    # in place
+    g = fh.clone()
+    c = pm.run_correction_device(f32, g, dims, cfg, out=g)
+    assert torch.equal(c.corrected, a.corrected)
+
+
+def test_launches_are_counted():
+    before = N.launch_count()
+    f = orc.perlin((16, 16, 16), 1)
+    xi = orc.relative_to_absolute(f, 1e-2)
+    pm.run_correction(sf((16, 16, 16), f), sf((16, 16, 16), orc.quantize(f, xi)), pm.CorrectionConfig(xi_abs=xi))
+    assert N.launch_count() > before

@@ -1,0 +1,139 @@
+"""Pin the CPU oracle to the reference's own outputs (tests/golden, generated
+by make_golden.py from /root/reference).  CPU only."""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from conftest import golden_inputs
+from oracle import oracle as orc
+from paper_2601_01787_b200 import codec
+from paper_2601_01787_b200.correction import EditSet
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def test_scan_matches_reference(golden):
+    meta, arrays = golden
+    for case in meta["scans"]:
+        k = case["key"]
+        s = orc.scan(arrays[k + "_v"], case["dims"])
+        assert np.array_equal(s.nmax, arrays[k + "_nmax"]), k
+        assert np.array_equal(s.nmin, arrays[k + "_nmin"]), k
+        assert np.array_equal(s.is_max, arrays[k + "_ismax"]), k
+        assert np.array_equal(s.is_min, arrays[k + "_ismin"]), k
+
+
+def test_perlin_and_quantize_match_reference(golden):
+    meta, _ = golden
+    for p in meta["perlin"]:
+        f = orc.perlin(p["dims"], p["seed"], p["frequency"], p["octaves"])
+        assert sha(f) == p["sha256"], p
+        assert sha(f.astype(np.float32)) == p["f32_sha256"]
+        xi = orc.relative_to_absolute(f, 1e-3)
+        assert xi == p["xi_rel_1e-3"]
+        assert sha(orc.quantize(f, xi)) == p["quantized_sha256"]
+
+
+def test_perlin_sub_box_is_a_slice_of_the_whole():
+    dims = (20, 17, 9)
+    whole = orc.perlin(dims, 7).reshape(9, 17, 20)
+    part = orc.perlin(dims, 7, lo=(3, 5, 2), ext=(10, 6, 4)).reshape(4, 6, 10)
+    assert np.array_equal(part, whole[2:6, 5:11, 3:13])
+
+
+def test_iterate_trajectory_matches_reference(golden):
+    meta, _ = golden
+    for case in meta["iterate"]:
+        dims = (8, 8, 8)
+        f = orc.perlin(dims, case["seed"])
+        fh = orc.quantize(f, case["xi"])
+        fs = orc.scan(f, dims)
+        g = fh
+        for step in case["trajectory"]:
+            g, ed = orc.iterate(dims, fs, g, f - case["xi"], case["tau"])
+            assert int(ed.sum()) == step["edits"]
+            assert sha(g) == step["g_sha256"]
+            assert sha(ed) == step["edited_sha256"]
+
+
+def test_run_correction_matches_reference(golden):
+    meta, arrays = golden
+    for run in meta["runs"]:
+        f, fh, dims = golden_inputs(run, arrays)
+        assert sha(f) == run["f_sha256"] and sha(fh) == run["fhat_sha256"], run["name"]
+        r = orc.run_correction(dims, f, fh, run["xi"], run["tau"], run["cap"])
+        assert r.status == orc.ORC_OK, run["name"]
+        assert r.iterations == run["iterations"]
+        assert list(r.edits_per_iteration) == run["edits_per_iteration"]
+        assert r.max_vertex_edits == run["max_vertex_edits"]
+        assert sha(r.corrected) == run["corrected_sha256"], run["name"]
+        ids = np.flatnonzero(r.corrected != fh)
+        assert np.array_equal(ids, arrays[run["name"] + "_ids"])
+        assert np.array_equal(r.corrected[ids], arrays[run["name"] + "_vals"])
+
+
+def test_failure_modes_match_reference(golden):
+    meta, arrays = golden
+    bv = meta["bound_violation"]
+    r = orc.run_correction((8, 8, 1), arrays["bound_f"], arrays["bound_fhat"], bv["xi"])
+    assert r.status == orc.ORC_BOUND
+    assert (r.bound_first, r.bound_count) == (bv["index"], bv["offenders"])
+    f = orc.perlin((8, 8, 8), 42)
+    xi = orc.relative_to_absolute(f, 1e-1)
+    r = orc.run_correction((8, 8, 8), f, orc.quantize(f, xi), xi, max_iter=meta["cap_error"]["cap"])
+    assert r.status == orc.ORC_CONVERGENCE and r.conv_kind == 1
+
+
+def test_golden_edits_file_hash(golden):
+    meta, arrays = golden
+    run = next(r for r in meta["runs"] if r["name"] == "golden8")
+    edits = EditSet(arrays["golden8_ids"], arrays["golden8_vals"], 512)
+    blob = codec.encode_edits(edits, run["xi"], run["tau"])
+    assert hashlib.sha256(blob).hexdigest() == meta["golden_edits_sha256"]
+    back, xi, tau = codec.decode_edits_meta(blob)
+    assert np.array_equal(back.ids, edits.ids) and np.array_equal(back.values, edits.values)
+    assert (xi, tau) == (run["xi"], run["tau"])
+
+
+def test_edits_codec_large_ids_round_trip():
+    rng = np.random.default_rng(0)
+    ids = np.unique(rng.integers(0, 2**40, 5000))
+    e = EditSet(ids, rng.standard_normal(ids.size), 2**41)
+    back = codec.decode_edits(codec.encode_edits(e, 0.1, 0.001))
+    assert np.array_equal(back.ids, e.ids) and np.array_equal(back.values, e.values)
+    with pytest.raises(codec.FormatError):
+        codec.decode_edits(codec.encode_edits(e, 0.1, 0.001)[:-1] + b"\x00")
+
+
+@pytest.mark.parametrize("idx", range(18))
+def test_run_parallel_matches_reference(golden, idx):
+    meta, arrays = golden
+    case = meta["parallel"][idx]
+    dims = tuple(case["dims"])
+    f = orc.perlin(dims, case["seed"])
+    fh = orc.quantize(f, case["xi"])
+    g, st = orc.run_parallel(dims, f, fh, case["xi"], tuple(case["grid"]), case["strategy"] == "lockstep")
+    ref = case["stats"]
+    assert st["rounds"] == ref["rounds"] and st["syncs"] == ref["syncs"]
+    assert list(st["per_block_iterations"]) == ref["per_block_iterations"]
+    assert list(st["per_block_edit_totals"]) == ref["per_block_edit_totals"]
+    assert list(st["per_block_max_vertex_edits"]) == ref["per_block_max_vertex_edits"]
+    assert list(st["edits_per_iteration"]) == case["edits_per_iteration"]
+    assert sha(g) == case["corrected_sha256"], case["name"]
+
+
+def test_bounded_noise_respects_bound_and_floor():
+    dims = (16, 12, 8)
+    f = orc.perlin(dims, 3).astype(np.float32).astype(np.float64)
+    xi = orc.relative_to_absolute(f, 1e-3)
+    fh = orc.bounded_noise(f, dims, xi, 11)
+    assert np.all(np.abs(f - fh) <= xi)
+    assert np.all(fh >= f - xi)
+    assert not np.array_equal(fh, f)
+    part = orc.bounded_noise(f.reshape(8, 12, 16)[2:5, 1:7, 4:9].reshape(-1), (5, 6, 3), xi, 11,
+                             gdims=dims, lo=(4, 1, 2))
+    assert np.array_equal(part, fh.reshape(8, 12, 16)[2:5, 1:7, 4:9].reshape(-1))
