@@ -111,11 +111,22 @@ const char* pmsz_version(void);
 /* Number of kernel launches issued by this library since load (evidence for bench). */
 int64_t pmsz_launch_count(void);
 
+/* Kernel classes for pmsz_profile_read. */
+enum {
+    PMSZ_K_PREP = 0, PMSZ_K_SWEEP_FULL = 1, PMSZ_K_SWEEP_SPARSE = 2, PMSZ_K_APPLY = 3,
+    PMSZ_K_VERIFY = 4, PMSZ_K_COMPACT = 5, PMSZ_K_OTHER = 6, PMSZ_K_COUNT = 8
+};
+
 /* ---- plans -------------------------------------------------------------- */
 pmsz_status pmsz_plan_create(const pmsz_desc* desc, pmsz_plan** out);
 void pmsz_plan_destroy(pmsz_plan* plan);
 /* Device bytes of scratch owned by the plan. */
 int64_t pmsz_plan_scratch_bytes(const pmsz_plan* plan);
+/* Time every kernel launch of this plan with CUDA events on its stream
+ * (enable != 0).  pmsz_profile_read returns the accumulated device time (ms)
+ * and launch count per kernel class (arrays of PMSZ_K_COUNT) and optionally resets. */
+pmsz_status pmsz_profile(pmsz_plan* plan, int32_t enable);
+pmsz_status pmsz_profile_read(pmsz_plan* plan, double* ms, int64_t* launches, int32_t reset);
 
 /*
  * run_correction (correction.py:391-436) on device-resident buffers.

@@ -402,11 +402,14 @@ void orc_perlin(const int64_t* gdims, const int64_t* lo, const int64_t* ext, con
     }
 }
 
-/* quantize (quantizer.py:122-154); returns 0, or -1 if the self-check fails. */
-int orc_quantize(const double* f, int64_t n, double xi, double* recon) {
+/* quantize (quantizer.py:122-154); returns 0, or -1 if the self-check fails.
+ * origin = min(f) unless use_origin (a sub-box of a larger field passes the
+ * whole field's minimum so the sample equals the slice of the whole). */
+int orc_quantize(const double* f, int64_t n, double xi, double origin_in, int use_origin, double* recon) {
     double origin = f[0];
     for (int64_t i = 1; i < n; ++i)
         if (f[i] < origin) origin = f[i];
+    if (use_origin) origin = origin_in;
     const double two_xi = 2.0 * xi;
     int bad = 0;
 #pragma omp parallel for reduction(| : bad) schedule(static)

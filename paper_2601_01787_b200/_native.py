@@ -28,6 +28,10 @@ PMSZ_CONV_CAP = 1
 PMSZ_CONV_BOUND = 2
 PMSZ_CONV_RESIDUAL = 3
 
+K_PREP, K_SWEEP_FULL, K_SWEEP_SPARSE, K_APPLY, K_VERIFY, K_COMPACT, K_OTHER = range(7)
+K_COUNT = 8
+K_NAMES = ("prep", "sweep_full", "sweep_sparse", "apply", "verify", "compact", "other")
+
 FLAG_INCREMENTAL = 1
 FLAG_EXTREMA_ONLY = 2
 FLAG_F32_ORIGINAL = 4
@@ -70,6 +74,8 @@ SIGNATURES = {
     "pmsz_plan_create": (i32, [ctypes.POINTER(PmszDesc), ctypes.POINTER(vp)]),
     "pmsz_plan_destroy": (None, [vp]),
     "pmsz_plan_scratch_bytes": (i64, [vp]),
+    "pmsz_profile": (i32, [vp, i32]),
+    "pmsz_profile_read": (i32, [vp, dp, i64p, i32]),
     "pmsz_run_correction": (i32, [vp, vp, vp, vp, i64p, i64, ctypes.POINTER(PmszResult), vp]),
     "pmsz_run_correction_host": (i32, [vp, vp, vp, vp, vp, vp, i64, i64p, i64,
                                        ctypes.POINTER(PmszResult), vp]),

@@ -340,6 +340,12 @@ struct pmsz_plan {
     // block-round bookkeeping
     int64_t iterations = 0, edit_total = 0;
     int f32 = 0;
+    // live kernel timing (pmsz_profile)
+    bool prof_on = false;
+    std::vector<cudaEvent_t> prof_ev;   // pairs
+    std::vector<int> prof_cls;          // class per recorded pair
+    double prof_ms[PMSZ_K_COUNT] = {};
+    long long prof_n[PMSZ_K_COUNT] = {};
 };
 
 namespace {
@@ -357,9 +363,47 @@ Dom make_dom(const pmsz_desc& d) {
     return o;
 }
 
+// ---- live kernel timing: an event pair around every launch of a plan --------
+int prof_begin(pmsz_plan* p, cudaStream_t s) {
+    if (!p->prof_on) return -1;
+    const size_t k = p->prof_cls.size();
+    while (p->prof_ev.size() < 2 * (k + 1)) {
+        cudaEvent_t e;
+        if (cudaEventCreate(&e) != cudaSuccess) return -1;
+        p->prof_ev.push_back(e);
+    }
+    cudaEventRecord(p->prof_ev[2 * k], s);
+    return (int)k;
+}
+
+void prof_end(pmsz_plan* p, cudaStream_t s, int tok, int cls) {
+    if (tok < 0) return;
+    cudaEventRecord(p->prof_ev[2 * tok + 1], s);
+    p->prof_cls.push_back(cls);
+}
+
+// Called once the stream is known to be idle.
+void prof_flush(pmsz_plan* p) {
+    for (size_t k = 0; k < p->prof_cls.size(); ++k) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, p->prof_ev[2 * k], p->prof_ev[2 * k + 1]) == cudaSuccess) {
+            p->prof_ms[p->prof_cls[k]] += ms;
+            p->prof_n[p->prof_cls[k]] += 1;
+        }
+    }
+    p->prof_cls.clear();
+}
+
+struct ProfScope {
+    pmsz_plan* p; cudaStream_t s; int tok; int cls;
+    ProfScope(pmsz_plan* p_, cudaStream_t s_, int cls_) : p(p_), s(s_), tok(prof_begin(p_, s_)), cls(cls_) {}
+    ~ProfScope() { prof_end(p, s, tok, cls); }
+};
+
 pmsz_status sync_counters(pmsz_plan* p, cudaStream_t s) {
     CUDA_TRY(cudaMemcpyAsync(p->hctr, p->ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
+    prof_flush(p);
     return PMSZ_OK;
 }
 
@@ -372,6 +416,7 @@ pmsz_status reset_iter(pmsz_plan* p, cudaStream_t s, int nxt) {
 
 template <typename FT>
 pmsz_status launch_apply(pmsz_plan* p, const void* f, double* g, cudaStream_t s, int nxt) {
+    ProfScope ps(p, s, PMSZ_K_APPLY);
     k_apply<FT><<<grid_for(p->n, 256, 16), 256, 0, s>>>(p->dom, (const FT*)f, g, p->w, nxt);
     LAUNCHED();
     return PMSZ_OK;
@@ -387,11 +432,13 @@ pmsz_status iterate_once(pmsz_plan* p, const void* f, double* g, cudaStream_t s)
         if (p->w.incremental) CUDA_TRY(cudaMemsetAsync(p->w.actbits, 0, p->nwords * 4, s));
         const int64_t cx = d.hi[0] - d.lo[0], cy = d.hi[1] - d.lo[1], cz = d.hi[2] - d.lo[2];
         if (cx > 0 && cy > 0 && cz > 0) {
+            ProfScope ps(p, s, PMSZ_K_SWEEP_FULL);
             launch_sweep_full<false>(d, g, p->w, s);
             LAUNCHED();
         }
         p->last_full = true;
     } else {
+        ProfScope ps(p, s, PMSZ_K_SWEEP_SPARSE);
         k_sweep_sparse<<<grid_for(p->w.act_cap, 256, 16), 256, 0, s>>>(d, g, p->w, p->cur);
         LAUNCHED();
         p->last_full = false;
@@ -438,10 +485,12 @@ pmsz_status prep(pmsz_plan* p, const void* f, const double* fh, double* g, cudaS
     const Dom& d = p->dom;
     dim3 block(32, 8, 1);
     dim3 grid((unsigned)((d.nx + 31) / 32), (unsigned)((d.ny + 7) / 8), (unsigned)d.nz);
+    ProfScope* ps = new ProfScope(p, s, PMSZ_K_PREP);
     if (p->f32)
         k_prep<float><<<grid, block, 0, s>>>(d, (const float*)f, fh, g, p->w.code, p->ctr);
     else
         k_prep<double><<<grid, block, 0, s>>>(d, (const double*)f, fh, g, p->w.code, p->ctr);
+    delete ps;
     LAUNCHED();
     CUDA_TRY(cudaGetLastError());
     st = sync_counters(p, s);
@@ -457,6 +506,7 @@ pmsz_status verify_sweep(pmsz_plan* p, const double* g, cudaStream_t s, int64_t 
     const Dom& d = p->dom;
     const int64_t cx = d.hi[0] - d.lo[0], cy = d.hi[1] - d.lo[1], cz = d.hi[2] - d.lo[2];
     if (cx > 0 && cy > 0 && cz > 0) {
+        ProfScope ps(p, s, PMSZ_K_VERIFY);
         launch_sweep_full<true>(d, g, p->w, s);
         LAUNCHED();
     }
@@ -469,10 +519,12 @@ pmsz_status verify_sweep(pmsz_plan* p, const double* g, cudaStream_t s, int64_t 
 
 pmsz_status count_bounds(pmsz_plan* p, const void* f, const double* g, cudaStream_t s, int64_t* out) {
     CUDA_TRY(cudaMemsetAsync(&p->ctr->scratch[1], 0, sizeof(unsigned long long), s));
+    ProfScope* ps = new ProfScope(p, s, PMSZ_K_OTHER);
     if (p->f32)
         k_bounds<float><<<grid_for(p->n, 256), 256, 0, s>>>(p->n, (const float*)f, g, p->dom.xi, &p->ctr->scratch[1]);
     else
         k_bounds<double><<<grid_for(p->n, 256), 256, 0, s>>>(p->n, (const double*)f, g, p->dom.xi, &p->ctr->scratch[1]);
+    delete ps;
     LAUNCHED();
     CUDA_TRY(cudaGetLastError());
     pmsz_status st = sync_counters(p, s);
@@ -482,9 +534,11 @@ pmsz_status count_bounds(pmsz_plan* p, const void* f, const double* g, cudaStrea
 }
 
 pmsz_status edit_count(pmsz_plan* p, cudaStream_t s, int64_t* count) {
+    ProfScope* ps = new ProfScope(p, s, PMSZ_K_COMPACT);
     k_bits_count<<<(unsigned)p->nblocks_compact, kCompactThreads, 0, s>>>(p->w.editbits, p->nwords, p->block_counts);
     LAUNCHED();
     k_exclusive_scan<<<1, 1024, 0, s>>>(p->block_counts, p->nblocks_compact, &p->ctr->scratch[2]);
+    delete ps;
     LAUNCHED();
     CUDA_TRY(cudaGetLastError());
     pmsz_status st = sync_counters(p, s);
@@ -572,7 +626,28 @@ void pmsz_plan_destroy(pmsz_plan* p) {
     cudaFree(p->w.code); cudaFree(p->ctr); cudaFree(p->block_counts);
     cudaFree(p->w.actbits); cudaFree(p->w.act[0]); cudaFree(p->w.act[1]);
     if (p->hctr) cudaFreeHost(p->hctr);
+    for (cudaEvent_t e : p->prof_ev) cudaEventDestroy(e);
     delete p;
+}
+
+pmsz_status pmsz_profile(pmsz_plan* p, int32_t enable) {
+    if (!p) return fail(PMSZ_ERR_INVALID, "null plan");
+    p->prof_on = enable != 0;
+    return PMSZ_OK;
+}
+
+pmsz_status pmsz_profile_read(pmsz_plan* p, double* ms, int64_t* launches, int32_t reset) {
+    if (!p) return fail(PMSZ_ERR_INVALID, "null plan");
+    if (!p->prof_cls.empty()) {
+        CUDA_TRY(cudaEventSynchronize(p->prof_ev[2 * (p->prof_cls.size() - 1) + 1]));
+        prof_flush(p);
+    }
+    for (int k = 0; k < PMSZ_K_COUNT; ++k) {
+        if (ms) ms[k] = p->prof_ms[k];
+        if (launches) launches[k] = p->prof_n[k];
+        if (reset) { p->prof_ms[k] = 0; p->prof_n[k] = 0; }
+    }
+    return PMSZ_OK;
 }
 
 int64_t pmsz_plan_scratch_bytes(const pmsz_plan* p) { return p ? p->scratch_bytes : 0; }
@@ -750,6 +825,7 @@ pmsz_status pmsz_edits_export(pmsz_plan* p, const double* g, int64_t* ids, doubl
     if (st) return st;
     if (count_out) *count_out = count;
     if (ids && vals && cap > 0 && count > 0) {
+        ProfScope ps(p, s, PMSZ_K_COMPACT);
         k_bits_write<<<(unsigned)p->nblocks_compact, kCompactThreads, 0, s>>>(p->w.editbits, p->nwords, p->n,
                                                                              p->block_counts, g, ids, vals, cap);
         LAUNCHED();

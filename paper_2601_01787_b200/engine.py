@@ -92,6 +92,15 @@ class DomainPlan:
         except Exception:
             pass
 
+    def profile(self, enable: bool = True):
+        N.check(self.lib.pmsz_profile(self.handle, int(bool(enable))), "pmsz_profile")
+
+    def profile_read(self, reset: bool = False) -> dict:
+        ms = (ctypes.c_double * N.K_COUNT)()
+        cnt = (ctypes.c_int64 * N.K_COUNT)()
+        N.check(self.lib.pmsz_profile_read(self.handle, ms, cnt, int(bool(reset))), "pmsz_profile_read")
+        return {name: (float(ms[k]), int(cnt[k])) for k, name in enumerate(N.K_NAMES)}
+
     @property
     def scratch_bytes(self) -> int:
         return int(self.lib.pmsz_plan_scratch_bytes(self.handle))
