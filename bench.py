@@ -230,7 +230,7 @@ def run_ours_single(args):
     # roofline of the dominant kernels (algorithmic bytes per launch / event time)
     peaks = measured_peaks()
     peak = float(peaks.get("hbm_gbs", 6650.0))
-    per_voxel = {"sweep_full": 9, "verify": 9, "prep": 4 + 8 + 8 + 1}
+    per_voxel = {"sweep_full": 9, "sweep_masked": 9, "verify": 9, "prep": 4 + 8 + 8 + 1}
     kernels = {}
     for name, (kms, cnt) in prof.items():
         if cnt == 0:
@@ -252,7 +252,8 @@ def run_ours_single(args):
     # correctness evidence of the timed run
     check = {"iterations": res.iterations, "edits_per_iteration": list(res.edits_per_iteration),
              "edit_count": int(res.edit_ids.numel()), "max_vertex_edits": res.max_vertex_edits,
-             "full_sweeps": res.full_sweeps, "sparse_sweeps": res.sparse_sweeps, "residual": 0}
+             "full_sweeps": res.full_sweeps, "masked_sweeps": res.masked_sweeps,
+             "sparse_sweeps": res.sparse_sweeps, "residual": 0}
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",

@@ -102,6 +102,7 @@ typedef struct {
     int64_t shared_dirty;          /* block mode: an edit touched a replicated vertex */
     int64_t last_edits;            /* edits of the last iteration */
     int64_t last_detections;       /* centres with a detection in the last iteration */
+    int64_t masked_sweeps;         /* tiled sweeps restricted to a dilated dirty bitmap */
 } pmsz_result;
 
 /* Error string of the last failing call on this thread. */
@@ -114,7 +115,8 @@ int64_t pmsz_launch_count(void);
 /* Kernel classes for pmsz_profile_read. */
 enum {
     PMSZ_K_PREP = 0, PMSZ_K_SWEEP_FULL = 1, PMSZ_K_SWEEP_SPARSE = 2, PMSZ_K_APPLY = 3,
-    PMSZ_K_VERIFY = 4, PMSZ_K_COMPACT = 5, PMSZ_K_OTHER = 6, PMSZ_K_COUNT = 8
+    PMSZ_K_VERIFY = 4, PMSZ_K_COMPACT = 5, PMSZ_K_OTHER = 6, PMSZ_K_SWEEP_MASKED = 7, PMSZ_K_DEFER = 8,
+    PMSZ_K_COUNT = 10
 };
 
 /* ---- plans -------------------------------------------------------------- */

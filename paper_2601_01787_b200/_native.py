@@ -28,9 +28,10 @@ PMSZ_CONV_CAP = 1
 PMSZ_CONV_BOUND = 2
 PMSZ_CONV_RESIDUAL = 3
 
-K_PREP, K_SWEEP_FULL, K_SWEEP_SPARSE, K_APPLY, K_VERIFY, K_COMPACT, K_OTHER = range(7)
-K_COUNT = 8
-K_NAMES = ("prep", "sweep_full", "sweep_sparse", "apply", "verify", "compact", "other")
+K_PREP, K_SWEEP_FULL, K_SWEEP_SPARSE, K_APPLY, K_VERIFY, K_COMPACT, K_OTHER, K_SWEEP_MASKED, K_DEFER = range(9)
+K_COUNT = 10
+K_NAMES = ("prep", "sweep_full", "sweep_sparse", "apply", "verify", "compact", "other", "sweep_masked",
+           "defer", "spare")
 
 FLAG_INCREMENTAL = 1
 FLAG_EXTREMA_ONLY = 2
@@ -62,7 +63,7 @@ class PmszResult(ctypes.Structure):
         ("floor_violations", i64), ("nonfinite", i64),
         ("residual", i64 * 6), ("convergence_kind", i64),
         ("full_sweeps", i64), ("sparse_sweeps", i64), ("shared_dirty", i64),
-        ("last_edits", i64), ("last_detections", i64),
+        ("last_edits", i64), ("last_detections", i64), ("masked_sweeps", i64),
     ]
 
 

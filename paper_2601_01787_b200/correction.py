@@ -183,6 +183,7 @@ class DeviceCorrection:
     max_vertex_edits: int
     full_sweeps: int
     sparse_sweeps: int
+    masked_sweeps: int = 0
 
 
 _PLAN_CACHE: dict = {}
@@ -233,7 +234,8 @@ def run_correction_device(f: torch.Tensor, fhat: torch.Tensor, dims, config: Cor
     return DeviceCorrection(corrected=g, edit_ids=ids, edit_values=vals,
                             iterations=int(res.iterations), edits_per_iteration=tuple(hist),
                             max_vertex_edits=int(res.max_vertex_edits),
-                            full_sweeps=int(res.full_sweeps), sparse_sweeps=int(res.sparse_sweeps))
+                            full_sweeps=int(res.full_sweeps), sparse_sweeps=int(res.sparse_sweeps),
+                            masked_sweeps=int(res.masked_sweeps))
 
 
 def run_correction(original: ScalarField, decompressed: ScalarField, config: CorrectionConfig,

@@ -18,19 +18,20 @@
 
 namespace pmsz {
 
-// Offsets in ascending-id (rank) order.
-__host__ __device__ constexpr int rank_dx(int r) {
-    constexpr int t[14] = {-1, 0, -1, 0, -1, 0, -1, 1, 0, 1, 0, 1, 0, 1};
-    return t[r];
-}
-__host__ __device__ constexpr int rank_dy(int r) {
-    constexpr int t[14] = {-1, -1, 0, 0, -1, -1, 0, 0, 1, 1, 0, 0, 1, 1};
-    return t[r];
-}
-__host__ __device__ constexpr int rank_dz(int r) {
-    constexpr int t[14] = {-1, -1, -1, -1, 0, 0, 0, 0, 0, 0, 1, 1, 1, 1};
-    return t[r];
-}
+// Offsets in ascending-id (rank) order, packed 2 bits per rank (value + 1) so
+// a run-time rank costs a shift and a mask, no memory table:
+//   dx: -1 0 -1 0 | -1 0 -1 1 0 1 | 0 1 0 1
+//   dy: -1 -1 0 0 | -1 -1 0 0 1 1 | 0 0 1 1
+//   dz: -1 -1 -1 -1 | 0 0 0 0 0 0 | 1 1 1 1
+constexpr unsigned kPackDX = 0u | (1u << 2) | (0u << 4) | (1u << 6) | (0u << 8) | (1u << 10) | (0u << 12) |
+                             (2u << 14) | (1u << 16) | (2u << 18) | (1u << 20) | (2u << 22) | (1u << 24) | (2u << 26);
+constexpr unsigned kPackDY = 0u | (0u << 2) | (1u << 4) | (1u << 6) | (0u << 8) | (0u << 10) | (1u << 12) |
+                             (1u << 14) | (2u << 16) | (2u << 18) | (1u << 20) | (1u << 22) | (2u << 24) | (2u << 26);
+constexpr unsigned kPackDZ = 0u | (0u << 2) | (0u << 4) | (0u << 6) | (1u << 8) | (1u << 10) | (1u << 12) |
+                             (1u << 14) | (1u << 16) | (1u << 18) | (2u << 20) | (2u << 22) | (2u << 24) | (2u << 26);
+__host__ __device__ constexpr int rank_dx(int r) { return (int)((kPackDX >> (2 * r)) & 3u) - 1; }
+__host__ __device__ constexpr int rank_dy(int r) { return (int)((kPackDY >> (2 * r)) & 3u) - 1; }
+__host__ __device__ constexpr int rank_dz(int r) { return (int)((kPackDZ >> (2 * r)) & 3u) - 1; }
 // Centre sorts above ranks 0..6 and below ranks 7..13.
 constexpr int kCenterBelow = 6;
 constexpr uint8_t kExtremum = 15;
@@ -46,6 +47,24 @@ struct Dom {
 };
 
 __device__ __forceinline__ double nan64() { return __longlong_as_double(0x7ff8000000000000ll); }
+
+// Read-only loads pinned at their program position (asm volatile), used for
+// software prefetching: ptxas may not sink them to the first use.
+__device__ __forceinline__ uint32_t ld_nc_u8(const uint8_t* p) {
+    uint32_t v;
+    asm volatile("ld.global.nc.u8 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ uint32_t ld_nc_u32(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ double ld_nc_f64(const double* p) {
+    double v;
+    asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
 
 // Order-preserving 64-bit key of a finite double (min-merge by atomicMin).
 // Proposals are g[a] - tau with tau > 0, which is never -0.0.
@@ -109,7 +128,7 @@ __device__ __forceinline__ bool in_dom(const Dom& d, int64_t x, int64_t y, int64
     return x >= 0 && x < d.nx && y >= 0 && y < d.ny && z >= 0 && z < d.nz;
 }
 
-__device__ __forceinline__ int64_t rank_off(const Dom& d, int r) {
+__host__ __device__ __forceinline__ int64_t rank_off(const Dom& d, int r) {
     return (int64_t)rank_dx(r) + (int64_t)rank_dy(r) * d.sy + (int64_t)rank_dz(r) * d.sz;
 }
 

@@ -68,49 +68,6 @@ inline unsigned grid_for(long long n, int threads, int per_sm = 8) {
     return (unsigned)b;
 }
 
-// ---- K0: validation + f-code + g <- fhat ----------------------------------
-template <typename FT>
-__global__ void __launch_bounds__(256) k_prep(Dom d, const FT* __restrict__ f, const double* __restrict__ fh,
-                                              double* __restrict__ g, uint8_t* __restrict__ code,
-                                              DevCounters* ctr) {
-    const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t y = (int64_t)blockIdx.y * blockDim.y + threadIdx.y;
-    const int64_t z = blockIdx.z;
-    const bool live = x < d.nx && y < d.ny;
-    unsigned bound = 0, floorv = 0, upper = 0, nonfin = 0;
-    if (live) {
-        const int64_t c = x + y * d.sy + z * d.sz;
-        const double fv = (double)f[c];
-        const double hv = fh[c];
-        nonfin = (!isfinite(fv) || !isfinite(hv)) ? 1u : 0u;
-        // validate_error_bound (correction.py:56-60)
-        if (fabs(fv - hv) > d.xi) {
-            bound = 1;
-            atomicMin(&ctr->bound_first, (unsigned long long)c);
-        }
-        floorv = hv < fv - d.xi ? 1u : 0u;   // hazard H6
-        upper = hv > fv + d.xi ? 1u : 0u;
-        if (g != fh) g[c] = hv;
-        // field_scan(original) (correction.py:404)
-        double nv[14];
-#pragma unroll
-        for (int r = 0; r < 14; ++r) {
-            const bool ok = in_dom(d, x + rank_dx(r), y + rank_dy(r), z + rank_dz(r));
-            nv[r] = ok ? (double)f[c + rank_off(d, r)] : nan64();
-        }
-        code[c] = scan_code(fold_scan(fv, nv));
-    }
-    const unsigned b = __reduce_add_sync(0xffffffffu, bound);
-    const unsigned fl = __reduce_add_sync(0xffffffffu, floorv);
-    const unsigned up = __reduce_add_sync(0xffffffffu, upper);
-    const unsigned nf = __reduce_add_sync(0xffffffffu, nonfin);
-    if (((threadIdx.y * blockDim.x + threadIdx.x) & 31) == 0) {
-        if (b) atomicAdd(&ctr->bound_viol, (unsigned long long)b);
-        if (fl) atomicAdd(&ctr->floor_viol, (unsigned long long)fl);
-        if (up) atomicAdd(&ctr->upper_viol, (unsigned long long)up);
-        if (nf) atomicAdd(&ctr->nonfinite, (unsigned long long)nf);
-    }
-}
 
 // ---- standalone scan (topology.scan_neighbors) -----------------------------
 __global__ void __launch_bounds__(256) k_scan_full(Dom d, const double* __restrict__ v, int64_t* nmax,
@@ -251,6 +208,49 @@ __global__ void __launch_bounds__(kCompactThreads) k_bits_write(const uint32_t* 
     }
 }
 
+// Bitmap -> ascending u32 id list (the touched targets after a full sweep);
+// the words are cleared on the way (the touched bitmap is all-zero between
+// iterations).
+__global__ void __launch_bounds__(kCompactThreads) k_bits_list(uint32_t* __restrict__ bits, int64_t nwords,
+                                                               const unsigned long long* block_offs, uint32_t* list,
+                                                               int clear) {
+    __shared__ unsigned warp_sums[kCompactThreads / 32];
+    const int64_t w0 = (int64_t)blockIdx.x * kWordsPerBlock + (int64_t)threadIdx.x * kWordsPerThread;
+    uint32_t wv[kWordsPerThread];
+    unsigned c = 0;
+    for (int k = 0; k < kWordsPerThread; ++k) {
+        wv[k] = (w0 + k < nwords) ? bits[w0 + k] : 0u;
+        c += __popc(wv[k]);
+        if (clear && wv[k]) bits[w0 + k] = 0u;
+    }
+    unsigned s = c;
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned y = __shfl_up_sync(0xffffffffu, s, o);
+        if ((threadIdx.x & 31) >= o) s += y;
+    }
+    if ((threadIdx.x & 31) == 31) warp_sums[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        unsigned t = threadIdx.x < kCompactThreads / 32 ? warp_sums[threadIdx.x] : 0u;
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned y = __shfl_up_sync(0xffffffffu, t, o);
+            if (threadIdx.x >= o) t += y;
+        }
+        if (threadIdx.x < kCompactThreads / 32) warp_sums[threadIdx.x] = t;
+    }
+    __syncthreads();
+    const unsigned warp_off = (threadIdx.x >> 5) ? warp_sums[(threadIdx.x >> 5) - 1] : 0u;
+    unsigned long long pos = block_offs[blockIdx.x] + warp_off + s - c;
+    for (int k = 0; k < kWordsPerThread; ++k) {
+        uint32_t m = wv[k];
+        while (m) {
+            const int b = __ffs(m) - 1;
+            m &= m - 1;
+            list[pos++] = (uint32_t)((w0 + k) * 32 + b);
+        }
+    }
+}
+
 // ---- ghost-box helpers -------------------------------------------------------
 struct Box {
     int64_t nx, ny;
@@ -288,23 +288,62 @@ __global__ void __launch_bounds__(256) k_box_unpack(Box b, double* __restrict__ 
     if ((threadIdx.x & 31) == 0 && mine && changed) atomicAdd(changed, (unsigned long long)mine);
 }
 
+// Vertices changed outside an iteration (ghost merges) dirty their 1-ring:
+// into the pending list (bits == 0) or the pending edit bitmap (bits != 0).
+__device__ __forceinline__ void mark_changed(const Dom& d, const Work& w, int64_t v, int cur, int bits) {
+    if (bits) atomicOr(w.iteredit + (v >> 5), 1u << (v & 31));
+    else mark_ring(d, w, v, cur);
+}
+
 __global__ void __launch_bounds__(256) k_box_mark(Dom d, Work w, Box b, const double* __restrict__ before,
-                                                  const double* __restrict__ g, int nxt) {
+                                                  const double* __restrict__ g, int cur, int bits) {
     const int64_t n = b.ext[0] * b.ext[1] * b.ext[2];
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t z = i / (b.ext[0] * b.ext[1]), r = i - z * b.ext[0] * b.ext[1];
         const int64_t y = r / b.ext[0], x = r - y * b.ext[0];
         const int64_t o = (b.lo[0] + x) + b.nx * ((b.lo[1] + y) + b.ny * (b.lo[2] + z));
-        if (g[o] != before[i]) mark_ring(d, w, o, nxt);
+        if (g[o] != before[i]) mark_changed(d, w, o, cur, bits);
     }
 }
 
-__global__ void __launch_bounds__(256) k_mark_ids(Dom d, Work w, const uint32_t* __restrict__ ids, int64_t n, int nxt) {
+__global__ void __launch_bounds__(256) k_mark_ids(Dom d, Work w, const uint32_t* __restrict__ ids, int64_t n, int cur,
+                                                  int bits) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
-        mark_ring(d, w, ids[i], nxt);
+        mark_changed(d, w, ids[i], cur, bits);
 }
+
+// Closed-1-ring dilation of the per-iteration edit bitmap: centre c is dirty
+// when c + delta_o was edited for some o in {0} u STENCIL.  Word-level funnel
+// shifts over the linear id space; bits that wrap across a row or plane edge
+// only add clean centres (a superset is exact).
+struct RingDelta {
+    int64_t d[15];
+};
+
+// The masked sweep re-evaluates exactly the dirty centres, so their detection
+// bits are cleared here and set again by the sweep for those that still fire.
+__global__ void __launch_bounds__(256) k_dilate(const uint32_t* __restrict__ e, uint32_t* __restrict__ out,
+                                                uint32_t* __restrict__ det, int64_t nwords, RingDelta rd) {
+    for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nwords;
+         w += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t acc = 0;
+#pragma unroll
+        for (int k = 0; k < 15; ++k) {
+            const int64_t p = w * 32 + rd.d[k];       // source bit of output bit 0
+            const int64_t q = p >> 5;                 // floor division (arithmetic shift)
+            const int sh = (int)(p & 31);
+            const uint32_t lo = (q >= 0 && q < nwords) ? __ldg(e + q) : 0u;
+            const uint32_t hi = (q + 1 >= 0 && q + 1 < nwords) ? __ldg(e + q + 1) : 0u;
+            acc |= __funnelshift_r(lo, hi, sh);
+        }
+        out[w] = acc;
+        if (acc) det[w] &= ~acc;
+    }
+}
+
+enum { kFull = 0, kMasked = 1, kList = 2 };
 
 template <typename FT>
 __global__ void __launch_bounds__(256) k_box_extract(Box b, int64_t gny, const FT* __restrict__ src, FT* __restrict__ dst) {
@@ -333,8 +372,10 @@ struct pmsz_plan {
     int64_t nblocks_compact = 0;
     int64_t scratch_bytes = 0;
     int cur = 0;              // pending dirty list
-    bool next_full = true;    // next iteration must sweep the whole core box
-    bool last_full = true;
+    int next_mode = 0;        // kFull / kMasked / kList for the next iteration
+    int last_mode = 0;
+    int64_t pending = 0;      // length of the pending dirty list (kList)
+    RingDelta ring_delta{};   // id offsets of the closed 1-ring (dilation)
     bool prepared = false;
     int64_t floor_viol = 0, upper_viol = 0;
     // block-round bookkeeping
@@ -414,47 +455,114 @@ pmsz_status reset_iter(pmsz_plan* p, cudaStream_t s, int nxt) {
     return PMSZ_OK;
 }
 
-template <typename FT>
-pmsz_status launch_apply(pmsz_plan* p, const void* f, double* g, cudaStream_t s, int nxt) {
-    ProfScope ps(p, s, PMSZ_K_APPLY);
-    k_apply<FT><<<grid_for(p->n, 256, 16), 256, 0, s>>>(p->dom, (const FT*)f, g, p->w, nxt);
+// Set bits of a bitmap: per-block counts + one-block exclusive scan; the total
+// lands in *dst on the device.
+void launch_bits_total(pmsz_plan* p, const uint32_t* bits, unsigned long long* dst, cudaStream_t s) {
+    k_bits_count<<<(unsigned)p->nblocks_compact, kCompactThreads, 0, s>>>(bits, p->nwords, p->block_counts);
     LAUNCHED();
+    k_exclusive_scan<<<1, 1024, 0, s>>>(p->block_counts, p->nblocks_compact, dst);
+    LAUNCHED();
+}
+
+template <typename FT>
+pmsz_status launch_apply(pmsz_plan* p, const void* f, double* g, cudaStream_t s, int nxt, bool after_full,
+                         int64_t bound) {
+    if (after_full) {
+        // touched bitmap -> ascending target list (load-balanced apply)
+        ProfScope ps(p, s, PMSZ_K_COMPACT);
+        launch_bits_total(p, p->w.touched, &p->ctr->nwork, s);
+        k_bits_list<<<(unsigned)p->nblocks_compact, kCompactThreads, 0, s>>>(p->w.touched, p->nwords,
+                                                                           p->block_counts, p->w.work, 1);
+        LAUNCHED();
+    }
+    ProfScope ps(p, s, PMSZ_K_APPLY);
+    k_apply_list<FT><<<grid_for(bound, 256, 8), 256, 0, s>>>(p->dom, (const FT*)f, g, p->w, nxt);
+    LAUNCHED();
+    if (p->w.incremental) {   // list-mode ring marking (no-op when the edits went to the bitmap)
+        k_mark_list<<<grid_for(std::min<int64_t>(15 * bound, (int64_t)p->w.mark_limit), 256, 4), 256, 0, s>>>(
+            p->dom, p->w, nxt);
+        LAUNCHED();
+    }
     return PMSZ_OK;
 }
 
-// One Jacobi iteration (K1 full or sparse, then K2).  Leaves counters on host.
+// One Jacobi iteration: K1 in one of three forms, then K2.  Leaves the
+// counters on the host and decides the form of the next iteration:
+//   kFull   -- tiled sweep over the whole core box (first iteration)
+//   kMasked -- tiled sweep restricted to the dilated edit bitmap of the
+//              previous iteration (large dirty sets; exact by SURVEY H7)
+//   kList   -- gather sweep over the explicit dirty-centre list (small sets)
 pmsz_status iterate_once(pmsz_plan* p, const void* f, double* g, cudaStream_t s) {
     const int nxt = p->cur ^ 1;
     pmsz_status st = reset_iter(p, s, nxt);
     if (st) return st;
     const Dom& d = p->dom;
-    if (p->next_full || !p->w.incremental) {
+    const int mode = p->w.incremental ? p->next_mode : kFull;
+    const int64_t cx = d.hi[0] - d.lo[0], cy = d.hi[1] - d.lo[1], cz = d.hi[2] - d.lo[2];
+    const bool nonempty = cx > 0 && cy > 0 && cz > 0;
+    int64_t apply_bound = p->n;   // upper bound of the targets, sizes the apply grid
+    if (mode == kFull) {
         if (p->w.incremental) CUDA_TRY(cudaMemsetAsync(p->w.actbits, 0, p->nwords * 4, s));
-        const int64_t cx = d.hi[0] - d.lo[0], cy = d.hi[1] - d.lo[1], cz = d.hi[2] - d.lo[2];
-        if (cx > 0 && cy > 0 && cz > 0) {
+        CUDA_TRY(cudaMemsetAsync(p->w.detbits, 0, p->nwords * 4, s));
+        p->w.track = 0;
+        if (nonempty) {
             ProfScope ps(p, s, PMSZ_K_SWEEP_FULL);
             launch_sweep_full<false>(d, g, p->w, s);
             LAUNCHED();
         }
-        p->last_full = true;
-    } else {
-        ProfScope ps(p, s, PMSZ_K_SWEEP_SPARSE);
-        k_sweep_sparse<<<grid_for(p->w.act_cap, 256, 16), 256, 0, s>>>(d, g, p->w, p->cur);
-        LAUNCHED();
-        p->last_full = false;
+    } else if (mode == kMasked) {
+        p->w.track = 0;
+        {
+            ProfScope ps(p, s, PMSZ_K_OTHER);
+            k_dilate<<<grid_for(p->nwords, 256, 8), 256, 0, s>>>(p->w.iteredit, p->w.actbits, p->w.detbits,
+                                                               p->nwords, p->ring_delta);
+            LAUNCHED();
+        }
+        CUDA_TRY(cudaMemsetAsync(p->w.iteredit, 0, p->nwords * 4, s));
+        if (nonempty) {
+            ProfScope ps(p, s, PMSZ_K_SWEEP_MASKED);
+            launch_sweep_full<false>(d, g, p->w, s, p->w.actbits);
+            LAUNCHED();
+        }
+        CUDA_TRY(cudaMemsetAsync(p->w.actbits, 0, p->nwords * 4, s));
     }
-    st = p->f32 ? launch_apply<float>(p, f, g, s, nxt) : launch_apply<double>(p, f, g, s, nxt);
+    if (mode != kList && nonempty) {
+        // centres with a detection (bitmap set by the tiled sweep) -> list -> rules
+        {
+            ProfScope ps(p, s, PMSZ_K_COMPACT);
+            launch_bits_total(p, p->w.detbits, &p->ctr->ndefer, s);
+            k_bits_list<<<(unsigned)p->nblocks_compact, kCompactThreads, 0, s>>>(p->w.detbits, p->nwords,
+                                                                               p->block_counts, p->w.work, 0);
+            LAUNCHED();
+        }
+        ProfScope ps(p, s, PMSZ_K_DEFER);
+        k_defer<<<grid_for(p->n, 256, 8), 256, 0, s>>>(d, g, p->w);
+        LAUNCHED();
+    }
+    if (mode == kList) {
+        ProfScope ps(p, s, PMSZ_K_SWEEP_SPARSE);
+        p->w.track = 1;
+        const int64_t m = std::min<int64_t>(p->pending, (int64_t)p->w.act_cap);
+        k_sweep_sparse<<<grid_for(m, 256, 8), 256, 0, s>>>(d, g, p->w, p->cur);
+        LAUNCHED();
+        apply_bound = std::min<int64_t>(p->n, 15 * m + 32);
+    }
+    p->last_mode = mode;
+    st = p->f32 ? launch_apply<float>(p, f, g, s, nxt, mode != kList, apply_bound)
+                : launch_apply<double>(p, f, g, s, nxt, mode != kList, apply_bound);
     if (st) return st;
     CUDA_TRY(cudaGetLastError());
     st = sync_counters(p, s);
     if (st) return st;
-    // next mode
     if (p->w.incremental) {
-        if (p->hctr->nact[nxt] > p->w.act_cap) {
-            p->next_full = true;
+        if (p->hctr->scratch[3] == kMarkBits) {
+            p->next_mode = kMasked;
+        } else if (p->hctr->nact[nxt] > p->w.act_cap) {
+            p->next_mode = kFull;
         } else {
-            p->next_full = false;
+            p->next_mode = kList;
             p->cur = nxt;
+            p->pending = (int64_t)p->hctr->nact[nxt];
         }
     }
     return PMSZ_OK;
@@ -465,9 +573,13 @@ pmsz_status reset_run_state(pmsz_plan* p, cudaStream_t s) {
     CUDA_TRY(cudaMemsetAsync(&p->ctr->bound_first, 0xff, sizeof(unsigned long long), s));
     CUDA_TRY(cudaMemsetAsync(p->w.editbits, 0, p->nwords * 4, s));
     CUDA_TRY(cudaMemsetAsync(p->w.counts, 0, p->n * sizeof(uint16_t), s));
-    if (p->w.incremental) CUDA_TRY(cudaMemsetAsync(p->w.actbits, 0, p->nwords * 4, s));
+    if (p->w.incremental) {
+        CUDA_TRY(cudaMemsetAsync(p->w.actbits, 0, p->nwords * 4, s));
+        CUDA_TRY(cudaMemsetAsync(p->w.iteredit, 0, p->nwords * 4, s));
+    }
     p->cur = 0;
-    p->next_full = true;
+    p->next_mode = kFull;
+    p->pending = 0;
     p->iterations = 0;
     p->edit_total = 0;
     return PMSZ_OK;
@@ -476,22 +588,21 @@ pmsz_status reset_run_state(pmsz_plan* p, cudaStream_t s) {
 // After an aborted run the proposal array may hold stale keys.
 pmsz_status restore_prop(pmsz_plan* p, cudaStream_t s) {
     CUDA_TRY(cudaMemsetAsync(p->w.prop, 0xff, p->n * sizeof(unsigned long long), s));
+    CUDA_TRY(cudaMemsetAsync(p->w.touched, 0, p->nwords * 4, s));
     return PMSZ_OK;
 }
 
 pmsz_status prep(pmsz_plan* p, const void* f, const double* fh, double* g, cudaStream_t s) {
     pmsz_status st = reset_run_state(p, s);
     if (st) return st;
-    const Dom& d = p->dom;
-    dim3 block(32, 8, 1);
-    dim3 grid((unsigned)((d.nx + 31) / 32), (unsigned)((d.ny + 7) / 8), (unsigned)d.nz);
-    ProfScope* ps = new ProfScope(p, s, PMSZ_K_PREP);
-    if (p->f32)
-        k_prep<float><<<grid, block, 0, s>>>(d, (const float*)f, fh, g, p->w.code, p->ctr);
-    else
-        k_prep<double><<<grid, block, 0, s>>>(d, (const double*)f, fh, g, p->w.code, p->ctr);
-    delete ps;
-    LAUNCHED();
+    {
+        ProfScope ps(p, s, PMSZ_K_PREP);
+        if (p->f32)
+            launch_prep<float>(p->dom, (const float*)f, fh, g, p->w.code, p->ctr, s);
+        else
+            launch_prep<double>(p->dom, (const double*)f, fh, g, p->w.code, p->ctr, s);
+        LAUNCHED();
+    }
     CUDA_TRY(cudaGetLastError());
     st = sync_counters(p, s);
     if (st) return st;
@@ -533,13 +644,23 @@ pmsz_status count_bounds(pmsz_plan* p, const void* f, const double* g, cudaStrea
     return PMSZ_OK;
 }
 
+pmsz_status bits_total(pmsz_plan* p, const uint32_t* bits, cudaStream_t s, int64_t* count) {
+    {
+        ProfScope ps(p, s, PMSZ_K_COMPACT);
+        launch_bits_total(p, bits, &p->ctr->scratch[2], s);
+    }
+    CUDA_TRY(cudaGetLastError());
+    pmsz_status st = sync_counters(p, s);
+    if (st) return st;
+    *count = (int64_t)p->hctr->scratch[2];
+    return PMSZ_OK;
+}
+
 pmsz_status edit_count(pmsz_plan* p, cudaStream_t s, int64_t* count) {
-    ProfScope* ps = new ProfScope(p, s, PMSZ_K_COMPACT);
-    k_bits_count<<<(unsigned)p->nblocks_compact, kCompactThreads, 0, s>>>(p->w.editbits, p->nwords, p->block_counts);
-    LAUNCHED();
-    k_exclusive_scan<<<1, 1024, 0, s>>>(p->block_counts, p->nblocks_compact, &p->ctr->scratch[2]);
-    delete ps;
-    LAUNCHED();
+    {
+        ProfScope ps(p, s, PMSZ_K_COMPACT);
+        launch_bits_total(p, p->w.editbits, &p->ctr->scratch[2], s);
+    }
     CUDA_TRY(cudaGetLastError());
     pmsz_status st = sync_counters(p, s);
     if (st) return st;
@@ -590,6 +711,15 @@ pmsz_status pmsz_plan_create(const pmsz_desc* desc, pmsz_plan** out) {
     const int64_t ncore = (d.core_hi[0] - d.core_lo[0]) * (d.core_hi[1] - d.core_lo[1]) *
                           (d.core_hi[2] - d.core_lo[2]);
     p->w.act_cap = (unsigned long long)std::max<int64_t>(ncore / 4, 4096);
+    // explicit dirty lists only while they stay below ~1.5% of the core box;
+    // larger dirty sets go through the dilated bitmap and a masked tiled sweep
+    p->w.mark_limit = (unsigned long long)std::max<int64_t>(ncore / 64, 4096);
+    p->w.nwords = p->nwords;
+    {
+        int k = 0;
+        p->ring_delta.d[k++] = 0;
+        for (int r = 0; r < 14; ++r) p->ring_delta.d[k++] = rank_off(p->dom, r);
+    }
     p->nblocks_compact = (p->nwords + kWordsPerBlock - 1) / kWordsPerBlock;
     auto alloc = [&](void** ptr, size_t bytes) -> bool {
         if (cudaMalloc(ptr, bytes) != cudaSuccess) return false;
@@ -598,11 +728,13 @@ pmsz_status pmsz_plan_create(const pmsz_desc* desc, pmsz_plan** out) {
     };
     bool ok = alloc((void**)&p->w.prop, n * 8) && alloc((void**)&p->w.work, n * 4) &&
               alloc((void**)&p->w.editbits, p->nwords * 4) && alloc((void**)&p->w.counts, n * 2) &&
+              alloc((void**)&p->w.touched, p->nwords * 4) && alloc((void**)&p->w.detbits, p->nwords * 4) &&
               alloc((void**)&p->w.code, n) && alloc((void**)&p->ctr, sizeof(DevCounters)) &&
               alloc((void**)&p->block_counts, std::max<int64_t>(p->nblocks_compact, 1) * 8);
     if (ok && p->w.incremental)
         ok = alloc((void**)&p->w.actbits, p->nwords * 4) && alloc((void**)&p->w.act[0], p->w.act_cap * 4) &&
-             alloc((void**)&p->w.act[1], p->w.act_cap * 4);
+             alloc((void**)&p->w.act[1], p->w.act_cap * 4) && alloc((void**)&p->w.iteredit, p->nwords * 4) &&
+             alloc((void**)&p->w.elist, p->w.mark_limit * 4);
     if (ok) ok = cudaMallocHost((void**)&p->hctr, sizeof(DevCounters)) == cudaSuccess;
     if (!ok) {
         cudaGetLastError();
@@ -612,6 +744,7 @@ pmsz_status pmsz_plan_create(const pmsz_desc* desc, pmsz_plan** out) {
     p->w.ctr = p->ctr;
     memset(p->hctr, 0, sizeof(DevCounters));
     if (cudaMemset(p->w.prop, 0xff, n * 8) != cudaSuccess || cudaMemset(p->ctr, 0, sizeof(DevCounters)) != cudaSuccess ||
+        cudaMemset(p->w.touched, 0, p->nwords * 4) != cudaSuccess || cudaMemset(p->w.detbits, 0, p->nwords * 4) != cudaSuccess ||
         cudaDeviceSynchronize() != cudaSuccess) {
         pmsz_plan_destroy(p);
         return fail(PMSZ_ERR_CUDA, "plan initialisation failed");
@@ -622,9 +755,10 @@ pmsz_status pmsz_plan_create(const pmsz_desc* desc, pmsz_plan** out) {
 
 void pmsz_plan_destroy(pmsz_plan* p) {
     if (!p) return;
-    cudaFree(p->w.prop); cudaFree(p->w.work); cudaFree(p->w.editbits); cudaFree(p->w.counts);
+    cudaFree(p->w.prop); cudaFree(p->w.work); cudaFree(p->w.touched); cudaFree(p->w.detbits); cudaFree(p->w.editbits); cudaFree(p->w.counts);
     cudaFree(p->w.code); cudaFree(p->ctr); cudaFree(p->block_counts);
-    cudaFree(p->w.actbits); cudaFree(p->w.act[0]); cudaFree(p->w.act[1]);
+    cudaFree(p->w.actbits); cudaFree(p->w.act[0]); cudaFree(p->w.act[1]); cudaFree(p->w.iteredit);
+    cudaFree(p->w.elist);
     if (p->hctr) cudaFreeHost(p->hctr);
     for (cudaEvent_t e : p->prof_ev) cudaEventDestroy(e);
     delete p;
@@ -685,7 +819,9 @@ pmsz_status pmsz_iterate(pmsz_plan* p, const void* f, double* g, uint8_t* edited
         r->shared_dirty = (int64_t)p->hctr->shared_dirty;
         r->iterations = p->iterations;
         r->edit_count = p->edit_total;
-        if (p->last_full) ++r->full_sweeps; else ++r->sparse_sweeps;
+        if (p->last_mode == kFull) ++r->full_sweeps;
+        else if (p->last_mode == kMasked) ++r->masked_sweeps;
+        else ++r->sparse_sweeps;
     }
     return PMSZ_OK;
 }
@@ -713,38 +849,43 @@ pmsz_status pmsz_block_round(pmsz_plan* p, const void* f, double* g, int32_t loc
 pmsz_status pmsz_mark_all_dirty(pmsz_plan* p, void* stream) {
     (void)stream;
     if (!p) return fail(PMSZ_ERR_INVALID, "null plan");
-    p->next_full = true;
+    p->next_mode = kFull;
+    return PMSZ_OK;
+}
+
+// After marking outside an iteration: refresh the pending list length, or
+// fall back to a full sweep when the list overflowed.
+static pmsz_status after_mark(pmsz_plan* p, cudaStream_t s) {
+    CUDA_TRY(cudaGetLastError());
+    pmsz_status st = sync_counters(p, s);
+    if (st) return st;
+    if (p->next_mode == kList) {
+        if (p->hctr->nact[p->cur] > p->w.act_cap) p->next_mode = kFull;
+        else p->pending = (int64_t)p->hctr->nact[p->cur];
+    }
     return PMSZ_OK;
 }
 
 pmsz_status pmsz_mark_dirty_ids(pmsz_plan* p, const uint32_t* ids, int64_t count, void* stream) {
     if (!p) return fail(PMSZ_ERR_INVALID, "null plan");
-    if (!p->w.incremental || p->next_full || count <= 0) return PMSZ_OK;
+    if (!p->w.incremental || p->next_mode == kFull || count <= 0) return PMSZ_OK;
     cudaStream_t s = S(stream);
-    k_mark_ids<<<grid_for(count, 256), 256, 0, s>>>(p->dom, p->w, ids, count, p->cur);
+    k_mark_ids<<<grid_for(count, 256), 256, 0, s>>>(p->dom, p->w, ids, count, p->cur, p->next_mode == kMasked);
     LAUNCHED();
-    CUDA_TRY(cudaGetLastError());
-    pmsz_status st = sync_counters(p, s);
-    if (st) return st;
-    if (p->hctr->nact[p->cur] > p->w.act_cap) p->next_full = true;
-    return PMSZ_OK;
+    return after_mark(p, s);
 }
 
 pmsz_status pmsz_box_mark_changed(pmsz_plan* p, const int64_t lo[3], const int64_t hi[3], const double* before,
                                   const double* g, void* stream) {
     if (!p) return fail(PMSZ_ERR_INVALID, "null plan");
-    if (!p->w.incremental || p->next_full) return PMSZ_OK;
+    if (!p->w.incremental || p->next_mode == kFull) return PMSZ_OK;
     cudaStream_t s = S(stream);
     Box b{p->dom.nx, p->dom.ny, {lo[0], lo[1], lo[2]}, {hi[0] - lo[0], hi[1] - lo[1], hi[2] - lo[2]}};
     const int64_t n = b.ext[0] * b.ext[1] * b.ext[2];
     if (n <= 0) return PMSZ_OK;
-    k_box_mark<<<grid_for(n, 256), 256, 0, s>>>(p->dom, p->w, b, before, g, p->cur);
+    k_box_mark<<<grid_for(n, 256), 256, 0, s>>>(p->dom, p->w, b, before, g, p->cur, p->next_mode == kMasked);
     LAUNCHED();
-    CUDA_TRY(cudaGetLastError());
-    pmsz_status st = sync_counters(p, s);
-    if (st) return st;
-    if (p->hctr->nact[p->cur] > p->w.act_cap) p->next_full = true;
-    return PMSZ_OK;
+    return after_mark(p, s);
 }
 
 pmsz_status pmsz_verify(pmsz_plan* p, const double* g, pmsz_result* r, void* stream) {
@@ -800,11 +941,19 @@ pmsz_status pmsz_run_correction(pmsz_plan* p, const void* f, const double* fh, d
             return fail(PMSZ_ERR_CONVERGENCE, "corrected field escaped the error bound");
         }
     }
-    // re-scan + _kind_masks must be empty (correction.py:424-426)
-    st = pmsz_verify(p, g, r, stream);
-    if (st) return st;
+    // re-scan + _kind_masks must be empty (correction.py:424-426).  Every
+    // centre's detection status at its latest evaluation is kept in detbits
+    // and a centre is re-evaluated whenever a vertex of its closed 1-ring
+    // changes (or by a full sweep), so the popcount equals the detections of
+    // a full re-scan of the final field.  The per-kind split is only computed
+    // when something survived.
     int64_t residual = 0;
-    for (int k = 0; k < 6; ++k) residual += r->residual[k];
+    st = bits_total(p, p->w.detbits, s, &residual);
+    if (st) return st;
+    if (residual) {
+        st = pmsz_verify(p, g, r, stream);
+        if (st) return st;
+    }
     if (residual) {
         r->convergence_kind = PMSZ_CONV_RESIDUAL;
         return fail(PMSZ_ERR_CONVERGENCE, "distortions survived a zero-edit iteration");

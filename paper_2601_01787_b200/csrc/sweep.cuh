@@ -2,27 +2,32 @@
 //
 // K1  detect+propose : per centre, steepest-neighbour scan of g, compare with
 //                      the packed f-code, and on a mismatch run the six rules of
-//                      correction.py:169-229, min-merging every
-//                      proposal g[a]-tau into prop[t] with a 64-bit atomicMin on
-//                      an order-preserving key.  The first proposer of a target
-//                      appends it to the work list (warp-aggregated).
-// K2  apply          : over the work list, g' = max(min(g, p), f - xi)
+//                      correction.py:169-229 on the register-resident
+//                      neighbour values.  Every proposal g[a]-tau is min-merged
+//                      into prop[t] by a fire-and-forget 64-bit RED.MIN on an
+//                      order-preserving key (exactly np.minimum.at) and t is
+//                      flagged in the `touched` bitmap (RED.OR).  Sparse sweeps
+//                      additionally append first-touched targets to a work list.
+// K2  apply          : over the touched targets, g' = max(min(g, p), f - xi)
 //                      (correction.py:239), edit counting, per-vertex edit
 //                      counts, ever-edited bitmap, dirty 1-ring for the next
 //                      incremental sweep, shared_dirty (parallel.py:249-250).
 // K4  verify         : the K1 scan in counting mode (correction.py:424-426).
 #pragma once
 #include <cooperative_groups.h>
+#include <cooperative_groups/scan.h>
 #include "common.cuh"
 
 namespace pmsz {
 namespace cg = cooperative_groups;
 
 struct DevCounters {
-    unsigned long long nwork;        // targets in the work list
+    unsigned long long nwork;        // targets in the work list (sparse mode)
     unsigned long long nedits;       // edits of the iteration
     unsigned long long ndetect;      // centres with >= 1 detection
     unsigned long long shared_dirty;
+    unsigned long long ndefer;       // mismatching centres handed from a tiled sweep to k_defer
+    unsigned long long nelist;       // edits recorded for list-mode ring marking
     unsigned long long nact[2];      // dirty-list lengths (ping-pong)
     unsigned long long maxcount;     // max per-vertex edit count
     unsigned long long kinds[6];     // verify: per-kind detection counts
@@ -37,16 +42,23 @@ struct DevCounters {
 
 struct Work {
     unsigned long long* prop;   // n, kNoProposal when idle
-    uint32_t* work;             // target list (cap n)
+    uint32_t* touched;          // n bits: has a pending proposal
+    uint32_t* work;             // target list (sparse mode)
     uint32_t* act[2];           // dirty centre lists
     uint32_t* actbits;          // n bits
     uint32_t* editbits;         // n bits: ever edited
+    uint32_t* detbits;          // n bits: centre had a detection at its latest evaluation
+    uint32_t* iteredit;         // n bits: edited in this iteration (bitmap-mode marking)
+    uint32_t* elist;            // edits of a list-mode iteration (ring marking input)
     uint16_t* counts;           // per-vertex edit counts
     uint8_t* code;              // packed f-code
     uint8_t* edited_mask;       // optional per-iteration mask
     DevCounters* ctr;
     unsigned long long act_cap;
+    unsigned long long mark_limit;  // K2 skips ring marking above this many detections
+    int64_t nwords;
     int incremental;
+    int track;                  // append first-touched targets to `work`
 };
 
 // Warp-aggregated append: returns the slot of this thread in `counter`.
@@ -58,16 +70,41 @@ __device__ __forceinline__ unsigned long long agg_append(unsigned long long* cou
     return base + g.thread_rank();
 }
 
-__device__ __forceinline__ void propose(const Work& w, int64_t t, double val) {
-    const unsigned long long k = okey(val);
-    // Skip the atomic when the current value already dominates (exact: min-merge).
-    if (k >= w.prop[t]) return;
-    const unsigned long long old = atomicMin(w.prop + t, k);
-    if (old == kNoProposal) {
-        const unsigned long long slot = agg_append(&w.ctr->nwork);
-        w.work[slot] = (uint32_t)t;
-    }
+// Proposal g[a]-tau -> prop[t]: min-merge by RED.MIN on the order key (exactly
+// np.minimum.at) and flag t in the touched bitmap (RED.OR).  Nothing returns,
+// so a thread's proposals are all in flight at once.
+__device__ __forceinline__ void propose_red(const Work& w, int64_t t, double val) {
+    atomicMin(w.prop + t, okey(val));
+    atomicOr(w.touched + (t >> 5), 1u << (t & 31));
 }
+
+struct EmitRed {
+    const Work& w;
+    __device__ __forceinline__ void operator()(int64_t t, double val) { propose_red(w, t, val); }
+};
+
+// Sparse sweeps also remember their targets; flush() reserves the thread's
+// slots of the work list with one warp-aggregated atomic.  Duplicates across
+// centres are resolved in K2 (first to clear the touched bit applies).
+struct EmitList {
+    const Work& w;
+    uint32_t t[18];
+    int n;
+    __device__ __forceinline__ void operator()(int64_t tt, double val) {
+        propose_red(w, tt, val);
+        t[n++] = (uint32_t)tt;
+    }
+    __device__ __forceinline__ void flush() {
+        cg::coalesced_group g = cg::coalesced_threads();
+        const unsigned mine = (unsigned)n;
+        const unsigned before = cg::exclusive_scan(g, mine);
+        const unsigned total = g.shfl(before + mine, g.size() - 1);
+        unsigned long long base = 0;
+        if (g.thread_rank() == 0 && total) base = atomicAdd(&w.ctr->nwork, (unsigned long long)total);
+        base = g.shfl(base, 0) + before;
+        for (int i = 0; i < n; ++i) w.work[base + i] = t[i];
+    }
+};
 
 // Mismatch between the g-scan and the f-code, i.e. "some rule fires".
 __device__ __forceinline__ bool code_mismatch(const Dom& d, uint8_t gcode, uint8_t fcode) {
@@ -77,12 +114,19 @@ __device__ __forceinline__ bool code_mismatch(const Dom& d, uint8_t gcode, uint8
     return (gx != fx) || (gn != fn);
 }
 
-// The six rules for centre c (correction.py:169-229).  kCount:
+__device__ __forceinline__ double pick(const double (&nv)[14], int r) {
+    double v = nv[0];
+#pragma unroll
+    for (int k = 1; k < 14; ++k) v = (r == k) ? nv[k] : v;
+    return v;
+}
+
+// The six rules for centre c (correction.py:169-229) on the
+// snapshot values nv[] (rank order, NaN = outside the domain).  kCount:
 // count detections per kind instead of proposing (verify sweep).
-template <bool kCount>
-__device__ __noinline__ void rules(const Dom& d, const double* __restrict__ g, const Work& w,
-                                   const Scan& s, uint8_t fcode, int64_t c,
-                                   int64_t x, int64_t y, int64_t z) {
+template <bool kCount, class Emit>
+__device__ __forceinline__ void rules(const Dom& d, const Work& w, const Scan& s, const double (&nv)[14],
+                                      uint8_t fcode, int64_t c, Emit& propose) {
     const int fr = fcode & 15, fs = fcode >> 4;
     const bool fmax = fr == kExtremum, fmin = fs == kExtremum;
     const bool k_fpmax = s.is_max && !fmax;
@@ -100,53 +144,58 @@ __device__ __noinline__ void rules(const Dom& d, const double* __restrict__ g, c
         if (k_desc) atomicAdd(&w.ctr->kinds[5], 1ull);
         return;
     }
-    if (!(k_fpmax | k_fnmax | k_fpmin | k_fnmin | k_asc | k_desc)) return;
-    atomicAdd(&w.ctr->ndetect, 1ull);
     const double tau = d.tau;
-    // FALSE_MAXIMUM: target c, anchor f.nmax(c)          (correction.py:213-215)
-    if (k_fpmax) propose(w, c, __ldg(g + c + rank_off(d, fr)) - tau);
-    // MISSING_MAXIMUM: anchor c, targets above c            (correction.py:216-218)
+    const double vc = s.vc;
+    // FALSE_MAXIMUM: target c, anchor f.nmax(c)              (correction.py:213-215)
+    // ASC_ORDER: anchor a = f.nmax(c), targets above a         (correction.py:225-227)
+    // MISSING_MAXIMUM: anchor c, targets above c               (correction.py:216-218)
+    if (k_fpmax || k_asc) {
+        const double va = pick(nv, fr);
+        if (k_fpmax) propose(c, va - tau);
+        if (k_asc) {
+            const double val = va - tau;
+#pragma unroll
+            for (int r = 0; r < 14; ++r) {
+                const double vj = nv[r];
+                if (vj > va || (vj == va && r > fr)) propose(c + rank_off(d, r), val);
+            }
+        }
+    }
     if (k_fnmax) {
-        const double vc = s.vc, val = vc - tau;
-#pragma unroll 1
+        const double val = vc - tau;
+#pragma unroll
         for (int r = 0; r < 14; ++r) {
-            if (!in_dom(d, x + rank_dx(r), y + rank_dy(r), z + rank_dz(r))) continue;
-            const int64_t j = c + rank_off(d, r);
-            const double vj = __ldg(g + j);
-            if (vj > vc || (vj == vc && r > kCenterBelow)) propose(w, j, val);
+            const double vj = nv[r];
+            if (vj > vc || (vj == vc && r > kCenterBelow)) propose(c + rank_off(d, r), val);
         }
     }
-    // ASC_ORDER: anchor a = f.nmax(c), targets above a     (correction.py:225-227)
-    if (k_asc) {
-        const double va = __ldg(g + c + rank_off(d, fr)), val = va - tau;
-#pragma unroll 1
-        for (int r = 0; r < 14; ++r) {
-            if (!in_dom(d, x + rank_dx(r), y + rank_dy(r), z + rank_dz(r))) continue;
-            const int64_t j = c + rank_off(d, r);
-            const double vj = __ldg(g + j);
-            if (vj > va || (vj == va && r > fr)) propose(w, j, val);
-        }
-    }
-    // FALSE_MINIMUM: anchor c, target f.nmin(c)            (correction.py:219-221)
-    if (k_fpmin) propose(w, c + rank_off(d, fs), s.vc - tau);
-    // MISSING_MINIMUM: anchor g.nmin(c), target c           (correction.py:222-224)
-    if (k_fnmin) propose(w, c, s.vmin - tau);
-    // DESC_ORDER: anchor g.nmin(c), target f.nmin(c)        (correction.py:228-229)
-    if (k_desc) propose(w, c + rank_off(d, fs), s.vmin - tau);
+    // FALSE_MINIMUM: anchor c, target f.nmin(c)               (correction.py:219-221)
+    if (k_fpmin) propose(c + rank_off(d, fs), vc - tau);
+    // MISSING_MINIMUM: anchor g.nmin(c), target c              (correction.py:222-224)
+    if (k_fnmin) propose(c, s.vmin - tau);
+    // DESC_ORDER: anchor g.nmin(c), target f.nmin(c)           (correction.py:228-229)
+    if (k_desc) propose(c + rank_off(d, fs), s.vmin - tau);
 }
 
-// ---------------------------------------------------------------------------
-// K1/K4 full sweep over the core box, one thread per centre (gather form).
-template <bool kCount>
-__global__ void __launch_bounds__(256) k_sweep_gather(Dom d, const double* __restrict__ g, Work w) {
-    const int64_t x = d.lo[0] + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t y = d.lo[1] + (int64_t)blockIdx.y * blockDim.y + threadIdx.y;
-    const int64_t z = d.lo[2] + (int64_t)blockIdx.z;
-    if (x >= d.hi[0] || y >= d.hi[1]) return;
-    const int64_t c = x + y * d.sy + z * d.sz;
-    const Scan s = gather_scan(d, g, x, y, z);
-    const uint8_t fc = w.code[c];
-    if (code_mismatch(d, scan_code(s), fc)) rules<kCount>(d, g, w, s, fc, c, x, y, z);
+// Rule evaluation of the centres a tiled sweep found mismatching (their ids are
+// in w.work[0 .. ndefer)); one thread per centre, neighbours gathered from g.
+__global__ void __launch_bounds__(256) k_defer(Dom d, const double* __restrict__ g, Work w) {
+    const unsigned long long n = w.ctr->ndefer;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (unsigned long long)gridDim.x * blockDim.x) {
+        const int64_t c = w.work[i];
+        int64_t x, y, z;
+        coords(d, c, x, y, z);
+        double nv[14];
+#pragma unroll
+        for (int r = 0; r < 14; ++r) {
+            const bool ok = in_dom(d, x + rank_dx(r), y + rank_dy(r), z + rank_dz(r));
+            nv[r] = ok ? __ldg(g + c + rank_off(d, r)) : nan64();
+        }
+        const Scan s = fold_scan(__ldg(g + c), nv);
+        EmitRed emit{w};
+        rules<false>(d, w, s, nv, w.code[c], c, emit);
+    }
 }
 
 // K1 sparse sweep over the dirty-centre list (grid-stride; count read on device).
@@ -160,9 +209,24 @@ __global__ void __launch_bounds__(256) k_sweep_sparse(Dom d, const double* __res
         atomicAnd(w.actbits + (c >> 5), ~(1u << (c & 31)));
         int64_t x, y, z;
         coords(d, c, x, y, z);
-        const Scan s = gather_scan(d, g, x, y, z);
+        double nv[14];
+#pragma unroll
+        for (int r = 0; r < 14; ++r) {
+            const bool ok = in_dom(d, x + rank_dx(r), y + rank_dy(r), z + rank_dz(r));
+            nv[r] = ok ? __ldg(g + c + rank_off(d, r)) : nan64();
+        }
+        const Scan s = fold_scan(__ldg(g + c), nv);
         const uint8_t fc = w.code[c];
-        if (code_mismatch(d, scan_code(s), fc)) rules<false>(d, g, w, s, fc, c, x, y, z);
+        const uint32_t bit = 1u << (c & 31);
+        if (code_mismatch(d, scan_code(s), fc)) {
+            atomicOr(w.detbits + (c >> 5), bit);
+            atomicAdd(&w.ctr->ndetect, 1ull);
+            EmitList emit{w, {}, 0};
+            rules<false>(d, w, s, nv, fc, c, emit);
+            emit.flush();
+        } else if (__ldcg(w.detbits + (c >> 5)) & bit) {
+            atomicAnd(w.detbits + (c >> 5), ~bit);
+        }
     }
 }
 
@@ -195,45 +259,136 @@ __device__ __forceinline__ void mark_ring(const Dom& d, const Work& w, int64_t v
     }
 }
 
-// K2 apply over the work list.
+struct ApplyAcc {
+    unsigned long long edits = 0;
+    unsigned int maxc = 0;
+    bool shared = false;
+};
+
+// Apply the merged proposal at t (correction.py:239) and do the bookkeeping.
+// Dirty marking of the next incremental sweep: none, explicit 1-ring lists
+// (small edit sets -> sparse sweep), or the per-iteration edit bitmap that the
+// dilation kernel turns into the mask of a masked tiled sweep (large sets).
+enum { kMarkNone = 0, kMarkList = 1, kMarkBits = 2 };
+
+// Operands of one target, loaded before any of them is used so a thread keeps
+// several scattered targets in flight.
+struct TargetOps {
+    unsigned long long key;
+    double gt, fv;
+    unsigned int cnt;
+};
 template <typename FT>
-__global__ void __launch_bounds__(256) k_apply(Dom d, const FT* __restrict__ f, double* __restrict__ g,
-                                               Work w, int nxt) {
-    const unsigned long long n = w.ctr->nwork;
-    unsigned long long my_edits = 0;
-    unsigned int my_max = 0;
-    bool my_shared = false;
-    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-         i += (unsigned long long)gridDim.x * blockDim.x) {
-        const int64_t t = w.work[i];
-        const double p = okey_inv(w.prop[t]);
-        w.prop[t] = kNoProposal;
-        const double gt = g[t];
-        const double lower = (double)f[t] - d.xi;           // BoundsField.lower (correction.py:122)
-        const double m = (p < gt) ? p : gt;                  // np.minimum(g, prop)
-        const double nv = (m < lower) ? lower : m;           // np.maximum(., lower)
-        if (nv != gt) {
-            g[t] = nv;
-            ++my_edits;
-            const unsigned int cnt = (unsigned int)w.counts[t] + 1u;
-            w.counts[t] = (uint16_t)min(cnt, 65535u);
-            my_max = max(my_max, cnt);
-            atomicOr(w.editbits + (t >> 5), 1u << (t & 31));
-            if (w.edited_mask) w.edited_mask[t] = 1;
-            int64_t x, y, z;
-            coords(d, t, x, y, z);
-            my_shared |= in_shared(d, x, y, z);
-            if (w.incremental) mark_ring(d, w, t, nxt);
-        }
+__device__ __forceinline__ TargetOps load_target(const FT* __restrict__ f, const double* __restrict__ g,
+                                                 const Work& w, int64_t t) {
+    return TargetOps{w.prop[t], g[t], (double)f[t], (unsigned int)w.counts[t]};
+}
+
+template <typename FT>
+__device__ __forceinline__ void apply_target(const Dom& d, const FT* __restrict__ f, double* __restrict__ g,
+                                             const Work& w, int64_t t, int mark, int nxt, ApplyAcc& acc,
+                                             const TargetOps& op) {
+    const double p = okey_inv(op.key);
+    w.prop[t] = kNoProposal;
+    const double gt = op.gt;
+    const double lower = op.fv - d.xi;                   // BoundsField.lower (correction.py:122)
+    const double m = (p < gt) ? p : gt;                  // np.minimum(g, prop)
+    const double nv = (m < lower) ? lower : m;           // np.maximum(., lower)
+    if (nv != gt) {
+        g[t] = nv;
+        ++acc.edits;
+        const unsigned int cnt = op.cnt + 1u;
+        w.counts[t] = (uint16_t)min(cnt, 65535u);
+        acc.maxc = max(acc.maxc, cnt);
+        atomicOr(w.editbits + (t >> 5), 1u << (t & 31));
+        if (w.edited_mask) w.edited_mask[t] = 1;
+        int64_t x, y, z;
+        coords(d, t, x, y, z);
+        acc.shared |= in_shared(d, x, y, z);
+        // list mode: the 1-rings are marked by k_mark_list, one thread per member
+        if (mark == kMarkList) w.elist[agg_append(&w.ctr->nelist)] = (uint32_t)t;
+        else if (mark == kMarkBits) atomicOr(w.iteredit + (t >> 5), 1u << (t & 31));
     }
-    // Block-level reduction of the counters, one atomic per warp.
-    const unsigned long long we = __reduce_add_sync(0xffffffffu, (unsigned)my_edits);
-    const unsigned int wm = __reduce_max_sync(0xffffffffu, my_max);
-    const unsigned int ws = __reduce_or_sync(0xffffffffu, my_shared ? 1u : 0u);
+}
+
+// The marking mode follows from the number of targets (an upper bound of the
+// edits): 15 ring entries per edit must fit the list budget.
+__device__ __forceinline__ int apply_marks(const Work& w) {
+    if (!w.incremental) return kMarkNone;
+    const int mode = (w.ctr->nwork * 15ull <= w.mark_limit) ? kMarkList : kMarkBits;
+    if (blockIdx.x == 0 && threadIdx.x == 0) w.ctr->scratch[3] = (unsigned long long)mode;
+    return mode;
+}
+
+__device__ __forceinline__ void flush_acc(const Work& w, const ApplyAcc& a) {
+    const unsigned long long we = __reduce_add_sync(0xffffffffu, (unsigned)a.edits);
+    const unsigned int wm = __reduce_max_sync(0xffffffffu, a.maxc);
+    const unsigned int ws = __reduce_or_sync(0xffffffffu, a.shared ? 1u : 0u);
     if ((threadIdx.x & 31) == 0) {
         if (we) atomicAdd(&w.ctr->nedits, we);
         if (wm) atomicMax(&w.ctr->maxcount, (unsigned long long)wm);
         if (ws) atomicOr(&w.ctr->shared_dirty, 1ull);
+    }
+}
+
+// K2 over the target list (compacted from the touched bitmap after a tiled
+// sweep, or appended by first touch in a sparse sweep).
+template <typename FT>
+__global__ void __launch_bounds__(256) k_apply_list(Dom d, const FT* __restrict__ f, double* __restrict__ g,
+                                                    Work w, int nxt) {
+    const int mark = apply_marks(w);
+    const unsigned long long n = w.ctr->nwork;
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    constexpr int kB = 4;   // targets in flight per thread
+    ApplyAcc acc;
+    for (unsigned long long i0 = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i0 < n;
+         i0 += kB * stride) {
+        int64_t t[kB];
+        bool ok[kB];
+#pragma unroll
+        for (int k = 0; k < kB; ++k) {
+            ok[k] = i0 + k * stride < n;
+            t[k] = ok[k] ? (int64_t)w.work[i0 + k * stride] : 0;
+        }
+        if (w.track) {
+            // sparse lists may repeat a target: the thread that clears its
+            // touched bit owns it (compacted lists have their bits cleared)
+#pragma unroll
+            for (int k = 0; k < kB; ++k) {
+                const uint32_t bit = 1u << (t[k] & 31);
+                if (ok[k]) ok[k] = (atomicAnd(w.touched + (t[k] >> 5), ~bit) & bit) != 0;
+            }
+        }
+        TargetOps ops[kB];
+#pragma unroll
+        for (int k = 0; k < kB; ++k)
+            if (ok[k]) ops[k] = load_target(f, g, w, t[k]);
+#pragma unroll
+        for (int k = 0; k < kB; ++k)
+            if (ok[k]) apply_target(d, f, g, w, t[k], mark, nxt, acc, ops[k]);
+    }
+    flush_acc(w, acc);
+}
+
+// 1-ring marking of the edits of a list-mode iteration: thread i marks ring
+// member (i % 15) of edit (i / 15).
+__global__ void __launch_bounds__(256) k_mark_list(Dom d, Work w, int nxt) {
+    const unsigned long long n = w.ctr->nelist * 15ull;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (unsigned long long)gridDim.x * blockDim.x) {
+        const int64_t v = w.elist[i / 15];
+        const int r = (int)(i % 15) - 1;
+        int64_t x, y, z;
+        coords(d, v, x, y, z);
+        const int64_t px = x + (r < 0 ? 0 : rank_dx(r));
+        const int64_t py = y + (r < 0 ? 0 : rank_dy(r));
+        const int64_t pz = z + (r < 0 ? 0 : rank_dz(r));
+        if (!in_core(d, px, py, pz)) continue;
+        const int64_t u = px + py * d.sy + pz * d.sz;
+        const uint32_t bit = 1u << (u & 31);
+        if (atomicOr(w.actbits + (u >> 5), bit) & bit) continue;
+        const unsigned long long slot = agg_append(&w.ctr->nact[nxt]);
+        if (slot < w.act_cap) w.act[nxt][slot] = (uint32_t)u;
     }
 }
 
