@@ -375,6 +375,7 @@ struct pmsz_plan {
     int next_mode = 0;        // kFull / kMasked / kList for the next iteration
     int last_mode = 0;
     int64_t pending = 0;      // length of the pending dirty list (kList)
+    int64_t ncore = 0;        // centres in the core box
     RingDelta ring_delta{};   // id offsets of the closed 1-ring (dilation)
     bool prepared = false;
     int64_t floor_viol = 0, upper_viol = 0;
@@ -556,7 +557,13 @@ pmsz_status iterate_once(pmsz_plan* p, const void* f, double* g, cudaStream_t s)
     if (st) return st;
     if (p->w.incremental) {
         if (p->hctr->scratch[3] == kMarkBits) {
-            p->next_mode = kMasked;
+            // dirty fraction ~ 15 x edits / core voxels
+            if (15 * (int64_t)p->hctr->nedits > p->ncore / 8) {
+                p->next_mode = kFull;
+                CUDA_TRY(cudaMemsetAsync(p->w.iteredit, 0, p->nwords * 4, s));
+            } else {
+                p->next_mode = kMasked;
+            }
         } else if (p->hctr->nact[nxt] > p->w.act_cap) {
             p->next_mode = kFull;
         } else {
@@ -711,9 +718,12 @@ pmsz_status pmsz_plan_create(const pmsz_desc* desc, pmsz_plan** out) {
     const int64_t ncore = (d.core_hi[0] - d.core_lo[0]) * (d.core_hi[1] - d.core_lo[1]) *
                           (d.core_hi[2] - d.core_lo[2]);
     p->w.act_cap = (unsigned long long)std::max<int64_t>(ncore / 4, 4096);
-    // explicit dirty lists only while they stay below ~1.5% of the core box;
-    // larger dirty sets go through the dilated bitmap and a masked tiled sweep
-    p->w.mark_limit = (unsigned long long)std::max<int64_t>(ncore / 64, 4096);
+    // explicit dirty lists while their ring entries stay below ~6% of the core
+    // box (gathers beat a tiled sweep there); larger dirty sets go through the
+    // edit bitmap: a masked tiled sweep, or a plain full sweep when the dirty
+    // set is so spread that every warp-step would be dirty anyway
+    p->w.mark_limit = (unsigned long long)std::max<int64_t>(ncore / 16, 4096);
+    p->ncore = ncore;
     p->w.nwords = p->nwords;
     {
         int k = 0;
