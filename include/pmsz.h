@@ -203,6 +203,14 @@ pmsz_status pmsz_box_unpack_min(int64_t nx, int64_t ny, int64_t nz, double* dst_
 pmsz_status pmsz_box_unpack_copy(int64_t nx, int64_t ny, int64_t nz, double* dst_dev,
                                  const int64_t lo[3], const int64_t hi[3], const double* buf_dev,
                                  unsigned long long* changed_dev, void* stream);
+/* Ghost merge of a received replica box (_merge_min, parallel.py:122-140):
+ * g[box] = min(g[box], buf) and every vertex that changed dirties its 1-ring
+ * for the next incremental sweep of the plan.  *changed_out = changed vertices. */
+pmsz_status pmsz_box_merge_min(pmsz_plan* plan, double* g_dev, const int64_t lo[3], const int64_t hi[3],
+                               const double* buf_dev, int64_t* changed_out, void* stream);
+/* Detections left at the latest evaluation of every core centre (the
+ * incremental equivalent of the final re-scan, correction.py:424-426). */
+pmsz_status pmsz_residual(pmsz_plan* plan, int64_t* count_out, void* stream);
 /* After a merge: mark the 1-ring of every vertex of box [lo,hi) whose value differs
  * from `before` as dirty for the next incremental sweep. */
 pmsz_status pmsz_box_mark_changed(pmsz_plan* plan, const int64_t lo[3], const int64_t hi[3],

@@ -94,6 +94,8 @@ SIGNATURES = {
     "pmsz_box_unpack_min": (i32, [i64, i64, i64, vp, i64p, i64p, vp, vp, vp]),
     "pmsz_box_unpack_copy": (i32, [i64, i64, i64, vp, i64p, i64p, vp, vp, vp]),
     "pmsz_box_mark_changed": (i32, [vp, i64p, i64p, vp, vp, vp]),
+    "pmsz_box_merge_min": (i32, [vp, vp, i64p, i64p, vp, i64p, vp]),
+    "pmsz_residual": (i32, [vp, i64p, vp]),
     "pmsz_perlin": (i32, [i64p, i64p, i64p, ctypes.POINTER(i32), ctypes.c_double, i32, vp, vp, vp]),
     "pmsz_minmax": (i32, [vp, i32, i64, dp, dp, vp]),
     "pmsz_quantize": (i32, [vp, i32, i64, ctypes.c_double, ctypes.c_double, vp, i64p, vp]),

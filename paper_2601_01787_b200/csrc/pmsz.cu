@@ -307,6 +307,30 @@ __global__ void __launch_bounds__(256) k_box_mark(Dom d, Work w, Box b, const do
     }
 }
 
+// Ghost merge: dst[box] = min(dst[box], buf); changed vertices dirty their
+// 1-ring (list or edit-bitmap, by the plan's pending mode; none if kFull).
+__global__ void __launch_bounds__(256) k_box_merge(Dom d, Work w, Box b, double* __restrict__ g,
+                                                   const double* __restrict__ buf, int cur, int mode,
+                                                   unsigned long long* changed) {
+    const int64_t n = b.ext[0] * b.ext[1] * b.ext[2];
+    unsigned mine = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t z = i / (b.ext[0] * b.ext[1]), r = i - z * b.ext[0] * b.ext[1];
+        const int64_t y = r / b.ext[0], x = r - y * b.ext[0];
+        const int64_t o = (b.lo[0] + x) + b.nx * ((b.lo[1] + y) + b.ny * (b.lo[2] + z));
+        const double cur_v = g[o], in = buf[i];
+        if (in < cur_v) {
+            g[o] = in;
+            ++mine;
+            if (mode == 1) mark_changed(d, w, o, cur, 1);        // masked: edit bitmap
+            else if (mode == 2) mark_changed(d, w, o, cur, 0);   // list
+        }
+    }
+    mine = __reduce_add_sync(0xffffffffu, mine);
+    if ((threadIdx.x & 31) == 0 && mine) atomicAdd(changed, (unsigned long long)mine);
+}
+
 __global__ void __launch_bounds__(256) k_mark_ids(Dom d, Work w, const uint32_t* __restrict__ ids, int64_t n, int cur,
                                                   int bits) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -896,6 +920,33 @@ pmsz_status pmsz_box_mark_changed(pmsz_plan* p, const int64_t lo[3], const int64
     k_box_mark<<<grid_for(n, 256), 256, 0, s>>>(p->dom, p->w, b, before, g, p->cur, p->next_mode == kMasked);
     LAUNCHED();
     return after_mark(p, s);
+}
+
+static bool make_box(int64_t nx, int64_t ny, int64_t nz, const int64_t lo[3], const int64_t hi[3], Box& b);
+
+pmsz_status pmsz_box_merge_min(pmsz_plan* p, double* g, const int64_t lo[3], const int64_t hi[3], const double* buf,
+                               int64_t* changed_out, void* stream) {
+    if (!p || !g || !buf) return fail(PMSZ_ERR_INVALID, "null argument");
+    cudaStream_t s = S(stream);
+    Box b;
+    if (!make_box(p->dom.nx, p->dom.ny, p->dom.nz, lo, hi, b)) return fail(PMSZ_ERR_INVALID, "box outside the domain");
+    const int64_t n = b.ext[0] * b.ext[1] * b.ext[2];
+    CUDA_TRY(cudaMemsetAsync(&p->ctr->changed, 0, sizeof(unsigned long long), s));
+    if (n > 0) {
+        const int mode = !p->w.incremental ? 0 : (p->next_mode == kMasked ? 1 : (p->next_mode == kList ? 2 : 0));
+        ProfScope ps(p, s, PMSZ_K_OTHER);
+        k_box_merge<<<grid_for(n, 256), 256, 0, s>>>(p->dom, p->w, b, g, buf, p->cur, mode, &p->ctr->changed);
+        LAUNCHED();
+    }
+    pmsz_status st = after_mark(p, s);
+    if (st) return st;
+    if (changed_out) *changed_out = (int64_t)p->hctr->changed;
+    return PMSZ_OK;
+}
+
+pmsz_status pmsz_residual(pmsz_plan* p, int64_t* count_out, void* stream) {
+    if (!p || !count_out) return fail(PMSZ_ERR_INVALID, "null argument");
+    return bits_total(p, p->w.detbits, S(stream), count_out);
 }
 
 pmsz_status pmsz_verify(pmsz_plan* p, const double* g, pmsz_result* r, void* stream) {

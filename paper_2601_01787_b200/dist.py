@@ -1,0 +1,316 @@
+"""Multi-GPU correction: one block of ``decompose`` per rank (one process per
+GPU, torch.distributed over NCCL), the reference's block-parallel round loop
+(parallel.py:258-367) with its two strategies:
+
+* relaxed (the paper's pMSz): every rank iterates its block to a local
+  fixpoint, then one allreduce of {round edits, shared_dirty} decides whether
+  a ghost exchange is needed at all (parallel.py:304-314);
+* lockstep (sync-pMSz): one iteration per round, exchange every round.
+
+The ghost exchange is the reference's global min-merge (`_merge_min`,
+parallel.py:122-140) restated pairwise: every pair of ranks whose extended
+blocks overlap exchanges the full overlap box (NCCL send/recv, batched) and
+takes the elementwise minimum.  With full ext overlaps this is exactly the
+global minimum over all replicas.  For z-slabs (the default
+weak-scaling layout) a rank talks to its two neighbours and each overlap is
+two contiguous planes, sent straight from the field without packing.
+
+The loop only needs a small engine interface (round / pack / merge), so the
+same code runs with the device engine (libpmsz plans) under NCCL and with the
+CPU oracle engine (tests/, gloo) -- the multi-rank host logic is tested on CPU.
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import time
+from dataclasses import dataclass
+
+import torch
+import torch.distributed as dist
+
+from .engine import ConvergenceError
+from .parallel import Block, decompose, block_domain
+
+
+@dataclass(frozen=True)
+class Exchange:
+    """One neighbour of this rank: the overlap box in this rank's ext coords."""
+
+    peer: int
+    lo: tuple[int, int, int]
+    hi: tuple[int, int, int]
+
+    @property
+    def size(self) -> int:
+        return (self.hi[0] - self.lo[0]) * (self.hi[1] - self.lo[1]) * (self.hi[2] - self.lo[2])
+
+
+def exchanges(blocks: tuple[Block, ...], rank: int) -> list[Exchange]:
+    """Overlaps of rank's ext extent with every other ext extent (ascending peer)."""
+    me = blocks[rank]
+    out = []
+    for q, other in enumerate(blocks):
+        if q == rank:
+            continue
+        lo = tuple(max(me.ext_start[a], other.ext_start[a]) for a in range(3))
+        hi = tuple(min(me.ext_stop[a], other.ext_stop[a]) for a in range(3))
+        if all(hi[a] > lo[a] for a in range(3)):
+            out.append(Exchange(q, tuple(lo[a] - me.ext_start[a] for a in range(3)),
+                                tuple(hi[a] - me.ext_start[a] for a in range(3))))
+    return out
+
+
+@dataclass
+class DistStats:
+    strategy: str
+    block_grid: tuple[int, int, int]
+    rounds: int
+    syncs: int
+    edits_per_round: tuple[int, ...]
+    iterations: int            # this rank's block iterations
+    edit_total: int            # this rank's edits
+    max_vertex_edits: int      # this rank's max per-vertex edit count
+    exchanged_bytes: int       # bytes this rank sent
+
+
+def run_distributed(engine, blocks, grid, rank: int, lockstep: bool, cap: int, group=None) -> DistStats:
+    """The round loop of run_parallel (parallel.py:289-322) across ranks."""
+    xs = exchanges(blocks, rank)
+    dev = engine.device
+    rounds = syncs = 0
+    totals: list[int] = []
+    sent = 0
+    while True:
+        if rounds >= cap:
+            raise ConvergenceError(f"no terminal round within {cap}")
+        rounds += 1
+        e, dirty = engine.round(lockstep)
+        t = torch.tensor([e, int(dirty)], dtype=torch.int64, device=dev)
+        dist.all_reduce(t, group=group)
+        round_edits, any_dirty = (int(v) for v in t.tolist())
+        totals.append(round_edits)
+        if not lockstep and (round_edits == 0 or any_dirty == 0):
+            break
+        # ghost exchange: send my replica of every overlap, min-merge theirs
+        recv = {x.peer: engine.empty(x) for x in xs}
+        ops = []
+        for x in xs:
+            buf = engine.pack(x)
+            sent += buf.numel() * buf.element_size()
+            ops.append(dist.P2POp(dist.isend, buf, x.peer, group=group))
+            ops.append(dist.P2POp(dist.irecv, recv[x.peer], x.peer, group=group))
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+        changed = 0
+        for x in xs:
+            changed += engine.merge(x, recv[x.peer])
+        syncs += 1
+        if lockstep:
+            c = torch.tensor([changed], dtype=torch.int64, device=dev)
+            dist.all_reduce(c, group=group)
+            if round_edits == 0 and int(c.item()) == 0:
+                break
+    it, et, mve = engine.block_stats()
+    return DistStats("lockstep" if lockstep else "relaxed", tuple(int(v) for v in grid), rounds, syncs,
+                     tuple(totals), it, et, mve, sent)
+
+
+def run_local(engines, blocks, grid, lockstep: bool, cap: int) -> DistStats:
+    """The same round loop with every block's engine in this process (one
+    device): the pairwise exchanges of run_distributed without a process
+    group.  Used to test the device engines' pack/merge on one GPU."""
+    xs = [exchanges(blocks, r) for r in range(len(blocks))]
+    rounds = syncs = 0
+    totals: list[int] = []
+    sent = 0
+    while True:
+        if rounds >= cap:
+            raise ConvergenceError(f"no terminal round within {cap}")
+        rounds += 1
+        res = [e.round(lockstep) for e in engines]
+        round_edits = sum(r[0] for r in res)
+        any_dirty = any(r[1] for r in res)
+        totals.append(round_edits)
+        if not lockstep and (round_edits == 0 or not any_dirty):
+            break
+        packed = {(r, x.peer): engines[r].pack(x).clone() for r in range(len(blocks)) for x in xs[r]}
+        changed = 0
+        for r in range(len(blocks)):
+            for x in xs[r]:
+                buf = packed[(x.peer, r)]          # the peer's replica of the same overlap
+                sent += buf.numel() * buf.element_size()
+                changed += engines[r].merge(x, buf)
+        syncs += 1
+        if lockstep and round_edits == 0 and changed == 0:
+            break
+    return DistStats("lockstep" if lockstep else "relaxed", tuple(int(v) for v in grid), rounds, syncs,
+                     tuple(totals), 0, 0, 0, sent)
+
+
+class DeviceEngine:
+    """One rank's block on its GPU: a libpmsz plan over the ext extent."""
+
+    def __init__(self, block: Block, gdims, f_ext: torch.Tensor, fhat_ext: torch.Tensor, config):
+        from .engine import DomainPlan, raise_for
+        from . import _native as N
+        self.block = block
+        self.spec = block_domain(block, gdims)
+        self.device = f_ext.device
+        self.f = f_ext
+        self.fh = fhat_ext
+        self.config = config
+        self.plan = DomainPlan(self.spec, config.xi_abs, config.tau, config.max_outer_iterations,
+                               incremental=True, f32_original=f_ext.dtype == torch.float32)
+        self.g = torch.empty_like(fhat_ext)
+        self._N = N
+        self._raise = raise_for
+        self.last = None
+
+    def prepare(self):
+        st, res = self.plan.prepare(self.f, self.fh, self.g)
+        self._raise(st, res, None, None, self.config.xi_abs, f_dev=self.f, fhat_dev=self.fh)
+
+    def round(self, lockstep: bool):
+        st, e, res = self.plan.block_round(self.f, self.g, lockstep)
+        if st == self._N.PMSZ_ERR_CONVERGENCE:
+            raise ConvergenceError(f"block {self.block.index} found no zero-edit iteration")
+        self._raise(st, res)
+        self.last = res
+        return e, bool(res.shared_dirty)
+
+    def _dims(self):
+        return self.spec.dims
+
+    def _is_planes(self, x: Exchange) -> bool:
+        nx, ny, _ = self.spec.dims
+        return x.lo[0] == 0 and x.lo[1] == 0 and x.hi[0] == nx and x.hi[1] == ny
+
+    def empty(self, x: Exchange) -> torch.Tensor:
+        return torch.empty(x.size, dtype=torch.float64, device=self.device)
+
+    def pack(self, x: Exchange) -> torch.Tensor:
+        nx, ny, nz = self.spec.dims
+        if self._is_planes(x):   # z-slab overlaps are contiguous planes
+            return self.g[x.lo[2] * nx * ny: x.hi[2] * nx * ny]
+        buf = self.empty(x)
+        self._N.check(self._N.lib().pmsz_box_pack(nx, ny, nz, self._N.ptr(self.g), self._N.ivec(x.lo),
+                                                   self._N.ivec(x.hi), self._N.ptr(buf), self._N.stream_handle()),
+                      "pmsz_box_pack")
+        return buf
+
+    def merge(self, x: Exchange, buf: torch.Tensor) -> int:
+        return self.plan.merge_min(self.g, x.lo, x.hi, buf)
+
+    def block_stats(self):
+        r = self.last
+        return (int(r.iterations), int(r.edit_count), int(r.max_vertex_edits)) if r is not None else (0, 0, 0)
+
+    def residual(self) -> int:
+        return self.plan.residual()
+
+
+# ---------------------------------------------------------------------------
+# bench.py --gpus N (torchrun): weak scaling, 512^3 per GPU, z-slabs
+def bench_main(args, metric, unit, ClockSampler, measured_peaks, cpu_sample_inputs, time_cpu_oracle):
+    import paper_2601_01787_b200 as pm
+    from . import _native as N
+    from . import inputs as gen
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if not dist.is_initialized():
+        dist.init_process_group("nccl", device_id=dev)
+    S = args.size
+    gdims = (S, S, S * world)
+    grid = (1, 1, world)
+    blocks = decompose(gdims, grid).blocks
+    blk = blocks[rank]
+    ext = blk.ext_dims
+    spec = gen.NoiseSpec(gdims, args.seed)
+    f32 = gen.perlin_device(spec, lo=blk.ext_start, ext=ext, f32=True, device=dev)
+    lo, hi = gen.minmax_device(f32)
+    mm = torch.tensor([-lo, hi], dtype=torch.float64, device=dev)
+    dist.all_reduce(mm, op=dist.ReduceOp.MAX)
+    glo, ghi = -float(mm[0].item()), float(mm[1].item())
+    xi = gen.relative_to_absolute_range(glo, ghi, args.rel)
+    fh = gen.quantize_device(f32, xi, glo, ghi)
+    cfg = pm.CorrectionConfig(xi_abs=xi)
+    eng = DeviceEngine(blk, gdims, f32, fh, cfg)
+    lockstep = args.strategy == "lockstep"
+    cap = cfg.max_outer_iterations
+
+    def step():
+        eng.prepare()
+        return run_distributed(eng, blocks, grid, rank, lockstep, cap)
+
+    for _ in range(max(args.warmup, 3)):
+        st = step()
+    torch.cuda.synchronize()
+    eng.plan.profile(True)
+    eng.plan.profile_read(reset=True)
+    launches0 = N.launch_count()
+    clocks = ClockSampler(local)
+    clocks.start()
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        st = step()
+    e1.record()
+    torch.cuda.synchronize()
+    dist.barrier()
+    clk = clocks.stop()
+    ms_local = e0.elapsed_time(e1) / args.steps
+    launches = N.launch_count() - launches0
+    prof = eng.plan.profile_read(reset=True)
+    eng.plan.profile(False)
+    t = torch.tensor([ms_local], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    residual = torch.tensor([eng.residual()], dtype=torch.int64, device=dev)
+    dist.all_reduce(residual)
+    per_rank = [None] * world
+    dist.all_gather_object(per_rank, {"rank": rank, "iterations": st.iterations, "edits": st.edit_total,
+                                      "max_vertex_edits": st.max_vertex_edits, "ms": ms_local,
+                                      "sent_bytes_per_step": st.exchanged_bytes, "clocks": clk})
+    nvox = S * S * S * world
+    if rank == 0:
+        peaks = measured_peaks()
+        peak = float(peaks.get("hbm_gbs", 6650.0))
+        kernels = {}
+        per_voxel = {"sweep_full": 9, "sweep_masked": 9, "prep": 4 + 8 + 8 + 1}
+        core = S ** 3
+        for name, (kms, cnt) in prof.items():
+            if cnt == 0:
+                continue
+            entry = {"ms_total_per_step": kms / args.steps, "launches_per_step": cnt / args.steps,
+                     "ms_per_launch": kms / cnt}
+            if name in per_voxel:
+                gbs = per_voxel[name] * core / (kms / cnt / 1e3) / 1e9
+                entry.update({"achieved_gbs": gbs, "frac": gbs / peak})
+            kernels[name] = entry
+        dk = kernels.get("sweep_full", {})
+        line = {"metric": metric, "value": nvox / (ms / 1e3), "unit": unit, "n_gpus": world, "steps": args.steps,
+                "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic (Perlin seed 0 f32 + quantizer, on device)",
+                "config": {"workload": f"perlin {S}^3 per GPU, global {gdims}, rel {args.rel:g}, quantizer",
+                           "decomposition": f"z-slabs {grid}", "strategy": st.strategy,
+                           "parallelism": f"block-parallel x{world} (NCCL ghost exchange)",
+                           "xi_abs": xi, "l2": "inputs > L2"},
+                "roofline": {"bound": "hbm", "kernel": "sweep_full (rank 0)", "achieved": dk.get("achieved_gbs"),
+                             "peak": peak, "unit": "GB/s", "frac": dk.get("frac"), "traffic": None,
+                             "per_kernel": kernels},
+                "clocks": clk, "gpu_launches": launches,
+                "result": {"rounds": st.rounds, "syncs": st.syncs, "edits_per_round": list(st.edits_per_round),
+                           "residual": int(residual.item()), "per_rank": per_rank}}
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+    return 0

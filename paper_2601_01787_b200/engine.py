@@ -162,6 +162,18 @@ class DomainPlan:
                                                 N.stream_handle(stream)), "pmsz_bounds_violations")
         return int(out.value)
 
+    def merge_min(self, g, lo, hi, buf, stream=None) -> int:
+        """Ghost merge of a received replica box; changed vertices dirty their ring."""
+        out = ctypes.c_int64()
+        N.check(self.lib.pmsz_box_merge_min(self.handle, N.ptr(g), N.ivec(lo), N.ivec(hi), N.ptr(buf),
+                                            ctypes.byref(out), N.stream_handle(stream)), "pmsz_box_merge_min")
+        return int(out.value)
+
+    def residual(self, stream=None) -> int:
+        out = ctypes.c_int64()
+        N.check(self.lib.pmsz_residual(self.handle, ctypes.byref(out), N.stream_handle(stream)), "pmsz_residual")
+        return int(out.value)
+
     def mark_all_dirty(self):
         N.check(self.lib.pmsz_mark_all_dirty(self.handle, None), "pmsz_mark_all_dirty")
 

@@ -245,3 +245,44 @@ def test_launches_are_counted():
     xi = orc.relative_to_absolute(f, 1e-2)
     pm.run_correction(sf((16, 16, 16), f), sf((16, 16, 16), orc.quantize(f, xi)), pm.CorrectionConfig(xi_abs=xi))
     assert N.launch_count() > before
+
+
+# --- multi-rank engines (dist.py) on one device -----------------------------
+@pytest.mark.parametrize("idx", range(18))
+def test_device_engines_pairwise_exchange_match_reference(golden, idx):
+    """dist.run_local: per-block DeviceEngines exchanging full ext overlaps
+    pairwise (the NCCL path's data movement) == the reference run_parallel."""
+    from paper_2601_01787_b200 import dist as pdist
+    meta, _ = golden
+    case = meta["parallel"][idx]
+    dims = tuple(case["dims"])
+    grid = tuple(case["grid"])
+    f = orc.perlin(dims, case["seed"])
+    fh = orc.quantize(f, case["xi"])
+    cfg = pm.CorrectionConfig(xi_abs=case["xi"])
+    nx, ny, nz = dims
+    blocks = pm.decompose(dims, grid).blocks
+    fz, hz = f.reshape(nz, ny, nx), fh.reshape(nz, ny, nx)
+    engines = []
+    for b in blocks:
+        fe = torch.from_numpy(np.ascontiguousarray(fz[b.ext_slices_zyx()]).reshape(-1)).to(DEV)
+        he = torch.from_numpy(np.ascontiguousarray(hz[b.ext_slices_zyx()]).reshape(-1)).to(DEV)
+        e = pdist.DeviceEngine(b, dims, fe, he, cfg)
+        e.prepare()
+        engines.append(e)
+    st = pdist.run_local(engines, blocks, grid, case["strategy"] == "lockstep", cfg.max_outer_iterations)
+    ref = case["stats"]
+    assert (st.rounds, st.syncs) == (ref["rounds"], ref["syncs"])
+    assert list(st.edits_per_round) == case["edits_per_iteration"]
+    assert [e.block_stats()[0] for e in engines] == ref["per_block_iterations"]
+    assert [e.block_stats()[1] for e in engines] == ref["per_block_edit_totals"]
+    assert [e.block_stats()[2] for e in engines] == ref["per_block_max_vertex_edits"]
+    g = np.empty((nz, ny, nx))
+    for b, e in zip(blocks, engines):
+        sp = e.spec
+        ed = sp.dims
+        v = e.g.cpu().numpy().reshape(ed[2], ed[1], ed[0])
+        g[b.core_slices_zyx()] = v[sp.core_lo[2]:sp.core_hi[2], sp.core_lo[1]:sp.core_hi[1],
+                                   sp.core_lo[0]:sp.core_hi[0]]
+        assert e.residual() == 0
+    assert sha(g.reshape(-1)) == case["corrected_sha256"], case["name"]
