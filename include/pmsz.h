@@ -51,7 +51,9 @@ enum {
 enum {
     PMSZ_FLAG_INCREMENTAL = 1,   /* dirty-ring sweeps after the first (exact) */
     PMSZ_FLAG_EXTREMA_ONLY = 2,  /* drop the two order kinds (BASELINE config 5) */
-    PMSZ_FLAG_F32_ORIGINAL = 4   /* f is passed as float32 (exact promotion) */
+    PMSZ_FLAG_F32_ORIGINAL = 4,  /* f is passed as float32 (exact promotion) */
+    PMSZ_FLAG_HOST_LOOP = 8      /* no device-resident tail: every iteration is launched
+                                    and synchronised from the host (A/B and tests) */
 };
 
 /* Distortion kinds, in the reference declaration order (correction.py:133-139). */
@@ -116,6 +118,7 @@ int64_t pmsz_launch_count(void);
 enum {
     PMSZ_K_PREP = 0, PMSZ_K_SWEEP_FULL = 1, PMSZ_K_SWEEP_SPARSE = 2, PMSZ_K_APPLY = 3,
     PMSZ_K_VERIFY = 4, PMSZ_K_COMPACT = 5, PMSZ_K_OTHER = 6, PMSZ_K_SWEEP_MASKED = 7, PMSZ_K_DEFER = 8,
+    PMSZ_K_TAIL = 9,   /* persistent list-mode iterations (one cooperative launch) */
     PMSZ_K_COUNT = 10
 };
 
@@ -146,7 +149,9 @@ pmsz_status pmsz_run_correction(pmsz_plan* plan, const void* f_dev, const double
  * The same call with HOST buffers (the end-to-end drop-in): copies f and fhat
  * in, runs, and writes the corrected field and the edit set back to the host.
  * g_host may be NULL (edit set only); ids_host/vals_host receive up to
- * edits_cap edits (EditSet.diff, correction.py:363-369).
+ * edits_cap edits (EditSet.diff, correction.py:363-369).  The device staging
+ * (12 or 16 bytes per voxel plus the edit record) is owned by the plan,
+ * allocated on the first call and reused.
  */
 pmsz_status pmsz_run_correction_host(pmsz_plan* plan, const void* f_host, const double* fhat_host,
                                      double* g_host, int64_t* ids_host, double* vals_host,

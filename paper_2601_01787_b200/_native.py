@@ -31,11 +31,12 @@ PMSZ_CONV_RESIDUAL = 3
 K_PREP, K_SWEEP_FULL, K_SWEEP_SPARSE, K_APPLY, K_VERIFY, K_COMPACT, K_OTHER, K_SWEEP_MASKED, K_DEFER = range(9)
 K_COUNT = 10
 K_NAMES = ("prep", "sweep_full", "sweep_sparse", "apply", "verify", "compact", "other", "sweep_masked",
-           "defer", "spare")
+           "defer", "tail")
 
 FLAG_INCREMENTAL = 1
 FLAG_EXTREMA_ONLY = 2
 FLAG_F32_ORIGINAL = 4
+FLAG_HOST_LOOP = 8
 
 i64 = ctypes.c_int64
 i32 = ctypes.c_int32

@@ -44,7 +44,15 @@ struct Dom {
     int32_t shl[3], shh[3]; // shared band widths (block mode)
     double xi, tau;
     int extrema_only;
+    // exact 32-bit division by the strides (ids < 2^32): q = umulhi64(m, c)
+    // with m = ceil(2^64 / stride) (Lemire-Kaser-Kurz); 0 encodes stride 1
+    uint64_t msy, msz;
 };
+
+__host__ __device__ inline uint64_t div_magic(uint64_t dv) { return dv <= 1 ? 0 : ~0ull / dv + 1; }
+__device__ __forceinline__ uint32_t fast_div(uint32_t c, uint64_t m) {
+    return m ? (uint32_t)__umul64hi(m, (uint64_t)c) : c;
+}
 
 __device__ __forceinline__ double nan64() { return __longlong_as_double(0x7ff8000000000000ll); }
 
@@ -118,10 +126,13 @@ __device__ __forceinline__ Scan fold_scan(double vc, const double (&nv)[14]) {
 }
 
 __device__ __forceinline__ void coords(const Dom& d, int64_t c, int64_t& x, int64_t& y, int64_t& z) {
-    z = c / d.sz;
-    int64_t r = c - z * d.sz;
-    y = r / d.sy;
-    x = r - y * d.sy;
+    const uint32_t cc = (uint32_t)c;
+    const uint32_t zz = fast_div(cc, d.msz);
+    const uint32_t r = cc - zz * (uint32_t)d.sz;
+    const uint32_t yy = fast_div(r, d.msy);
+    x = (int64_t)(r - yy * (uint32_t)d.sy);
+    y = (int64_t)yy;
+    z = (int64_t)zz;
 }
 
 __device__ __forceinline__ bool in_dom(const Dom& d, int64_t x, int64_t y, int64_t z) {

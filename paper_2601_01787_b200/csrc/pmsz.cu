@@ -14,6 +14,7 @@
 //   counts u16[N]   per-vertex edit counts (max_vertex_edits)
 #include <cuda_runtime.h>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -25,6 +26,7 @@
 #include "sweep.cuh"
 #include "gen.cuh"
 #include "tiles.cuh"
+#include "tail.cuh"
 
 using namespace pmsz;
 
@@ -412,6 +414,20 @@ struct pmsz_plan {
     std::vector<int> prof_cls;          // class per recorded pair
     double prof_ms[PMSZ_K_COUNT] = {};
     long long prof_n[PMSZ_K_COUNT] = {};
+    // device-resident tail (k_tail)
+    bool tail_on = true;
+    TailState* tail = nullptr;
+    TailState* htail = nullptr;          // pinned mirror
+    unsigned long long* thist = nullptr;  // per-iteration edits of one tail launch
+    unsigned long long* hthist = nullptr; // pinned mirror
+    int tail_blocks[2] = {0, 0};          // cooperative grid per FT (f64, f32)
+    int64_t sort_min = 65536;             // dirty lists above this are sorted (compacted from actbits)
+    // host-buffer entry point staging (pmsz_run_correction_host)
+    void* stage_f = nullptr;
+    double* stage_g = nullptr;
+    int64_t* stage_ids = nullptr;
+    double* stage_vals = nullptr;
+    int64_t stage_cap = 0;
 };
 
 namespace {
@@ -426,6 +442,8 @@ Dom make_dom(const pmsz_desc& d) {
     }
     o.xi = d.xi; o.tau = d.tau;
     o.extrema_only = (d.flags & PMSZ_FLAG_EXTREMA_ONLY) ? 1 : 0;
+    o.msy = div_magic((uint64_t)o.sy);
+    o.msz = div_magic((uint64_t)o.sz);
     return o;
 }
 
@@ -487,6 +505,19 @@ void launch_bits_total(pmsz_plan* p, const uint32_t* bits, unsigned long long* d
     LAUNCHED();
     k_exclusive_scan<<<1, 1024, 0, s>>>(p->block_counts, p->nblocks_compact, dst);
     LAUNCHED();
+}
+
+// A large pending dirty list is replaced by the ascending compaction of actbits
+// (the same set; the bits are cleared on the way): neighbouring threads then
+// gather neighbouring cache lines instead of one ring after another.
+int sort_pending(pmsz_plan* p, cudaStream_t s) {
+    if (p->pending <= p->sort_min) return 0;
+    ProfScope ps(p, s, PMSZ_K_COMPACT);
+    launch_bits_total(p, p->w.actbits, &p->ctr->nact[p->cur], s);
+    k_bits_list<<<(unsigned)p->nblocks_compact, kCompactThreads, 0, s>>>(p->w.actbits, p->nwords, p->block_counts,
+                                                                       p->w.act[p->cur], 1);
+    LAUNCHED();
+    return 1;
 }
 
 template <typename FT>
@@ -565,10 +596,11 @@ pmsz_status iterate_once(pmsz_plan* p, const void* f, double* g, cudaStream_t s)
         LAUNCHED();
     }
     if (mode == kList) {
+        const int sorted = sort_pending(p, s);
         ProfScope ps(p, s, PMSZ_K_SWEEP_SPARSE);
         p->w.track = 1;
         const int64_t m = std::min<int64_t>(p->pending, (int64_t)p->w.act_cap);
-        k_sweep_sparse<<<grid_for(m, 256, 8), 256, 0, s>>>(d, g, p->w, p->cur);
+        k_sweep_sparse<<<grid_for(m, 256, 8), 256, 0, s>>>(d, g, p->w, p->cur, sorted);
         LAUNCHED();
         apply_bound = std::min<int64_t>(p->n, 15 * m + 32);
     }
@@ -597,6 +629,115 @@ pmsz_status iterate_once(pmsz_plan* p, const void* f, double* g, cudaStream_t s)
         }
     }
     return PMSZ_OK;
+}
+
+// ---- device-resident tail ---------------------------------------------------
+void fill_result(pmsz_plan* p, pmsz_result* r);
+
+bool tail_ok(const pmsz_plan* p) {
+    return p->tail_on && p->w.incremental && p->next_mode == kList && p->floor_viol == 0 &&
+           p->w.edited_mask == nullptr;
+}
+
+template <typename FT>
+pmsz_status launch_tail(pmsz_plan* p, const void* f, double* g, cudaStream_t s, long long budget, int sorted) {
+    int& nb = p->tail_blocks[std::is_same<FT, float>::value ? 1 : 0];
+    if (nb == 0) {
+        int per = 0;
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_tail<FT>, 256, 0));
+        if (per < 1) return fail(PMSZ_ERR_CUDA, "k_tail cannot be resident");
+        nb = std::min(per, 4) * num_sms();
+    }
+    unsigned long long sort_min = (unsigned long long)p->sort_min;
+    Dom d = p->dom;
+    const FT* fp = (const FT*)f;
+    Work w = p->w;
+    int cur = p->cur;
+    unsigned long long* h = p->thist;
+    TailState* t = p->tail;
+    // PMSZ_TAIL_TRACE=1: per-iteration device timestamps printed to stderr
+    // (diagnostics only; synchronises after the launch)
+    unsigned long long* tr = nullptr;
+    static const bool trace = getenv("PMSZ_TAIL_TRACE") != nullptr;
+    static unsigned long long* trace_buf = nullptr;
+    if (trace) {
+        if (!trace_buf) CUDA_TRY(cudaMalloc(&trace_buf, 2 * 8 * 4096));
+        tr = trace_buf;
+        CUDA_TRY(cudaMemsetAsync(tr, 0, 2 * 8 * 4096, s));
+    }
+    void* args[] = {&d, &fp, &g, &w, &cur, &sorted, &sort_min, &budget, &h, &t, &tr};
+    CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_tail<FT>, dim3(nb), dim3(256), args, 0, s));
+    LAUNCHED();
+    if (trace) {
+        std::vector<unsigned long long> h2(2 * 4096);
+        cudaMemcpyAsync(h2.data(), tr, h2.size() * 8, cudaMemcpyDeviceToHost, s);
+        cudaStreamSynchronize(s);
+        fprintf(stderr, "tail nb=%d cur=%d pending=%lld:", nb, cur, (long long)p->pending);
+        for (int i = 0; i < 4000 && h2[2 * i]; ++i)
+            fprintf(stderr, " %.1fus/%llu", (h2[2 * i] - (i ? h2[2 * i - 2] : h2[8190])) / 1e3, h2[2 * i + 1]);
+        fprintf(stderr, "\n  phases S/A/M of the first iterations:");
+        for (int i = 0; i < 4 && h2[2 * i]; ++i) {
+            const unsigned long long t0 = i ? h2[2 * i - 2] : h2[8190];
+            fprintf(stderr, " [%.1f %.1f %.1f]", (h2[8000 + 2 * i] - t0) / 1e3, (h2[8001 + 2 * i] - h2[8000 + 2 * i]) / 1e3,
+                    (h2[2 * i] - h2[8001 + 2 * i]) / 1e3);
+        }
+        fprintf(stderr, "\n");
+    }
+    return PMSZ_OK;
+}
+
+// Run up to `budget` list-mode iterations in one k_tail launch and bring the
+// plan state to where iterate_once would have left it.  Per-iteration edit
+// counts land in p->hthist[0 .. *k).
+pmsz_status tail_step(pmsz_plan* p, const void* f, double* g, cudaStream_t s, long long budget, int64_t* k,
+                      bool* shared_any) {
+    pmsz_status st = reset_iter(p, s, p->cur ^ 1);
+    if (st) return st;
+    const int sorted = sort_pending(p, s);
+    {
+        ProfScope ps(p, s, PMSZ_K_TAIL);
+        st = p->f32 ? launch_tail<float>(p, f, g, s, budget, sorted) : launch_tail<double>(p, f, g, s, budget, sorted);
+        if (st) return st;
+    }
+    CUDA_TRY(cudaMemcpyAsync(p->htail, p->tail, sizeof(TailState), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(p->hthist, p->thist, sizeof(unsigned long long) * budget, cudaMemcpyDeviceToHost, s));
+    st = sync_counters(p, s);
+    if (st) return st;
+    const TailState& ts = *p->htail;
+    *k = (int64_t)ts.iterations;
+    *shared_any = ts.shared_or != 0;
+    p->iterations += *k;
+    for (int64_t i = 0; i < *k; ++i) p->edit_total += (int64_t)p->hthist[i];
+    p->last_mode = kList;
+    switch (ts.exit) {
+    case kTailBits:   // the last iteration's edits went to the edit bitmap
+        if (15 * (int64_t)ts.last_edits > p->ncore / 8) {
+            p->next_mode = kFull;
+            CUDA_TRY(cudaMemsetAsync(p->w.iteredit, 0, p->nwords * 4, s));
+        } else {
+            p->next_mode = kMasked;
+        }
+        break;
+    case kTailOverflow:
+        p->next_mode = kFull;
+        break;
+    default:          // converged or budget spent: the next list is pending
+        p->next_mode = kList;
+        p->cur = (int)ts.cur;
+        p->pending = (int64_t)ts.pending;
+    }
+    return PMSZ_OK;
+}
+
+void tail_result(pmsz_plan* p, pmsz_result* r, int64_t k) {
+    if (!r) return;
+    fill_result(p, r);
+    r->last_edits = (int64_t)p->htail->last_edits;
+    r->last_detections = (int64_t)p->htail->last_detect;
+    r->shared_dirty = p->htail->shared_or ? 1 : 0;
+    r->iterations = p->iterations;
+    r->edit_count = p->edit_total;
+    r->sparse_sweeps += k;
 }
 
 pmsz_status reset_run_state(pmsz_plan* p, cudaStream_t s) {
@@ -769,7 +910,13 @@ pmsz_status pmsz_plan_create(const pmsz_desc* desc, pmsz_plan** out) {
         ok = alloc((void**)&p->w.actbits, p->nwords * 4) && alloc((void**)&p->w.act[0], p->w.act_cap * 4) &&
              alloc((void**)&p->w.act[1], p->w.act_cap * 4) && alloc((void**)&p->w.iteredit, p->nwords * 4) &&
              alloc((void**)&p->w.elist, p->w.mark_limit * 4);
-    if (ok) ok = cudaMallocHost((void**)&p->hctr, sizeof(DevCounters)) == cudaSuccess;
+    const int64_t hist_n = std::max<int64_t>(d.max_iterations, 1);
+    if (ok) ok = alloc((void**)&p->tail, sizeof(TailState)) && alloc((void**)&p->thist, hist_n * 8);
+    if (ok) ok = cudaMallocHost((void**)&p->hctr, sizeof(DevCounters)) == cudaSuccess &&
+                 cudaMallocHost((void**)&p->htail, sizeof(TailState)) == cudaSuccess &&
+                 cudaMallocHost((void**)&p->hthist, hist_n * 8) == cudaSuccess;
+    p->tail_on = (d.flags & PMSZ_FLAG_HOST_LOOP) == 0;
+    if (const char* e = getenv("PMSZ_SORT_MIN")) p->sort_min = atoll(e);
     if (!ok) {
         cudaGetLastError();
         pmsz_plan_destroy(p);
@@ -794,6 +941,10 @@ void pmsz_plan_destroy(pmsz_plan* p) {
     cudaFree(p->w.actbits); cudaFree(p->w.act[0]); cudaFree(p->w.act[1]); cudaFree(p->w.iteredit);
     cudaFree(p->w.elist);
     if (p->hctr) cudaFreeHost(p->hctr);
+    cudaFree(p->tail); cudaFree(p->thist);
+    if (p->htail) cudaFreeHost(p->htail);
+    if (p->hthist) cudaFreeHost(p->hthist);
+    cudaFree(p->stage_f); cudaFree(p->stage_g); cudaFree(p->stage_ids); cudaFree(p->stage_vals);
     for (cudaEvent_t e : p->prof_ev) cudaEventDestroy(e);
     delete p;
 }
@@ -866,6 +1017,22 @@ pmsz_status pmsz_block_round(pmsz_plan* p, const void* f, double* g, int32_t loc
     int64_t total = 0;
     bool dirty = false;
     for (int64_t it = 0; it < p->desc.max_iterations; ++it) {
+        if (!lockstep && tail_ok(p)) {
+            int64_t k = 0;
+            bool sh = false;
+            pmsz_status st = tail_step(p, f, g, S(stream), p->desc.max_iterations - it, &k, &sh);
+            if (st) { restore_prop(p, S(stream)); return st; }
+            tail_result(p, r, k);
+            for (int64_t i = 0; i < k; ++i) total += (int64_t)p->hthist[i];
+            dirty = dirty || sh;
+            it += k - 1;
+            if (p->htail->last_edits == 0) {
+                if (round_edits) *round_edits = total;
+                if (r) r->shared_dirty = dirty;
+                return PMSZ_OK;
+            }
+            continue;
+        }
         pmsz_status st = pmsz_iterate(p, f, g, nullptr, r, stream);
         if (st) return st;
         const int64_t e = (int64_t)p->hctr->nedits;
@@ -978,6 +1145,19 @@ pmsz_status pmsz_run_correction(pmsz_plan* p, const void* f, const double* fh, d
     bool converged = false;
     int64_t it = 0;
     for (; it < p->desc.max_iterations; ++it) {
+        if (tail_ok(p)) {
+            int64_t k = 0;
+            bool sh = false;
+            st = tail_step(p, f, g, s, p->desc.max_iterations - it, &k, &sh);
+            if (st) { restore_prop(p, s); return st; }
+            tail_result(p, r, k);
+            for (int64_t i = 0; i < k; ++i)
+                if (history && it + i < history_cap) history[it + i] = (int64_t)p->hthist[i];
+            it += k;
+            if (p->htail->last_edits == 0) { converged = true; break; }
+            --it;   // the loop increment
+            continue;
+        }
         st = pmsz_iterate(p, f, g, nullptr, r, stream);
         if (st) return st;
         const int64_t e = (int64_t)p->hctr->nedits;
@@ -1050,13 +1230,19 @@ pmsz_status pmsz_run_correction_host(pmsz_plan* p, const void* f_host, const dou
     if (!p || !f_host || !fh_host) return fail(PMSZ_ERR_INVALID, "null argument");
     cudaStream_t s = S(stream);
     const size_t fbytes = p->n * (p->f32 ? 4 : 8), gbytes = p->n * 8;
-    void* f = nullptr;
-    double* g = nullptr;
-    int64_t* ids = nullptr;
-    double* vals = nullptr;
+    // device staging owned by the plan (allocated on first use, reused: a
+    // per-call allocation would remap ~12 bytes/voxel of device memory)
+    auto grow = [&](void** ptr, size_t bytes) -> bool {
+        if (*ptr) return true;
+        if (cudaMalloc(ptr, bytes) != cudaSuccess) { cudaGetLastError(); return false; }
+        p->scratch_bytes += (int64_t)bytes;
+        return true;
+    };
+    if (!grow(&p->stage_f, fbytes) || !grow((void**)&p->stage_g, gbytes))
+        return fail(PMSZ_ERR_CUDA, "staging allocation failed");
+    void* f = p->stage_f;
+    double* g = p->stage_g;
     pmsz_status st = PMSZ_OK;
-    CUDA_TRY(cudaMallocAsync(&f, fbytes, s));
-    CUDA_TRY(cudaMallocAsync((void**)&g, gbytes, s));
     CUDA_TRY(cudaMemcpyAsync(f, f_host, fbytes, cudaMemcpyHostToDevice, s));
     CUDA_TRY(cudaMemcpyAsync(g, fh_host, gbytes, cudaMemcpyHostToDevice, s));
     st = pmsz_run_correction(p, f, g, g, history, history_cap, r, stream);
@@ -1064,19 +1250,25 @@ pmsz_status pmsz_run_correction_host(pmsz_plan* p, const void* f_host, const dou
         if (g_host) CUDA_TRY(cudaMemcpyAsync(g_host, g, gbytes, cudaMemcpyDeviceToHost, s));
         if (ids_host && vals_host && edits_cap > 0 && r && r->edit_count > 0) {
             const int64_t m = std::min(edits_cap, r->edit_count);
-            CUDA_TRY(cudaMallocAsync((void**)&ids, m * 8, s));
-            CUDA_TRY(cudaMallocAsync((void**)&vals, m * 8, s));
-            st = pmsz_edits_export(p, g, ids, vals, m, nullptr, stream);
-            if (st == PMSZ_OK) {
-                CUDA_TRY(cudaMemcpyAsync(ids_host, ids, m * 8, cudaMemcpyDeviceToHost, s));
-                CUDA_TRY(cudaMemcpyAsync(vals_host, vals, m * 8, cudaMemcpyDeviceToHost, s));
+            if (m > p->stage_cap) {
+                cudaFree(p->stage_ids);
+                cudaFree(p->stage_vals);
+                p->stage_ids = nullptr;
+                p->stage_vals = nullptr;
+                p->scratch_bytes -= p->stage_cap * 16;
+                p->stage_cap = 0;
+                const int64_t want = std::min<int64_t>(p->n, std::max<int64_t>(m, m + m / 4));
+                if (!grow((void**)&p->stage_ids, want * 8) || !grow((void**)&p->stage_vals, want * 8))
+                    return fail(PMSZ_ERR_CUDA, "staging allocation failed");
+                p->stage_cap = want;
             }
-            cudaFreeAsync(ids, s);
-            cudaFreeAsync(vals, s);
+            st = pmsz_edits_export(p, g, p->stage_ids, p->stage_vals, m, nullptr, stream);
+            if (st == PMSZ_OK) {
+                CUDA_TRY(cudaMemcpyAsync(ids_host, p->stage_ids, m * 8, cudaMemcpyDeviceToHost, s));
+                CUDA_TRY(cudaMemcpyAsync(vals_host, p->stage_vals, m * 8, cudaMemcpyDeviceToHost, s));
+            }
         }
     }
-    cudaFreeAsync(f, s);
-    cudaFreeAsync(g, s);
     CUDA_TRY(cudaStreamSynchronize(s));
     return st;
 }

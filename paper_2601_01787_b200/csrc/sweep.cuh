@@ -199,23 +199,25 @@ __global__ void __launch_bounds__(256) k_defer(Dom d, const double* __restrict__
 }
 
 // K1 sparse sweep over the dirty-centre list (grid-stride; count read on device).
-__global__ void __launch_bounds__(256) k_sweep_sparse(Dom d, const double* __restrict__ g, Work w,
-                                                     int cur) {
-    const unsigned long long n = min(w.ctr->nact[cur], w.act_cap);
+// `sorted`: the list was compacted from actbits (ascending ids, bits already
+// cleared), so neighbouring threads gather neighbouring cache lines.
+__device__ __forceinline__ void sweep_sparse_range(const Dom& d, const double* __restrict__ g, const Work& w,
+                                                   int cur, bool sorted, unsigned long long i,
+                                                   unsigned long long stride) {
+    const unsigned long long n = min(__ldcg(&w.ctr->nact[cur]), w.act_cap);
     const uint32_t* list = w.act[cur];
-    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-         i += (unsigned long long)gridDim.x * blockDim.x) {
-        const int64_t c = list[i];
-        atomicAnd(w.actbits + (c >> 5), ~(1u << (c & 31)));
+    for (; i < n; i += stride) {
+        const int64_t c = __ldcg(list + i);
+        if (!sorted) atomicAnd(w.actbits + (c >> 5), ~(1u << (c & 31)));
         int64_t x, y, z;
         coords(d, c, x, y, z);
         double nv[14];
 #pragma unroll
         for (int r = 0; r < 14; ++r) {
             const bool ok = in_dom(d, x + rank_dx(r), y + rank_dy(r), z + rank_dz(r));
-            nv[r] = ok ? __ldg(g + c + rank_off(d, r)) : nan64();
+            nv[r] = ok ? __ldcg(g + c + rank_off(d, r)) : nan64();
         }
-        const Scan s = fold_scan(__ldg(g + c), nv);
+        const Scan s = fold_scan(__ldcg(g + c), nv);
         const uint8_t fc = w.code[c];
         const uint32_t bit = 1u << (c & 31);
         if (code_mismatch(d, scan_code(s), fc)) {
@@ -228,6 +230,12 @@ __global__ void __launch_bounds__(256) k_sweep_sparse(Dom d, const double* __res
             atomicAnd(w.detbits + (c >> 5), ~bit);
         }
     }
+}
+
+__global__ void __launch_bounds__(256) k_sweep_sparse(Dom d, const double* __restrict__ g, Work w, int cur,
+                                                     int sorted) {
+    sweep_sparse_range(d, g, w, cur, sorted != 0, (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x,
+                       (unsigned long long)gridDim.x * blockDim.x);
 }
 
 __device__ __forceinline__ bool in_core(const Dom& d, int64_t x, int64_t y, int64_t z) {
@@ -281,7 +289,7 @@ struct TargetOps {
 template <typename FT>
 __device__ __forceinline__ TargetOps load_target(const FT* __restrict__ f, const double* __restrict__ g,
                                                  const Work& w, int64_t t) {
-    return TargetOps{w.prop[t], g[t], (double)f[t], (unsigned int)w.counts[t]};
+    return TargetOps{__ldcg(w.prop + t), __ldcg(g + t), (double)f[t], (unsigned int)__ldcg(w.counts + t)};
 }
 
 template <typename FT>
@@ -315,7 +323,7 @@ __device__ __forceinline__ void apply_target(const Dom& d, const FT* __restrict_
 // edits): 15 ring entries per edit must fit the list budget.
 __device__ __forceinline__ int apply_marks(const Work& w) {
     if (!w.incremental) return kMarkNone;
-    const int mode = (w.ctr->nwork * 15ull <= w.mark_limit) ? kMarkList : kMarkBits;
+    const int mode = (__ldcg(&w.ctr->nwork) * 15ull <= w.mark_limit) ? kMarkList : kMarkBits;
     if (blockIdx.x == 0 && threadIdx.x == 0) w.ctr->scratch[3] = (unsigned long long)mode;
     return mode;
 }
@@ -334,21 +342,19 @@ __device__ __forceinline__ void flush_acc(const Work& w, const ApplyAcc& a) {
 // K2 over the target list (compacted from the touched bitmap after a tiled
 // sweep, or appended by first touch in a sparse sweep).
 template <typename FT>
-__global__ void __launch_bounds__(256) k_apply_list(Dom d, const FT* __restrict__ f, double* __restrict__ g,
-                                                    Work w, int nxt) {
-    const int mark = apply_marks(w);
-    const unsigned long long n = w.ctr->nwork;
-    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+__device__ __forceinline__ void apply_range(const Dom& d, const FT* __restrict__ f, double* __restrict__ g,
+                                            const Work& w, int nxt, int mark, unsigned long long i0,
+                                            unsigned long long stride) {
+    const unsigned long long n = __ldcg(&w.ctr->nwork);
     constexpr int kB = 4;   // targets in flight per thread
     ApplyAcc acc;
-    for (unsigned long long i0 = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i0 < n;
-         i0 += kB * stride) {
+    for (; i0 < n; i0 += kB * stride) {
         int64_t t[kB];
         bool ok[kB];
 #pragma unroll
         for (int k = 0; k < kB; ++k) {
             ok[k] = i0 + k * stride < n;
-            t[k] = ok[k] ? (int64_t)w.work[i0 + k * stride] : 0;
+            t[k] = ok[k] ? (int64_t)__ldcg(w.work + i0 + k * stride) : 0;
         }
         if (w.track) {
             // sparse lists may repeat a target: the thread that clears its
@@ -370,13 +376,21 @@ __global__ void __launch_bounds__(256) k_apply_list(Dom d, const FT* __restrict_
     flush_acc(w, acc);
 }
 
+template <typename FT>
+__global__ void __launch_bounds__(256) k_apply_list(Dom d, const FT* __restrict__ f, double* __restrict__ g,
+                                                    Work w, int nxt) {
+    const int mark = apply_marks(w);
+    apply_range(d, f, g, w, nxt, mark, (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x,
+                (unsigned long long)gridDim.x * blockDim.x);
+}
+
 // 1-ring marking of the edits of a list-mode iteration: thread i marks ring
 // member (i % 15) of edit (i / 15).
-__global__ void __launch_bounds__(256) k_mark_list(Dom d, Work w, int nxt) {
-    const unsigned long long n = w.ctr->nelist * 15ull;
-    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-         i += (unsigned long long)gridDim.x * blockDim.x) {
-        const int64_t v = w.elist[i / 15];
+__device__ __forceinline__ void mark_list_range(const Dom& d, const Work& w, int nxt, unsigned long long i,
+                                                unsigned long long stride) {
+    const unsigned long long n = __ldcg(&w.ctr->nelist) * 15ull;
+    for (; i < n; i += stride) {
+        const int64_t v = __ldcg(w.elist + i / 15);
         const int r = (int)(i % 15) - 1;
         int64_t x, y, z;
         coords(d, v, x, y, z);
@@ -390,6 +404,11 @@ __global__ void __launch_bounds__(256) k_mark_list(Dom d, Work w, int nxt) {
         const unsigned long long slot = agg_append(&w.ctr->nact[nxt]);
         if (slot < w.act_cap) w.act[nxt][slot] = (uint32_t)u;
     }
+}
+
+__global__ void __launch_bounds__(256) k_mark_list(Dom d, Work w, int nxt) {
+    mark_list_range(d, w, nxt, (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x,
+                    (unsigned long long)gridDim.x * blockDim.x);
 }
 
 }  // namespace pmsz

@@ -1,0 +1,136 @@
+// tail.cuh -- the list-mode iterations of the correction loop in ONE
+// persistent cooperative kernel.
+//
+// After the first one or two sweeps the dirty set collapses to a few thousand
+// centres and every iteration is latency bound: a sparse sweep, an apply and a
+// ring marking of a few microseconds each, plus a host round trip to read the
+// edit count and choose the next iteration's form.  k_tail runs those
+// iterations back to back on a grid that is co-resident on all 148 SMs, with
+// three grid barriers per iteration instead of three launches and a host
+// synchronisation:
+//
+//   S  sparse sweep of the dirty list act[cur]  -> proposals, target list
+//   |  grid barrier
+//   A  apply the merged proposals (K2)         -> edits, elist
+//   |  grid barrier
+//   M  1-ring marking of the edits             -> act[nxt]
+//   |  grid barrier; every CTA reads the same final counters and takes the
+//      same decision: stop (zero edits), hand back to the host (the edit set
+//      grew past the list budget, the next dirty list is large enough to be
+//      worth sorting first -- see sort_pending -- or the iteration budget is
+//      spent), or go on.
+//
+// The arithmetic is the list-mode iteration of iterate_once unchanged (same
+// device functions), so results are bit-identical whichever form runs an
+// iteration.  Mutable data are read with ld.global.cg (L2) only.
+//
+// Counter lifetimes (each is reset in a phase where nobody can still read
+// the previous value, so no extra barrier is needed):
+//   nwork   written S, read A, reset M      ndetect written S, read A, reset M
+//   nedits  written A, read M, reset S'     nelist  written A, read M, reset S'
+//   nact[nxt] reset A, written M, read after the M barrier and in S'
+#pragma once
+#include <cooperative_groups.h>
+#include "sweep.cuh"
+
+namespace pmsz {
+
+enum : unsigned long long { kTailConverged = 1, kTailBits = 2, kTailOverflow = 3, kTailBudget = 4, kTailSort = 5 };
+
+struct TailState {
+    unsigned long long iterations;   // iterations run by this launch
+    unsigned long long exit;         // kTail*
+    unsigned long long cur;          // dirty list the next iteration would sweep
+    unsigned long long pending;      // its length
+    unsigned long long last_edits;
+    unsigned long long last_detect;
+    unsigned long long shared_or;    // shared_dirty of any iteration
+    unsigned long long detections;   // sum over iterations
+};
+
+template <typename FT>
+__global__ void __launch_bounds__(256) k_tail(Dom d, const FT* __restrict__ f, double* g, Work w, int cur,
+                                              int sorted, unsigned long long sort_min, long long budget, unsigned long long* __restrict__ hist,
+                                              TailState* ts, unsigned long long* __restrict__ trace) {
+    cg::grid_group grid = cg::this_grid();
+    const unsigned long long tid = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    const bool leader = tid == 0;
+    DevCounters* c = w.ctr;
+    w.track = 1;
+    unsigned long long shared_or = 0, detections = 0;
+    for (long long it = 0;; ++it) {
+        const int nxt = cur ^ 1;
+        // ---- S ---------------------------------------------------------------
+        if (trace && leader && it == 0) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            trace[8190] = t;
+        }
+        if (leader && it > 0) {
+            c->nedits = 0;
+            c->nelist = 0;
+            c->shared_dirty = 0;
+        }
+        sweep_sparse_range(d, g, w, cur, sorted && it == 0, tid, stride);
+        grid.sync();
+        if (trace && leader && it < 4) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            trace[8000 + 2 * it] = t;
+        }
+        // ---- A ---------------------------------------------------------------
+        const unsigned long long ndet = __ldcg(&c->ndetect);
+        if (leader) c->nact[nxt] = 0;
+        const int mark = apply_marks(w);
+        apply_range(d, f, g, w, nxt, mark, tid, stride);
+        grid.sync();
+        if (trace && leader && it < 4) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            trace[8001 + 2 * it] = t;
+        }
+        // ---- M ---------------------------------------------------------------
+        const unsigned long long nedits = __ldcg(&c->nedits);
+        shared_or |= __ldcg(&c->shared_dirty);
+        detections += ndet;
+        if (leader) {
+            hist[it] = nedits;
+            c->nwork = 0;
+            c->ndetect = 0;
+        }
+        if (mark == kMarkList) mark_list_range(d, w, nxt, tid, stride);
+        grid.sync();
+        // ---- decide ------------------------------------------------------------
+        const unsigned long long nact = __ldcg(&c->nact[nxt]);
+        if (trace && leader) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            trace[2 * it] = t;
+            trace[2 * it + 1] = nact;
+        }
+        unsigned long long exit = 0;
+        if (nedits == 0) exit = kTailConverged;
+        else if (mark != kMarkList) exit = kTailBits;
+        else if (nact > w.act_cap) exit = kTailOverflow;
+        else if (it + 1 >= budget) exit = kTailBudget;
+        else if (nact > sort_min) exit = kTailSort;   // large: the host sorts the list first
+        if (exit) {
+            if (leader) {
+                ts->iterations = (unsigned long long)(it + 1);
+                ts->exit = exit;
+                ts->cur = (unsigned long long)nxt;
+                ts->pending = nact;
+                ts->last_edits = nedits;
+                ts->last_detect = ndet;
+                ts->shared_or = shared_or;
+                ts->detections = detections;
+                c->ndetect = ndet;   // the host reads the last iteration's counters
+            }
+            return;
+        }
+        cur = nxt;
+    }
+}
+
+}  // namespace pmsz

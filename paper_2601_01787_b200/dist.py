@@ -212,6 +212,48 @@ class DeviceEngine:
         return self.plan.residual()
 
 
+def _e2e_host(args, eng, blocks, grid, rank, lockstep, cap, dev, nvox_total) -> dict:
+    """End to end per rank: pinned host f32 original + f64 decompressed ext
+    slab -> device, the distributed correction, the block's edit record
+    (ids + values) -> pinned host.  Wall time per rank, max over ranks."""
+    f_host = torch.empty(eng.f.numel(), dtype=eng.f.dtype, pin_memory=True)
+    fh_host = torch.empty(eng.fh.numel(), dtype=torch.float64, pin_memory=True)
+    f_host.copy_(eng.f)
+    fh_host.copy_(eng.fh)
+    out = {}
+
+    def call():
+        eng.f.copy_(f_host, non_blocking=True)
+        eng.fh.copy_(fh_host, non_blocking=True)
+        eng.prepare()
+        run_distributed(eng, blocks, grid, rank, lockstep, cap)
+        ids, vals = eng.plan.export_edits(eng.g)
+        hi = torch.empty(ids.numel(), dtype=torch.int64, pin_memory=True)
+        hv = torch.empty(vals.numel(), dtype=torch.float64, pin_memory=True)
+        hi.copy_(ids, non_blocking=True)
+        hv.copy_(vals, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        out["edits"] = int(ids.numel())
+
+    for _ in range(2):
+        call()
+    dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        call()
+    torch.cuda.synchronize()
+    dt = torch.tensor([(time.perf_counter() - t0) / args.steps], dtype=torch.float64, device=dev)
+    dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+    sec = float(dt.item())
+    io = torch.tensor([f_host.numel() * f_host.element_size() + fh_host.numel() * 8, out["edits"] * 16],
+                      dtype=torch.int64, device=dev)
+    dist.all_reduce(io)
+    return {"value": nvox_total / sec, "unit": "voxels/s", "h2d_bytes_per_step": int(io[0].item()),
+            "d2h_bytes_per_step": int(io[1].item()), "ms_per_step": sec * 1e3, "bytes": "summed over ranks",
+            "path": "per rank: pinned host ext slab in, DeviceEngine + NCCL round loop, edit record out"}
+
+
 # ---------------------------------------------------------------------------
 # bench.py --gpus N (torchrun): weak scaling, 512^3 per GPU, z-slabs
 def bench_main(args, metric, unit, ClockSampler, measured_peaks, cpu_sample_inputs, time_cpu_oracle):
@@ -276,6 +318,7 @@ def bench_main(args, metric, unit, ClockSampler, measured_peaks, cpu_sample_inpu
     ms = float(t.item())
     residual = torch.tensor([eng.residual()], dtype=torch.int64, device=dev)
     dist.all_reduce(residual)
+    e2e = None if args.no_e2e else _e2e_host(args, eng, blocks, grid, rank, lockstep, cap, dev, S ** 3 * world)
     per_rank = [None] * world
     dist.all_gather_object(per_rank, {"rank": rank, "iterations": st.iterations, "edits": st.edit_total,
                                       "max_vertex_edits": st.max_vertex_edits, "ms": ms_local,
@@ -310,6 +353,8 @@ def bench_main(args, metric, unit, ClockSampler, measured_peaks, cpu_sample_inpu
                 "clocks": clk, "gpu_launches": launches,
                 "result": {"rounds": st.rounds, "syncs": st.syncs, "edits_per_round": list(st.edits_per_round),
                            "residual": int(residual.item()), "per_rank": per_rank}}
+        if e2e is not None:
+            line["e2e"] = e2e
         print(json.dumps(line), flush=True)
     dist.barrier()
     dist.destroy_process_group()

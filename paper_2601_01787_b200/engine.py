@@ -57,7 +57,7 @@ class DomainPlan:
 
     def __init__(self, spec: DomainSpec, xi: float, tau: float, max_iterations: int,
                  *, incremental: bool = True, extrema_only: bool = False,
-                 f32_original: bool = False):
+                 f32_original: bool = False, host_loop: bool = False):
         self.lib = N.lib()
         self.spec = spec
         self.xi, self.tau, self.max_iterations = float(xi), float(tau), int(max_iterations)
@@ -72,7 +72,8 @@ class DomainPlan:
         d.xi, d.tau, d.max_iterations = self.xi, self.tau, self.max_iterations
         d.flags = ((N.FLAG_INCREMENTAL if incremental else 0)
                    | (N.FLAG_EXTREMA_ONLY if extrema_only else 0)
-                   | (N.FLAG_F32_ORIGINAL if f32_original else 0))
+                   | (N.FLAG_F32_ORIGINAL if f32_original else 0)
+                   | (N.FLAG_HOST_LOOP if host_loop else 0))
         h = ctypes.c_void_p()
         st = self.lib.pmsz_plan_create(ctypes.byref(d), ctypes.byref(h))
         if st == N.PMSZ_ERR_INVALID:

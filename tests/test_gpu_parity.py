@@ -223,6 +223,31 @@ def test_device_path_matches_oracle_at_scale(n, rel, noise):
     assert np.abs(g - f_h).max() <= xi
 
 
+@pytest.mark.parametrize("n,rel", [(128, 1e-4), (96, 1e-3)])
+def test_device_tail_equals_host_loop(n, rel):
+    """The persistent cooperative tail (k_tail) and the host-driven loop run
+    the same iterations: identical trajectory, field, edits and counters."""
+    from paper_2601_01787_b200.engine import DomainPlan, DomainSpec
+    dims = (n, n, n)
+    f32 = gen.perlin_device(gen.NoiseSpec(dims, 3), f32=True)
+    xi = gen.relative_to_absolute_device(f32, rel)
+    fh = gen.quantize_device(f32, xi)
+    cfg = pm.CorrectionConfig(xi_abs=xi)
+    outs = []
+    for host_loop in (False, True):
+        plan = DomainPlan(DomainSpec.whole(dims), xi, cfg.tau, cfg.max_outer_iterations,
+                          f32_original=True, host_loop=host_loop)
+        plan.profile(True)
+        outs.append((pm.run_correction_device(f32, fh, dims, cfg, plan=plan), plan.profile_read()))
+    (a, pa), (b, pb) = outs
+    assert pa["tail"][1] >= 1 and pb["tail"][1] == 0
+    assert a.edits_per_iteration == b.edits_per_iteration
+    assert torch.equal(a.corrected, b.corrected)
+    assert torch.equal(a.edit_ids, b.edit_ids) and torch.equal(a.edit_values, b.edit_values)
+    assert a.max_vertex_edits == b.max_vertex_edits
+    assert (a.full_sweeps, a.masked_sweeps, a.sparse_sweeps) == (b.full_sweeps, b.masked_sweeps, b.sparse_sweeps)
+
+
 def test_plan_is_reusable_and_restores_invariants():
     dims = (64, 64, 64)
     f32 = gen.perlin_device(gen.NoiseSpec(dims, 2), f32=True)
