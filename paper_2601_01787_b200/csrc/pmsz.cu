@@ -27,6 +27,7 @@
 #include "gen.cuh"
 #include "tiles.cuh"
 #include "tail.cuh"
+#include "gather.cuh"
 
 using namespace pmsz;
 
@@ -369,7 +370,7 @@ __global__ void __launch_bounds__(256) k_dilate(const uint32_t* __restrict__ e, 
     }
 }
 
-enum { kFull = 0, kMasked = 1, kList = 2 };
+enum { kFull = 0, kMasked = 1, kList = 2, kMaskedList = 3 };
 
 template <typename FT>
 __global__ void __launch_bounds__(256) k_box_extract(Box b, int64_t gny, const FT* __restrict__ src, FT* __restrict__ dst) {
@@ -398,7 +399,7 @@ struct pmsz_plan {
     int64_t nblocks_compact = 0;
     int64_t scratch_bytes = 0;
     int cur = 0;              // pending dirty list
-    int next_mode = 0;        // kFull / kMasked / kList for the next iteration
+    int next_mode = 0;        // kFull / kMasked / kList / kMaskedList for the next iteration
     int last_mode = 0;
     int64_t pending = 0;      // length of the pending dirty list (kList)
     int64_t ncore = 0;        // centres in the core box
@@ -422,6 +423,9 @@ struct pmsz_plan {
     unsigned long long* hthist = nullptr; // pinned mirror
     int tail_blocks[2] = {0, 0};          // cooperative grid per FT (f64, f32)
     int64_t sort_min = 65536;             // dirty lists above this are sorted (compacted from actbits)
+    int64_t dense_min = 0;                // dirty lists above this take the pipelined gather (kMaskedList)
+    bool bits_only = false;               // the pending dirty set is in actbits only (no list)
+    bool gather_on = true;                // masked iterations as sorted gathers (gather.cuh)
     // host-buffer entry point staging (pmsz_run_correction_host)
     void* stage_f = nullptr;
     double* stage_g = nullptr;
@@ -511,7 +515,8 @@ void launch_bits_total(pmsz_plan* p, const uint32_t* bits, unsigned long long* d
 // (the same set; the bits are cleared on the way): neighbouring threads then
 // gather neighbouring cache lines instead of one ring after another.
 int sort_pending(pmsz_plan* p, cudaStream_t s) {
-    if (p->pending <= p->sort_min) return 0;
+    if (p->pending <= p->sort_min && !p->bits_only) return 0;
+    p->bits_only = false;
     ProfScope ps(p, s, PMSZ_K_COMPACT);
     launch_bits_total(p, p->w.actbits, &p->ctr->nact[p->cur], s);
     k_bits_list<<<(unsigned)p->nblocks_compact, kCompactThreads, 0, s>>>(p->w.actbits, p->nwords, p->block_counts,
@@ -536,18 +541,52 @@ pmsz_status launch_apply(pmsz_plan* p, const void* f, double* g, cudaStream_t s,
     LAUNCHED();
     if (p->w.incremental) {   // list-mode ring marking (no-op when the edits went to the bitmap)
         k_mark_list<<<grid_for(std::min<int64_t>(15 * bound, (int64_t)p->w.mark_limit), 256, 4), 256, 0, s>>>(
-            p->dom, p->w, nxt);
+            p->dom, p->w, nxt, (unsigned long long)p->sort_min);
         LAUNCHED();
     }
     return PMSZ_OK;
 }
 
-// One Jacobi iteration: K1 in one of three forms, then K2.  Leaves the
+// Form of the next iteration from the marking of the last one:
+//   edits marked in the edit bitmap (many edits) -> masked sweep over its
+//     dilation (or, with the old tiled scan, a full sweep when dense);
+//   dirty list overflowed                        -> full sweep;
+//   dirty list longer than dense_min             -> masked sweep over actbits;
+//   otherwise                                    -> list (gather) sweep.
+pmsz_status choose_next(pmsz_plan* p, cudaStream_t s, bool marked_bits, int64_t nedits, int nxt, int64_t nact,
+                        bool appended, int64_t bound) {
+    if (marked_bits) {
+        if (15 * nedits > p->ncore / 8) {
+            p->next_mode = kFull;
+            CUDA_TRY(cudaMemsetAsync(p->w.iteredit, 0, p->nwords * 4, s));
+        } else {
+            p->next_mode = kMasked;
+        }
+    } else if (!appended) {   // dirty set in actbits only; `bound` >= its size
+        p->cur = nxt;
+        p->pending = bound;
+        p->bits_only = true;
+        p->next_mode = (p->gather_on && bound > p->dense_min) ? kMaskedList : kList;
+    } else if (nact > (int64_t)p->w.act_cap) {
+        p->next_mode = kFull;
+    } else {
+        p->cur = nxt;
+        p->pending = nact;
+        p->bits_only = false;
+        p->next_mode = (p->gather_on && nact > p->dense_min) ? kMaskedList : kList;
+    }
+    return PMSZ_OK;
+}
+
+// One Jacobi iteration: K1 in one of four forms, then K2.  Leaves the
 // counters on the host and decides the form of the next iteration:
-//   kFull   -- tiled sweep over the whole core box (first iteration)
-//   kMasked -- tiled sweep restricted to the dilated edit bitmap of the
-//              previous iteration (large dirty sets; exact by SURVEY H7)
-//   kList   -- gather sweep over the explicit dirty-centre list (small sets)
+//   kFull       -- tiled sweep of every core centre (first iteration)
+//   kMasked     -- the centres of the dilated edit bitmap of the previous
+//                  iteration (exact by SURVEY H7), compacted to an ascending
+//                  list and swept by the pipelined gather (gather.cuh)
+//   kMaskedList -- the same over the marked dirty set (actbits) when the
+//                  explicit list is long
+//   kList       -- gather sweep over the explicit dirty-centre list (short)
 pmsz_status iterate_once(pmsz_plan* p, const void* f, double* g, cudaStream_t s) {
     const int nxt = p->cur ^ 1;
     pmsz_status st = reset_iter(p, s, nxt);
@@ -557,6 +596,8 @@ pmsz_status iterate_once(pmsz_plan* p, const void* f, double* g, cudaStream_t s)
     const int64_t cx = d.hi[0] - d.lo[0], cy = d.hi[1] - d.lo[1], cz = d.hi[2] - d.lo[2];
     const bool nonempty = cx > 0 && cy > 0 && cz > 0;
     int64_t apply_bound = p->n;   // upper bound of the targets, sizes the apply grid
+    const bool gather = p->gather_on && mode != kFull;
+    if (mode != kList) p->bits_only = false;   // actbits is consumed (compacted or cleared) below
     if (mode == kFull) {
         if (p->w.incremental) CUDA_TRY(cudaMemsetAsync(p->w.actbits, 0, p->nwords * 4, s));
         CUDA_TRY(cudaMemsetAsync(p->w.detbits, 0, p->nwords * 4, s));
@@ -566,23 +607,40 @@ pmsz_status iterate_once(pmsz_plan* p, const void* f, double* g, cudaStream_t s)
             launch_sweep_full<false>(d, g, p->w, s);
             LAUNCHED();
         }
-    } else if (mode == kMasked) {
+    } else if (mode == kMasked || mode == kMaskedList) {
         p->w.track = 0;
-        {
+        if (mode == kMasked) {   // dirty set = dilation of the previous iteration's edits
             ProfScope ps(p, s, PMSZ_K_OTHER);
             k_dilate<<<grid_for(p->nwords, 256, 8), 256, 0, s>>>(p->w.iteredit, p->w.actbits, p->w.detbits,
                                                                p->nwords, p->ring_delta);
             LAUNCHED();
+            CUDA_TRY(cudaMemsetAsync(p->w.iteredit, 0, p->nwords * 4, s));
+        }                        // kMaskedList: the dirty set is actbits as marked (list dropped)
+        if (gather) {
+            // actbits -> ascending centre list (in `work`, bits cleared) -> pipelined gather sweep
+            {
+                ProfScope ps(p, s, PMSZ_K_COMPACT);
+                launch_bits_total(p, p->w.actbits, &p->ctr->ndefer, s);
+                k_bits_list<<<(unsigned)p->nblocks_compact, kCompactThreads, 0, s>>>(p->w.actbits, p->nwords,
+                                                                                   p->block_counts, p->w.work, 1);
+                LAUNCHED();
+            }
+            if (nonempty) {
+                ProfScope ps(p, s, PMSZ_K_SWEEP_MASKED);
+                k_gather<false><<<num_sms() * 2, kGWarps * 32, kGatherSmem, s>>>(d, g, p->w, p->w.work,
+                                                                                 &p->ctr->ndefer);
+                LAUNCHED();
+            }
+        } else {
+            if (nonempty) {
+                ProfScope ps(p, s, PMSZ_K_SWEEP_MASKED);
+                launch_sweep_full<false>(d, g, p->w, s, p->w.actbits);
+                LAUNCHED();
+            }
+            CUDA_TRY(cudaMemsetAsync(p->w.actbits, 0, p->nwords * 4, s));
         }
-        CUDA_TRY(cudaMemsetAsync(p->w.iteredit, 0, p->nwords * 4, s));
-        if (nonempty) {
-            ProfScope ps(p, s, PMSZ_K_SWEEP_MASKED);
-            launch_sweep_full<false>(d, g, p->w, s, p->w.actbits);
-            LAUNCHED();
-        }
-        CUDA_TRY(cudaMemsetAsync(p->w.actbits, 0, p->nwords * 4, s));
     }
-    if (mode != kList && nonempty) {
+    if (mode != kList && nonempty && !gather) {
         // centres with a detection (bitmap set by the tiled sweep) -> list -> rules
         {
             ProfScope ps(p, s, PMSZ_K_COMPACT);
@@ -612,21 +670,10 @@ pmsz_status iterate_once(pmsz_plan* p, const void* f, double* g, cudaStream_t s)
     st = sync_counters(p, s);
     if (st) return st;
     if (p->w.incremental) {
-        if (p->hctr->scratch[3] == kMarkBits) {
-            // dirty fraction ~ 15 x edits / core voxels
-            if (15 * (int64_t)p->hctr->nedits > p->ncore / 8) {
-                p->next_mode = kFull;
-                CUDA_TRY(cudaMemsetAsync(p->w.iteredit, 0, p->nwords * 4, s));
-            } else {
-                p->next_mode = kMasked;
-            }
-        } else if (p->hctr->nact[nxt] > p->w.act_cap) {
-            p->next_mode = kFull;
-        } else {
-            p->next_mode = kList;
-            p->cur = nxt;
-            p->pending = (int64_t)p->hctr->nact[nxt];
-        }
+        const int64_t bound = 15 * (int64_t)p->hctr->nelist;
+        st = choose_next(p, s, p->hctr->scratch[3] == kMarkBits, (int64_t)p->hctr->nedits, nxt,
+                         (int64_t)p->hctr->nact[nxt], bound <= p->sort_min, bound);
+        if (st) return st;
     }
     return PMSZ_OK;
 }
@@ -709,22 +756,12 @@ pmsz_status tail_step(pmsz_plan* p, const void* f, double* g, cudaStream_t s, lo
     p->iterations += *k;
     for (int64_t i = 0; i < *k; ++i) p->edit_total += (int64_t)p->hthist[i];
     p->last_mode = kList;
-    switch (ts.exit) {
-    case kTailBits:   // the last iteration's edits went to the edit bitmap
-        if (15 * (int64_t)ts.last_edits > p->ncore / 8) {
-            p->next_mode = kFull;
-            CUDA_TRY(cudaMemsetAsync(p->w.iteredit, 0, p->nwords * 4, s));
-        } else {
-            p->next_mode = kMasked;
-        }
-        break;
-    case kTailOverflow:
+    if (ts.exit == kTailOverflow) {
         p->next_mode = kFull;
-        break;
-    default:          // converged or budget spent: the next list is pending
-        p->next_mode = kList;
-        p->cur = (int)ts.cur;
-        p->pending = (int64_t)ts.pending;
+    } else {
+        st = choose_next(p, s, ts.exit == kTailBits, (int64_t)ts.last_edits, (int)ts.cur, (int64_t)ts.pending,
+                         ts.appended != 0, (int64_t)ts.pending);
+        if (st) return st;
     }
     return PMSZ_OK;
 }
@@ -752,6 +789,7 @@ pmsz_status reset_run_state(pmsz_plan* p, cudaStream_t s) {
     p->cur = 0;
     p->next_mode = kFull;
     p->pending = 0;
+    p->bits_only = false;
     p->iterations = 0;
     p->edit_total = 0;
     return PMSZ_OK;
@@ -916,7 +954,18 @@ pmsz_status pmsz_plan_create(const pmsz_desc* desc, pmsz_plan** out) {
                  cudaMallocHost((void**)&p->htail, sizeof(TailState)) == cudaSuccess &&
                  cudaMallocHost((void**)&p->hthist, hist_n * 8) == cudaSuccess;
     p->tail_on = (d.flags & PMSZ_FLAG_HOST_LOOP) == 0;
+    p->dense_min = std::max<int64_t>(ncore / 96, 65536);
     if (const char* e = getenv("PMSZ_SORT_MIN")) p->sort_min = atoll(e);
+    if (const char* e = getenv("PMSZ_DENSE_MIN")) p->dense_min = atoll(e);
+    if (const char* e = getenv("PMSZ_SWEEP")) p->gather_on = strcmp(e, "tiled") != 0;
+    if (cudaFuncSetAttribute(k_gather<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGatherSmem) !=
+            cudaSuccess ||
+        cudaFuncSetAttribute(k_gather<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGatherSmem) !=
+            cudaSuccess) {
+        cudaGetLastError();
+        pmsz_plan_destroy(p);
+        return fail(PMSZ_ERR_CUDA, "k_gather shared memory configuration failed");
+    }
     if (!ok) {
         cudaGetLastError();
         pmsz_plan_destroy(p);
@@ -1005,7 +1054,7 @@ pmsz_status pmsz_iterate(pmsz_plan* p, const void* f, double* g, uint8_t* edited
         r->iterations = p->iterations;
         r->edit_count = p->edit_total;
         if (p->last_mode == kFull) ++r->full_sweeps;
-        else if (p->last_mode == kMasked) ++r->masked_sweeps;
+        else if (p->last_mode == kMasked || p->last_mode == kMaskedList) ++r->masked_sweeps;
         else ++r->sparse_sweeps;
     }
     return PMSZ_OK;
@@ -1060,9 +1109,16 @@ static pmsz_status after_mark(pmsz_plan* p, cudaStream_t s) {
     CUDA_TRY(cudaGetLastError());
     pmsz_status st = sync_counters(p, s);
     if (st) return st;
-    if (p->next_mode == kList) {
-        if (p->hctr->nact[p->cur] > p->w.act_cap) p->next_mode = kFull;
-        else p->pending = (int64_t)p->hctr->nact[p->cur];
+    if (p->next_mode == kList || p->next_mode == kMaskedList) {
+        const int64_t nact = (int64_t)p->hctr->nact[p->cur];
+        if (p->bits_only) {
+            p->pending += nact;   // still a bound; the list is rebuilt from actbits
+        } else if (nact > (int64_t)p->w.act_cap) {
+            p->next_mode = kFull;
+        } else {
+            p->pending = nact;
+            if (p->gather_on && nact > p->dense_min) p->next_mode = kMaskedList;
+        }
     }
     return PMSZ_OK;
 }
@@ -1100,7 +1156,8 @@ pmsz_status pmsz_box_merge_min(pmsz_plan* p, double* g, const int64_t lo[3], con
     const int64_t n = b.ext[0] * b.ext[1] * b.ext[2];
     CUDA_TRY(cudaMemsetAsync(&p->ctr->changed, 0, sizeof(unsigned long long), s));
     if (n > 0) {
-        const int mode = !p->w.incremental ? 0 : (p->next_mode == kMasked ? 1 : (p->next_mode == kList ? 2 : 0));
+        const int mode = !p->w.incremental ? 0
+                         : (p->next_mode == kMasked ? 1 : ((p->next_mode == kList || p->next_mode == kMaskedList) ? 2 : 0));
         ProfScope ps(p, s, PMSZ_K_OTHER);
         k_box_merge<<<grid_for(n, 256), 256, 0, s>>>(p->dom, p->w, b, g, buf, p->cur, mode, &p->ctr->changed);
         LAUNCHED();

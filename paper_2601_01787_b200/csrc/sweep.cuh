@@ -385,9 +385,16 @@ __global__ void __launch_bounds__(256) k_apply_list(Dom d, const FT* __restrict_
 }
 
 // 1-ring marking of the edits of a list-mode iteration: thread i marks ring
-// member (i % 15) of edit (i / 15).
-__device__ __forceinline__ void mark_list_range(const Dom& d, const Work& w, int nxt, unsigned long long i,
-                                                unsigned long long stride) {
+// member (i % 15) of edit (i / 15).  The dirty set always goes to actbits; it
+// is appended to the list act[nxt] only when short (`append`) -- a long list
+// is compacted from actbits in ascending order before its sweep anyway, and
+// appending millions of entries through one counter serialises on it.
+__device__ __forceinline__ bool mark_appends(const Work& w, unsigned long long list_limit) {
+    return __ldcg(&w.ctr->nelist) * 15ull <= list_limit;
+}
+
+__device__ __forceinline__ void mark_list_range(const Dom& d, const Work& w, int nxt, bool append,
+                                                unsigned long long i, unsigned long long stride) {
     const unsigned long long n = __ldcg(&w.ctr->nelist) * 15ull;
     for (; i < n; i += stride) {
         const int64_t v = __ldcg(w.elist + i / 15);
@@ -400,14 +407,18 @@ __device__ __forceinline__ void mark_list_range(const Dom& d, const Work& w, int
         if (!in_core(d, px, py, pz)) continue;
         const int64_t u = px + py * d.sy + pz * d.sz;
         const uint32_t bit = 1u << (u & 31);
+        if (!append) {
+            atomicOr(w.actbits + (u >> 5), bit);
+            continue;
+        }
         if (atomicOr(w.actbits + (u >> 5), bit) & bit) continue;
         const unsigned long long slot = agg_append(&w.ctr->nact[nxt]);
         if (slot < w.act_cap) w.act[nxt][slot] = (uint32_t)u;
     }
 }
 
-__global__ void __launch_bounds__(256) k_mark_list(Dom d, Work w, int nxt) {
-    mark_list_range(d, w, nxt, (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x,
+__global__ void __launch_bounds__(256) k_mark_list(Dom d, Work w, int nxt, unsigned long long list_limit) {
+    mark_list_range(d, w, nxt, mark_appends(w, list_limit), (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x,
                     (unsigned long long)gridDim.x * blockDim.x);
 }
 

@@ -46,6 +46,7 @@ struct TailState {
     unsigned long long last_detect;
     unsigned long long shared_or;    // shared_dirty of any iteration
     unsigned long long detections;   // sum over iterations
+    unsigned long long appended;     // the pending dirty set is listed (else: actbits only, `pending` a bound)
 };
 
 template <typename FT>
@@ -99,7 +100,9 @@ __global__ void __launch_bounds__(256) k_tail(Dom d, const FT* __restrict__ f, d
             c->nwork = 0;
             c->ndetect = 0;
         }
-        if (mark == kMarkList) mark_list_range(d, w, nxt, tid, stride);
+        const unsigned long long nel = __ldcg(&c->nelist);
+        const bool append = nel * 15ull <= sort_min;
+        if (mark == kMarkList) mark_list_range(d, w, nxt, append, tid, stride);
         grid.sync();
         // ---- decide ------------------------------------------------------------
         const unsigned long long nact = __ldcg(&c->nact[nxt]);
@@ -114,17 +117,18 @@ __global__ void __launch_bounds__(256) k_tail(Dom d, const FT* __restrict__ f, d
         else if (mark != kMarkList) exit = kTailBits;
         else if (nact > w.act_cap) exit = kTailOverflow;
         else if (it + 1 >= budget) exit = kTailBudget;
-        else if (nact > sort_min) exit = kTailSort;   // large: the host sorts the list first
+        else if (!append || nact > sort_min) exit = kTailSort;   // large: the host sorts the list first
         if (exit) {
             if (leader) {
                 ts->iterations = (unsigned long long)(it + 1);
                 ts->exit = exit;
                 ts->cur = (unsigned long long)nxt;
-                ts->pending = nact;
+                ts->pending = append ? nact : nel * 15ull;   // a bound when only actbits was marked
                 ts->last_edits = nedits;
                 ts->last_detect = ndet;
                 ts->shared_or = shared_or;
                 ts->detections = detections;
+                ts->appended = append ? 1ull : 0ull;
                 c->ndetect = ndet;   // the host reads the last iteration's counters
             }
             return;
