@@ -196,6 +196,24 @@ pmsz_status pmsz_scan_neighbors(int64_t nx, int64_t ny, int64_t nz, const double
 pmsz_status pmsz_scan_codes(int64_t nx, int64_t ny, int64_t nz, const double* values_dev,
                             uint8_t* code_dev, void* stream);
 
+/* ---- segmentation and distortion report (topology.py:156-174, 254-274) ---- */
+/* compute_segmentation(field): asc_target = minimum reached by the descending
+ * steepest path, desc_target = maximum reached by the ascending path (int64
+ * vertex ids, device arrays of nx*ny*nz).  v is f64, or f32 with is_f32. */
+pmsz_status pmsz_segmentation(int64_t nx, int64_t ny, int64_t nz, const void* values_dev, int32_t is_f32,
+                              int64_t* asc_target_dev, int64_t* desc_target_dev, void* stream);
+/* compare_plmss(reference, test): counts[7] (host) = sizes of fp_max, fn_max,
+ * fp_min, fn_min, asc_order_violations, desc_order_violations, then
+ * wrong_label_count.  kind_bits (device, may be NULL) receives the six vertex
+ * sets as bitmaps of ceil(n/32) words each, in that order. */
+pmsz_status pmsz_compare_plmss(int64_t nx, int64_t ny, int64_t nz, const void* reference_dev, int32_t ref_f32,
+                               const void* test_dev, int32_t test_f32, uint32_t* kind_bits_dev,
+                               int64_t* counts, void* stream);
+/* Ascending ids of the set bits of a device bitmap (np.flatnonzero); *count
+ * always receives the number of set bits; ids is written when it fits cap. */
+pmsz_status pmsz_bits_to_ids(const uint32_t* bits_dev, int64_t nbits, int64_t* ids_dev, int64_t cap,
+                             int64_t* count, void* stream);
+
 /* ---- ghost exchange helpers (_merge_min, parallel.py:122-140) ------------ */
 /* Pack a sub-box [lo, hi) of a domain array into a contiguous buffer. */
 pmsz_status pmsz_box_pack(int64_t nx, int64_t ny, int64_t nz, const double* src_dev,

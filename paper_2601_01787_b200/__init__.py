@@ -8,14 +8,15 @@ hand-written sm_100a kernels behind the C ABI of include/pmsz.h.
 from .grid import (RANK_OFFSETS, STENCIL, ScalarField, linear_index, neighbors, precedes,
                    vertex_coords)
 from .engine import BoundViolationError, ConvergenceError
-from .topology import (DistortionReport, ExtremaSet, NeighborScan, field_scan, find_extrema,
-                       scan_neighbors)
+from .topology import (DistortionReport, ExtremaSet, NeighborScan, SegmentationLabels, compare_plmss,
+                       compute_segmentation, field_scan, find_extrema, scan_neighbors)
 from .correction import (BoundsField, CorrectionConfig, CorrectionResult, DeviceCorrection, EditSet,
                          apply_edit, compute_bounds, iterate_array, run_correction,
                          run_correction_device, validate_error_bound)
 from .parallel import (Block, BlockDecomposition, ParallelStats, SyncStrategy, block_domain, decompose,
                        run_parallel)
-from .codec import FormatError, decode_edits, decode_edits_meta, encode_edits
+from .codec import (FormatError, decode_edits, decode_edits_meta, encode_edits, read_field, read_labels,
+                    write_field, write_labels)
 from .inputs import NoiseSpec
 
 __version__ = "0.1.0"

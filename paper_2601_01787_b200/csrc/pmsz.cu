@@ -28,6 +28,7 @@
 #include "tiles.cuh"
 #include "tail.cuh"
 #include "gather.cuh"
+#include "segment.cuh"
 
 using namespace pmsz;
 
@@ -214,8 +215,9 @@ __global__ void __launch_bounds__(kCompactThreads) k_bits_write(const uint32_t* 
 // Bitmap -> ascending u32 id list (the touched targets after a full sweep);
 // the words are cleared on the way (the touched bitmap is all-zero between
 // iterations).
+template <typename IdT>
 __global__ void __launch_bounds__(kCompactThreads) k_bits_list(uint32_t* __restrict__ bits, int64_t nwords,
-                                                               const unsigned long long* block_offs, uint32_t* list,
+                                                               const unsigned long long* block_offs, IdT* list,
                                                                int clear) {
     __shared__ unsigned warp_sums[kCompactThreads / 32];
     const int64_t w0 = (int64_t)blockIdx.x * kWordsPerBlock + (int64_t)threadIdx.x * kWordsPerThread;
@@ -249,7 +251,7 @@ __global__ void __launch_bounds__(kCompactThreads) k_bits_list(uint32_t* __restr
         while (m) {
             const int b = __ffs(m) - 1;
             m &= m - 1;
-            list[pos++] = (uint32_t)((w0 + k) * 32 + b);
+            list[pos++] = (IdT)((w0 + k) * 32 + b);
         }
     }
 }
@@ -519,7 +521,7 @@ int sort_pending(pmsz_plan* p, cudaStream_t s) {
     p->bits_only = false;
     ProfScope ps(p, s, PMSZ_K_COMPACT);
     launch_bits_total(p, p->w.actbits, &p->ctr->nact[p->cur], s);
-    k_bits_list<<<(unsigned)p->nblocks_compact, kCompactThreads, 0, s>>>(p->w.actbits, p->nwords, p->block_counts,
+    k_bits_list<uint32_t><<<(unsigned)p->nblocks_compact, kCompactThreads, 0, s>>>(p->w.actbits, p->nwords, p->block_counts,
                                                                        p->w.act[p->cur], 1);
     LAUNCHED();
     return 1;
@@ -532,7 +534,7 @@ pmsz_status launch_apply(pmsz_plan* p, const void* f, double* g, cudaStream_t s,
         // touched bitmap -> ascending target list (load-balanced apply)
         ProfScope ps(p, s, PMSZ_K_COMPACT);
         launch_bits_total(p, p->w.touched, &p->ctr->nwork, s);
-        k_bits_list<<<(unsigned)p->nblocks_compact, kCompactThreads, 0, s>>>(p->w.touched, p->nwords,
+        k_bits_list<uint32_t><<<(unsigned)p->nblocks_compact, kCompactThreads, 0, s>>>(p->w.touched, p->nwords,
                                                                            p->block_counts, p->w.work, 1);
         LAUNCHED();
     }
@@ -621,7 +623,7 @@ pmsz_status iterate_once(pmsz_plan* p, const void* f, double* g, cudaStream_t s)
             {
                 ProfScope ps(p, s, PMSZ_K_COMPACT);
                 launch_bits_total(p, p->w.actbits, &p->ctr->ndefer, s);
-                k_bits_list<<<(unsigned)p->nblocks_compact, kCompactThreads, 0, s>>>(p->w.actbits, p->nwords,
+                k_bits_list<uint32_t><<<(unsigned)p->nblocks_compact, kCompactThreads, 0, s>>>(p->w.actbits, p->nwords,
                                                                                    p->block_counts, p->w.work, 1);
                 LAUNCHED();
             }
@@ -645,7 +647,7 @@ pmsz_status iterate_once(pmsz_plan* p, const void* f, double* g, cudaStream_t s)
         {
             ProfScope ps(p, s, PMSZ_K_COMPACT);
             launch_bits_total(p, p->w.detbits, &p->ctr->ndefer, s);
-            k_bits_list<<<(unsigned)p->nblocks_compact, kCompactThreads, 0, s>>>(p->w.detbits, p->nwords,
+            k_bits_list<uint32_t><<<(unsigned)p->nblocks_compact, kCompactThreads, 0, s>>>(p->w.detbits, p->nwords,
                                                                                p->block_counts, p->w.work, 0);
             LAUNCHED();
         }
@@ -1505,6 +1507,131 @@ pmsz_status pmsz_bounded_noise(const void* f, int32_t is_f32, int64_t nx, int64_
                                                                     gdims[1], lo[0], lo[1], lo[2], xi, seed, out);
     LAUNCHED();
     CUDA_TRY(cudaGetLastError());
+    return PMSZ_OK;
+}
+
+// ---- segmentation / compare_plmss ----------------------
+static pmsz_status full_codes(int64_t nx, int64_t ny, int64_t nz, const void* v, int32_t is_f32, uint16_t* fc,
+                              cudaStream_t s) {
+    Dom d = whole_dom(nx, ny, nz);
+    dim3 block(32, 8, 1), grid((unsigned)((nx + 31) / 32), (unsigned)((ny + 7) / 8), (unsigned)nz);
+    if (is_f32) k_full_code<float><<<grid, block, 0, s>>>(d, (const float*)v, fc);
+    else k_full_code<double><<<grid, block, 0, s>>>(d, (const double*)v, fc);
+    LAUNCHED();
+    CUDA_TRY(cudaGetLastError());
+    return PMSZ_OK;
+}
+
+// Pointer jumping to the fixpoint; `flag` is one device counter.
+static pmsz_status jump_to_roots(uint32_t* ptr, int64_t n, unsigned long long* flag, cudaStream_t s) {
+    for (int pass = 0; pass < 64; ++pass) {
+        unsigned long long h = 0;
+        CUDA_TRY(cudaMemsetAsync(flag, 0, sizeof(h), s));
+        k_jump<<<grid_for(n, 256, 16), 256, 0, s>>>(ptr, n, flag);
+        LAUNCHED();
+        CUDA_TRY(cudaMemcpyAsync(&h, flag, sizeof(h), cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        if (h == 0) return PMSZ_OK;
+    }
+    return fail(PMSZ_ERR_CUDA, "pointer jumping did not reach a fixpoint");
+}
+
+// up/down root pointers of one field into asc (down) / desc (up), u32 device arrays.
+static pmsz_status segment_u32(int64_t nx, int64_t ny, int64_t nz, const void* v, int32_t is_f32, uint16_t* fc,
+                               uint32_t* asc, uint32_t* desc, unsigned long long* flag, cudaStream_t s) {
+    pmsz_status st = full_codes(nx, ny, nz, v, is_f32, fc, s);
+    if (st) return st;
+    Dom d = whole_dom(nx, ny, nz);
+    k_seg_ptr<<<grid_for(d.n, 256, 16), 256, 0, s>>>(d, fc, desc, asc);
+    LAUNCHED();
+    st = jump_to_roots(desc, d.n, flag, s);
+    if (st) return st;
+    return jump_to_roots(asc, d.n, flag, s);
+}
+
+pmsz_status pmsz_segmentation(int64_t nx, int64_t ny, int64_t nz, const void* v, int32_t is_f32,
+                              int64_t* asc_target, int64_t* desc_target, void* stream) {
+    if (nx < 1 || ny < 1 || nz < 1 || !v || !asc_target || !desc_target) return fail(PMSZ_ERR_INVALID, "bad arguments");
+    const int64_t n = nx * ny * nz;
+    if (n >= (int64_t)0xffffffffll) return fail(PMSZ_ERR_INVALID, "domain too large for 32-bit ids");
+    cudaStream_t s = S(stream);
+    uint16_t* fc = nullptr;
+    uint32_t *a = nullptr, *dd = nullptr;
+    unsigned long long* flag = nullptr;
+    CUDA_TRY(cudaMallocAsync((void**)&fc, n * 2, s));
+    CUDA_TRY(cudaMallocAsync((void**)&a, n * 4, s));
+    CUDA_TRY(cudaMallocAsync((void**)&dd, n * 4, s));
+    CUDA_TRY(cudaMallocAsync((void**)&flag, 8, s));
+    pmsz_status st = segment_u32(nx, ny, nz, v, is_f32, fc, a, dd, flag, s);
+    if (st == PMSZ_OK) {
+        k_widen<<<grid_for(n, 256, 16), 256, 0, s>>>(a, asc_target, n);
+        LAUNCHED();
+        k_widen<<<grid_for(n, 256, 16), 256, 0, s>>>(dd, desc_target, n);
+        LAUNCHED();
+    }
+    cudaFreeAsync(fc, s); cudaFreeAsync(a, s); cudaFreeAsync(dd, s); cudaFreeAsync(flag, s);
+    CUDA_TRY(cudaGetLastError());
+    return st;
+}
+
+pmsz_status pmsz_compare_plmss(int64_t nx, int64_t ny, int64_t nz, const void* ref, int32_t ref_f32, const void* test,
+                               int32_t test_f32, uint32_t* kind_bits, int64_t* counts, void* stream) {
+    if (nx < 1 || ny < 1 || nz < 1 || !ref || !test || !counts) return fail(PMSZ_ERR_INVALID, "bad arguments");
+    const int64_t n = nx * ny * nz;
+    if (n >= (int64_t)0xffffffffll) return fail(PMSZ_ERR_INVALID, "domain too large for 32-bit ids");
+    cudaStream_t s = S(stream);
+    uint16_t *rc = nullptr, *tc = nullptr;
+    uint32_t *ra = nullptr, *rd = nullptr, *ta = nullptr, *td = nullptr;
+    unsigned long long* cnt = nullptr;
+    CUDA_TRY(cudaMallocAsync((void**)&rc, n * 2, s));
+    CUDA_TRY(cudaMallocAsync((void**)&tc, n * 2, s));
+    CUDA_TRY(cudaMallocAsync((void**)&ra, n * 4, s));
+    CUDA_TRY(cudaMallocAsync((void**)&rd, n * 4, s));
+    CUDA_TRY(cudaMallocAsync((void**)&ta, n * 4, s));
+    CUDA_TRY(cudaMallocAsync((void**)&td, n * 4, s));
+    CUDA_TRY(cudaMallocAsync((void**)&cnt, 8 * 8, s));
+    pmsz_status st = segment_u32(nx, ny, nz, ref, ref_f32, rc, ra, rd, cnt + 7, s);
+    if (st == PMSZ_OK) st = segment_u32(nx, ny, nz, test, test_f32, tc, ta, td, cnt + 7, s);
+    if (st == PMSZ_OK) {
+        CUDA_TRY(cudaMemsetAsync(cnt, 0, 7 * 8, s));
+        k_plmss<<<grid_for((n + 31) / 32 * 32, 256, 16), 256, 0, s>>>(n, rc, tc, ra, ta, rd, td, kind_bits,
+                                                                       (n + 31) / 32, cnt);
+        LAUNCHED();
+        unsigned long long h[7];
+        CUDA_TRY(cudaMemcpyAsync(h, cnt, sizeof(h), cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        for (int k = 0; k < 7; ++k) counts[k] = (int64_t)h[k];
+    }
+    cudaFreeAsync(rc, s); cudaFreeAsync(tc, s); cudaFreeAsync(ra, s); cudaFreeAsync(rd, s);
+    cudaFreeAsync(ta, s); cudaFreeAsync(td, s); cudaFreeAsync(cnt, s);
+    CUDA_TRY(cudaGetLastError());
+    return st;
+}
+
+pmsz_status pmsz_bits_to_ids(const uint32_t* bits, int64_t nbits, int64_t* ids, int64_t cap, int64_t* count,
+                             void* stream) {
+    if (!bits || nbits < 0 || !count) return fail(PMSZ_ERR_INVALID, "bad arguments");
+    cudaStream_t s = S(stream);
+    const int64_t nwords = (nbits + 31) / 32;
+    const int64_t nblocks = std::max<int64_t>((nwords + kWordsPerBlock - 1) / kWordsPerBlock, 1);
+    unsigned long long* bc = nullptr;
+    CUDA_TRY(cudaMallocAsync((void**)&bc, (nblocks + 1) * 8, s));
+    k_bits_count<<<(unsigned)nblocks, kCompactThreads, 0, s>>>(bits, nwords, bc);
+    LAUNCHED();
+    k_exclusive_scan<<<1, 1024, 0, s>>>(bc, nblocks, bc + nblocks);
+    LAUNCHED();
+    unsigned long long total = 0;
+    CUDA_TRY(cudaMemcpyAsync(&total, bc + nblocks, 8, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    *count = (int64_t)total;
+    if (ids && (int64_t)total <= cap && total > 0) {
+        k_bits_list<int64_t><<<(unsigned)nblocks, kCompactThreads, 0, s>>>(const_cast<uint32_t*>(bits), nwords, bc,
+                                                                           ids, 0);
+        LAUNCHED();
+    }
+    cudaFreeAsync(bc, s);
+    CUDA_TRY(cudaGetLastError());
+    if (ids && (int64_t)total > cap) return fail(PMSZ_ERR_INVALID, "id buffer too small");
     return PMSZ_OK;
 }
 

@@ -60,25 +60,33 @@ constexpr int kAhead = 5;
 constexpr int kSlots = 8;
 static_assert(kAhead + 2 <= kSlots && (kSlots & (kSlots - 1)) == 0, "ring");
 
-__device__ __forceinline__ double dinf() { return __longlong_as_double(0x7ff0000000000000ll); }
+// The folds run in the type of the staged field: f32 originals are folded in
+// f32 (the f32 -> f64 promotion is exact and monotone, so ranks and
+// extremum flags are identical) -- no conversions, single-register selects.
+template <typename V> __device__ __forceinline__ V vinf();
+template <> __device__ __forceinline__ double vinf<double>() { return __longlong_as_double(0x7ff0000000000000ll); }
+template <> __device__ __forceinline__ float vinf<float>() { return __int_as_float(0x7f800000); }
 
 // A leaf value as seen by the max fold (-inf if missing) and the min fold (+inf).
+template <typename V>
 struct Leaf {
-    double mx, mn;
+    V mx, mn;
 };
-template <bool kEdge>
-__device__ __forceinline__ Leaf leaf(double v, bool miss) {
-    if (!kEdge) return Leaf{v, v};
-    return Leaf{miss ? -dinf() : v, miss ? dinf() : v};
+template <bool kEdge, typename V>
+__device__ __forceinline__ Leaf<V> leaf(V v, bool miss) {
+    if (!kEdge) return Leaf<V>{v, v};
+    return Leaf<V>{miss ? -vinf<V>() : v, miss ? vinf<V>() : v};
 }
 
 // x-pair (left = lower id): winner bit 1 = right.
+template <typename V>
 struct Pair {
-    double mx, mn;
+    V mx, mn;
     int bx, bn;
 };
-__device__ __forceinline__ Pair xpair(const Leaf& l, const Leaf& r) {
-    Pair p;
+template <typename V>
+__device__ __forceinline__ Pair<V> xpair(const Leaf<V>& l, const Leaf<V>& r) {
+    Pair<V> p;
     const bool tx = r.mx >= l.mx;   // ties -> larger id
     p.mx = tx ? r.mx : l.mx;
     p.bx = tx;
@@ -89,12 +97,14 @@ __device__ __forceinline__ Pair xpair(const Leaf& l, const Leaf& r) {
 }
 
 // 2x2 box from the x-pairs of rows r (lo) and r+1 (hi): corner 0..3 in id order.
+template <typename V>
 struct Quad {
-    double mx, mn;
+    V mx, mn;
     int cx, cn;
 };
-__device__ __forceinline__ Quad ybox(const Pair& lo, const Pair& hi) {
-    Quad b;
+template <typename V>
+__device__ __forceinline__ Quad<V> ybox(const Pair<V>& lo, const Pair<V>& hi) {
+    Quad<V> b;
     const bool tx = hi.mx >= lo.mx;
     b.mx = tx ? hi.mx : lo.mx;
     b.cx = tx ? 2 + hi.bx : lo.bx;
@@ -103,15 +113,19 @@ __device__ __forceinline__ Quad ybox(const Pair& lo, const Pair& hi) {
     b.cn = tn ? 2 + hi.bn : lo.bn;
     return b;
 }
-__device__ __forceinline__ Quad missing_quad() { return Quad{-dinf(), dinf(), 0, 0}; }
+template <typename V>
+__device__ __forceinline__ Quad<V> missing_quad() { return Quad<V>{-vinf<V>(), vinf<V>(), 0, 0}; }
 
 // Running fold in ascending rank order.
+template <typename V>
 struct Acc {
-    double mx, mn;
+    V mx, mn;
     int rx, rn;
 };
-__device__ __forceinline__ Acc acc_from(const Quad& b) { return Acc{b.mx, b.mn, b.cx, b.cn}; }
-__device__ __forceinline__ void acc_pair(Acc& a, const Pair& p, int base) {
+template <typename V>
+__device__ __forceinline__ Acc<V> acc_from(const Quad<V>& b) { return Acc<V>{b.mx, b.mn, b.cx, b.cn}; }
+template <typename V>
+__device__ __forceinline__ void acc_pair(Acc<V>& a, const Pair<V>& p, int base) {
     const bool tx = p.mx >= a.mx;
     a.mx = tx ? p.mx : a.mx;
     a.rx = tx ? base + p.bx : a.rx;
@@ -119,7 +133,8 @@ __device__ __forceinline__ void acc_pair(Acc& a, const Pair& p, int base) {
     a.mn = tn ? p.mn : a.mn;
     a.rn = tn ? base + p.bn : a.rn;
 }
-__device__ __forceinline__ void acc_leaf(Acc& a, const Leaf& l, int rank) {
+template <typename V>
+__device__ __forceinline__ void acc_leaf(Acc<V>& a, const Leaf<V>& l, int rank) {
     const bool tx = l.mx >= a.mx;
     a.mx = tx ? l.mx : a.mx;
     a.rx = tx ? rank : a.rx;
@@ -127,7 +142,8 @@ __device__ __forceinline__ void acc_leaf(Acc& a, const Leaf& l, int rank) {
     a.mn = tn ? l.mn : a.mn;
     a.rn = tn ? rank : a.rn;
 }
-__device__ __forceinline__ void acc_quad(Acc& a, const Quad& b, int base) {
+template <typename V>
+__device__ __forceinline__ void acc_quad(Acc<V>& a, const Quad<V>& b, int base) {
     const bool tx = b.mx >= a.mx;
     a.mx = tx ? b.mx : a.mx;
     a.rx = tx ? base + b.cx : a.rx;
@@ -135,11 +151,12 @@ __device__ __forceinline__ void acc_quad(Acc& a, const Quad& b, int base) {
     a.mn = tn ? b.mn : a.mn;
     a.rn = tn ? base + b.cn : a.rn;
 }
-__device__ __forceinline__ Scan acc_scan(const Acc& a, double vc) {
+template <typename V>
+__device__ __forceinline__ Scan acc_scan(const Acc<V>& a, V vc) {
     Scan s;
-    s.vc = vc;
-    s.vmax = a.mx;
-    s.vmin = a.mn;
+    s.vc = (double)vc;
+    s.vmax = (double)a.mx;
+    s.vmin = (double)a.mn;
     s.rmax = a.rx;
     s.rmin = a.rn;
     s.is_max = (a.mx < vc) || (a.mx == vc && a.rx <= kCenterBelow);   // topology.py:79
@@ -246,35 +263,36 @@ struct PrepOp {
 // ---------------------------------------------------------------------------
 // Per-plane work of one thread: six x-pairs, two U boxes, two D boxes and the
 // in-plane groups of its two centres.
+template <typename V>
 struct PlaneOut {
-    Quad ua, ub;       // U groups of centres (x, ya) and (x, yb) at plane p-1
-    Quad da, db;       // D groups of the same centres at plane p+1
-    Pair h1, h2, h5, h6;   // in-plane x-pairs of plane p
-    Leaf b, c, i, j;   // in-plane singles of plane p
-    double fa, fb;     // centre values at plane p
+    Quad<V> ua, ub;           // U groups of centres (x, ya) and (x, yb) at plane p-1
+    Quad<V> da, db;           // D groups of the same centres at plane p+1
+    Pair<V> h1, h2, h5, h6;   // in-plane x-pairs of plane p
+    Leaf<V> b, c, i, j;       // in-plane singles of plane p
+    V fa, fb;                 // centre values at plane p
 };
 
-template <bool kEdge, typename T>
-__device__ __forceinline__ PlaneOut plane_work(const T* __restrict__ s, int cell, bool mxl, bool mxr, bool myl,
-                                               bool myb, bool my2) {
+template <bool kEdge, typename V>
+__device__ __forceinline__ PlaneOut<V> plane_work(const V* __restrict__ s, int cell, bool mxl, bool mxr, bool myl,
+                                                  bool myb, bool my2) {
     // column x-1: rows ya-1, ya, yb; column x: ya-1..ya+2; column x+1: ya..ya+2
-    const Leaf a = leaf<kEdge>((double)s[cell - kPX - 1], mxl || myl);
-    const Leaf b = leaf<kEdge>((double)s[cell - 1], mxl);
-    const Leaf c = leaf<kEdge>((double)s[cell + kPX - 1], mxl || myb);
-    const Leaf e = leaf<kEdge>((double)s[cell - kPX], myl);
-    const double fv = (double)s[cell];
-    const double gv = (double)s[cell + kPX];
-    const Leaf f{fv, fv};
-    const Leaf g = leaf<kEdge>(gv, myb);
-    const Leaf h = leaf<kEdge>((double)s[cell + 2 * kPX], my2);
-    const Leaf i = leaf<kEdge>((double)s[cell + 1], mxr);
-    const Leaf j = leaf<kEdge>((double)s[cell + kPX + 1], mxr || myb);
-    const Leaf k = leaf<kEdge>((double)s[cell + 2 * kPX + 1], mxr || my2);
-    PlaneOut o;
+    const Leaf<V> a = leaf<kEdge>(s[cell - kPX - 1], mxl || myl);
+    const Leaf<V> b = leaf<kEdge>(s[cell - 1], mxl);
+    const Leaf<V> c = leaf<kEdge>(s[cell + kPX - 1], mxl || myb);
+    const Leaf<V> e = leaf<kEdge>(s[cell - kPX], myl);
+    const V fv = s[cell];
+    const V gv = s[cell + kPX];
+    const Leaf<V> f{fv, fv};
+    const Leaf<V> g = leaf<kEdge>(gv, myb);
+    const Leaf<V> h = leaf<kEdge>(s[cell + 2 * kPX], my2);
+    const Leaf<V> i = leaf<kEdge>(s[cell + 1], mxr);
+    const Leaf<V> j = leaf<kEdge>(s[cell + kPX + 1], mxr || myb);
+    const Leaf<V> k = leaf<kEdge>(s[cell + 2 * kPX + 1], mxr || my2);
+    PlaneOut<V> o;
     o.h1 = xpair(a, e);   // (x-1, ya-1)
     o.h2 = xpair(b, f);   // (x-1, ya)
-    const Pair h3 = xpair(c, g);   // (x-1, yb)
-    const Pair h4 = xpair(f, i);   // (x, ya)
+    const Pair<V> h3 = xpair(c, g);   // (x-1, yb)
+    const Pair<V> h4 = xpair(f, i);   // (x, ya)
     o.h5 = xpair(g, j);   // (x, yb)
     o.h6 = xpair(h, k);   // (x, ya+2)
     o.ua = ybox(h4, o.h5);
@@ -288,16 +306,18 @@ __device__ __forceinline__ PlaneOut plane_work(const T* __restrict__ s, int cell
 }
 
 // Partial fold of the groups of ranks 0..9 (D, in-plane).
-__device__ __forceinline__ Acc partial_a(const Quad& d, const PlaneOut& o) {
-    Acc a = acc_from(d);
+template <typename V>
+__device__ __forceinline__ Acc<V> partial_a(const Quad<V>& d, const PlaneOut<V>& o) {
+    Acc<V> a = acc_from(d);
     acc_pair(a, o.h1, 4);
     acc_leaf(a, o.b, 6);
     acc_leaf(a, o.i, 7);
     acc_pair(a, o.h5, 8);
     return a;
 }
-__device__ __forceinline__ Acc partial_b(const Quad& d, const PlaneOut& o) {
-    Acc a = acc_from(d);
+template <typename V>
+__device__ __forceinline__ Acc<V> partial_b(const Quad<V>& d, const PlaneOut<V>& o) {
+    Acc<V> a = acc_from(d);
     acc_pair(a, o.h2, 4);
     acc_leaf(a, o.c, 6);
     acc_leaf(a, o.j, 7);
@@ -375,18 +395,18 @@ __device__ __forceinline__ void tiled_body(const Dom& d, T (*sm)[kPlane], Stager
     // prologue: plane zb-1 (D groups), plane zb (partial folds)
     cp_async_wait<kAhead>();
     __syncthreads();
-    Quad da, db;
+    Quad<T> da, db;
     if (zb - 1 >= 0) {
-        const PlaneOut o = plane_work<kEdge>(sm[0], cell, mxl, mxr, myl, myb, my2);
+        const PlaneOut<T> o = plane_work<kEdge>(sm[0], cell, mxl, mxr, myl, myb, my2);
         da = o.da;
         db = o.db;
     } else {
-        da = db = missing_quad();
+        da = db = missing_quad<T>();
     }
-    Acc pa, pb;
-    double fa, fb;
+    Acc<T> pa, pb;
+    T fa, fb;
     {
-        const PlaneOut o = plane_work<kEdge>(sm[1], cell, mxl, mxr, myl, myb, my2);
+        const PlaneOut<T> o = plane_work<kEdge>(sm[1], cell, mxl, mxr, myl, myb, my2);
         pa = partial_a(da, o);
         pb = partial_b(db, o);
         da = o.da;
@@ -414,15 +434,15 @@ __device__ __forceinline__ void tiled_body(const Dom& d, T (*sm)[kPlane], Stager
         if (op.skippable())
             work = __any_sync(0xffffffffu, op.wants(pa0) || op.wants(pb0) || op.wants(pa1) || op.wants(pb1) ||
                                                op.wants(pa2) || op.wants(pb2));
-        PlaneOut o;
+        PlaneOut<T> o;
         if (kUp && work) o = plane_work<kEdge>(sm[(k + 2) & (kSlots - 1)], cell, mxl, mxr, myl, myb, my2);
         if (work && live_a && op.wants(pa0)) {
-            Acc a = pa;
+            Acc<T> a = pa;
             if (kUp) acc_quad(a, o.ua, 10);
             op.center(d, ca, acc_scan(a, fa), pa0);
         }
         if (work && live_b && op.wants(pb0)) {
-            Acc a = pb;
+            Acc<T> a = pb;
             if (kUp) acc_quad(a, o.ub, 10);
             op.center(d, ca + sy, acc_scan(a, fb), pb0);
         }

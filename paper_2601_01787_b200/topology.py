@@ -1,9 +1,11 @@
 """Steepest-neighbour topology on the GPU (mirror of topocorrect.topology).
 
 ``scan_neighbors`` runs the K-scan kernel (topology.py:47-86 semantics:
-(value, id)-largest / smallest neighbour, is_max / is_min).  The segmentation
-and full ``compare_plmss`` are SURVEY §8(f) rank 1 ("next"); the correction
-path only needs the clean-report certificate described in correction.py.
+(value, id)-largest / smallest neighbour, is_max / is_min).
+``compute_segmentation`` and ``compare_plmss`` (topology.py:156-174,254-274)
+run on the device too (csrc/segment.cuh: 16-bit full codes, pointer jumping
+to the path roots, the six kinds as bitmaps); the correction path itself
+only needs the clean-report certificate described in correction.py.
 """
 
 from __future__ import annotations
@@ -120,3 +122,88 @@ class DistortionReport:
                 "asc_order_violations": self.asc_order_violations.tolist(),
                 "desc_order_violations": self.desc_order_violations.tolist(),
                 "wrong_label_count": int(self.wrong_label_count), "clean": self.is_clean}
+
+
+# ---------------------------------------------------------------------------
+# segmentation (topology.py:127-174)
+@dataclass(frozen=True, eq=False)
+class SegmentationLabels:
+    """asc_target: minimum reached by the descending path of each vertex;
+    desc_target: maximum reached by the ascending path (topology.py:127-140)."""
+
+    dims: tuple
+    asc_target: np.ndarray
+    desc_target: np.ndarray
+
+    def pair_equal(self, other: "SegmentationLabels") -> np.ndarray:
+        return np.logical_and(self.asc_target == other.asc_target, self.desc_target == other.desc_target)
+
+
+def _as_device(values, dev) -> torch.Tensor:
+    if isinstance(values, torch.Tensor):
+        return values.to(dev) if values.device != dev else values
+    v = np.ascontiguousarray(values)
+    if v.dtype not in (np.float32, np.float64):
+        v = v.astype(np.float64)
+    return torch.from_numpy(v).to(dev)
+
+
+def compute_segmentation_device(values: torch.Tensor, dims) -> tuple[torch.Tensor, torch.Tensor]:
+    """(asc_target, desc_target) int64 device tensors of a f64/f32 device field."""
+    nx, ny, nz = _dims3(dims)
+    n = nx * ny * nz
+    asc = torch.empty(n, dtype=torch.int64, device=values.device)
+    desc = torch.empty(n, dtype=torch.int64, device=values.device)
+    N.check(N.lib().pmsz_segmentation(nx, ny, nz, N.ptr(values), int(values.dtype == torch.float32), N.ptr(asc),
+                                      N.ptr(desc), N.stream_handle()), "pmsz_segmentation")
+    return asc, desc
+
+
+def compute_segmentation(field: ScalarField) -> SegmentationLabels:
+    dev = torch.device("cuda", torch.cuda.current_device())
+    asc, desc = compute_segmentation_device(_as_device(field.values, dev), field.dims)
+    return SegmentationLabels(dims=field.dims, asc_target=asc.cpu().numpy(), desc_target=desc.cpu().numpy())
+
+
+def _bits_to_ids(bits: torch.Tensor, nbits: int) -> np.ndarray:
+    cnt = N.ctypes.c_int64()
+    lib = N.lib()
+    N.check(lib.pmsz_bits_to_ids(N.ptr(bits), nbits, None, 0, N.ctypes.byref(cnt), N.stream_handle()),
+            "pmsz_bits_to_ids")
+    m = int(cnt.value)
+    if m == 0:
+        return _empty()
+    ids = torch.empty(m, dtype=torch.int64, device=bits.device)
+    N.check(lib.pmsz_bits_to_ids(N.ptr(bits), nbits, N.ptr(ids), m, N.ctypes.byref(cnt), N.stream_handle()),
+            "pmsz_bits_to_ids")
+    return ids.cpu().numpy()
+
+
+def compare_plmss_device(reference: torch.Tensor, test: torch.Tensor, dims,
+                         with_sets: bool = True) -> DistortionReport:
+    """compare_plmss on device fields (f64 or f32 each)."""
+    nx, ny, nz = _dims3(dims)
+    n = nx * ny * nz
+    nwords = (n + 31) // 32
+    bits = torch.zeros(6 * nwords, dtype=torch.int32, device=reference.device) if with_sets else None
+    counts = (N.ctypes.c_int64 * 7)()
+    N.check(N.lib().pmsz_compare_plmss(nx, ny, nz, N.ptr(reference), int(reference.dtype == torch.float32),
+                                       N.ptr(test), int(test.dtype == torch.float32),
+                                       N.ptr(bits) if bits is not None else None, counts, N.stream_handle()),
+            "pmsz_compare_plmss")
+    if not with_sets:
+        # sized placeholders: only the counts are meaningful
+        sets = [np.zeros(int(counts[k]), dtype=np.int64) for k in range(6)]
+    else:
+        sets = [_bits_to_ids(bits[k * nwords:(k + 1) * nwords], n) if counts[k] else _empty() for k in range(6)]
+    return DistortionReport(fp_max=sets[0], fn_max=sets[1], fp_min=sets[2], fn_min=sets[3],
+                            asc_order_violations=sets[4], desc_order_violations=sets[5],
+                            wrong_label_count=int(counts[6]))
+
+
+def compare_plmss(reference: ScalarField, test: ScalarField) -> DistortionReport:
+    """Distortion report of test relative to reference (topology.py:254-274)."""
+    if reference.dims != test.dims:
+        raise ValueError(f"dims differ: {reference.dims} vs {test.dims}")
+    dev = torch.device("cuda", torch.cuda.current_device())
+    return compare_plmss_device(_as_device(reference.values, dev), _as_device(test.values, dev), reference.dims)

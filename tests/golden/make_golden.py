@@ -208,6 +208,44 @@ def main():
                         "max_vertex_edits": res.max_vertex_edits, "corrected_sha256": sha(res.corrected.values)})
     meta["parallel"] = par
 
+    # ---- segmentation + compare_plmss (topology.py:156-174,254-274; test_codec.py:15-26)
+    segs = []
+    gf = tc.perlin(tc.NoiseSpec(dims=(8, 8, 8), seed=42))
+    lab = tc.compute_segmentation(gf)
+    meta["golden_labels"] = {
+        "asc_file_sha256": hashlib.sha256(codec.write_labels(gf.dims, lab.asc_target)).hexdigest(),
+        "desc_file_sha256": hashlib.sha256(codec.write_labels(gf.dims, lab.desc_target)).hexdigest(),
+        "field_file_sha256": hashlib.sha256(codec.write_field(gf)).hexdigest(),
+        "field_f32_file_sha256": hashlib.sha256(codec.write_field(gf, precision="f32")).hexdigest(),
+    }
+    for i, (dims, style) in enumerate([((8, 8, 8), "perlin"), ((9, 7, 5), "plateau"), ((16, 12, 1), "uniform"),
+                                      ((6, 6, 6), "ramp"), ((13, 11, 7), "coarse"), ((24, 20, 16), "perlin")]):
+        n = int(np.prod(dims))
+        if style == "perlin":
+            v = tc.perlin(tc.NoiseSpec(dims=dims, seed=i + 3)).values
+        elif style == "plateau":
+            v = rng.integers(0, 3, size=n).astype(np.float64)
+        elif style == "uniform":
+            v = rng.standard_normal(n)
+        elif style == "ramp":
+            v = np.arange(n, dtype=np.float64) * 0.5
+        else:
+            v = np.round(rng.standard_normal(n), 1)
+        f = tc.ScalarField(dims, v)
+        lab = tc.compute_segmentation(f)
+        key = f"seg_{i}"
+        arrays[key + "_v"] = v
+        arrays[key + "_asc"] = lab.asc_target
+        arrays[key + "_desc"] = lab.desc_target
+        # a perturbed copy for compare_plmss: noise plus a few forced ties
+        w = v + np.round(rng.standard_normal(n) * 0.3, 1)
+        w[rng.integers(0, n, size=max(1, n // 10))] = float(np.median(v))
+        t = tc.ScalarField(dims, w)
+        rep = tc.compare_plmss(f, t)
+        arrays[key + "_w"] = w
+        segs.append({"key": key, "dims": list(dims), "style": style, "report": rep.to_dict()})
+    meta["segmentation"] = segs
+
     (OUT / "golden.json").write_text(json.dumps(meta, indent=1, sort_keys=True))
     np.savez_compressed(OUT / "golden.npz", **arrays)
     print("wrote", OUT / "golden.json", OUT / "golden.npz",

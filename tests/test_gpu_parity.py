@@ -311,3 +311,48 @@ def test_device_engines_pairwise_exchange_match_reference(golden, idx):
                                    sp.core_lo[0]:sp.core_hi[0]]
         assert e.residual() == 0
     assert sha(g.reshape(-1)) == case["corrected_sha256"], case["name"]
+
+
+# --- segmentation / compare_plmss on the device ---------------------------------
+def test_segmentation_matches_reference(golden):
+    meta, arrays = golden
+    for case in meta["segmentation"]:
+        k = case["key"]
+        lab = pm.compute_segmentation(sf(tuple(case["dims"]), arrays[k + "_v"]))
+        assert np.array_equal(lab.asc_target, arrays[k + "_asc"]), k
+        assert np.array_equal(lab.desc_target, arrays[k + "_desc"]), k
+    g = meta["golden_labels"]
+    f = sf((8, 8, 8), orc.perlin((8, 8, 8), 42))
+    lab = pm.compute_segmentation(f)
+    assert hashlib.sha256(pm.write_labels(f.dims, lab.asc_target)).hexdigest() == g["asc_file_sha256"]
+    assert hashlib.sha256(pm.write_labels(f.dims, lab.desc_target)).hexdigest() == g["desc_file_sha256"]
+
+
+def test_compare_plmss_matches_reference(golden):
+    meta, arrays = golden
+    for case in meta["segmentation"]:
+        k = case["key"]
+        dims = tuple(case["dims"])
+        rep = pm.compare_plmss(sf(dims, arrays[k + "_v"]), sf(dims, arrays[k + "_w"]))
+        assert rep.to_dict() == case["report"], k
+
+
+@pytest.mark.parametrize("n", [64, 128])
+def test_segmentation_and_plmss_match_oracle_at_scale(n):
+    from paper_2601_01787_b200.topology import compare_plmss_device, compute_segmentation_device
+    dims = (n, n, n)
+    f32 = gen.perlin_device(gen.NoiseSpec(dims, 5), f32=True)
+    xi = gen.relative_to_absolute_device(f32, 1e-3)
+    fh = gen.quantize_device(f32, xi)
+    f64 = f32.double().cpu().numpy()
+    a, d = compute_segmentation_device(f32, dims)
+    ra, rd = orc.segmentation(f64, dims)
+    assert np.array_equal(a.cpu().numpy(), ra) and np.array_equal(d.cpu().numpy(), rd)
+    rep = compare_plmss_device(f32, fh, dims)
+    ref = orc.compare_plmss(f64, fh.cpu().numpy(), dims)
+    for name in ("fp_max", "fn_max", "fp_min", "fn_min", "asc_order_violations", "desc_order_violations"):
+        assert np.array_equal(getattr(rep, name), ref[name]), name
+    assert rep.wrong_label_count == ref["wrong_label_count"] > 0
+    # the corrected field is clean against the original (correction.py:427-429)
+    out = pm.run_correction_device(f32, fh, dims, pm.CorrectionConfig(xi_abs=xi))
+    assert compare_plmss_device(f32, out.corrected, dims).is_clean

@@ -137,3 +137,64 @@ def test_bounded_noise_respects_bound_and_floor():
     part = orc.bounded_noise(f.reshape(8, 12, 16)[2:5, 1:7, 4:9].reshape(-1), (5, 6, 3), xi, 11,
                              gdims=dims, lo=(4, 1, 2))
     assert np.array_equal(part, fh.reshape(8, 12, 16)[2:5, 1:7, 4:9].reshape(-1))
+
+
+# --- segmentation / compare_plmss / field + label files ------------------------
+def test_oracle_segmentation_matches_reference(golden):
+    meta, arrays = golden
+    for case in meta["segmentation"]:
+        k = case["key"]
+        a, d = orc.segmentation(arrays[k + "_v"], case["dims"])
+        assert np.array_equal(a, arrays[k + "_asc"]), k
+        assert np.array_equal(d, arrays[k + "_desc"]), k
+
+
+def test_oracle_compare_plmss_matches_reference(golden):
+    meta, arrays = golden
+    for case in meta["segmentation"]:
+        k = case["key"]
+        rep = orc.compare_plmss(arrays[k + "_v"], arrays[k + "_w"], case["dims"])
+        ref = case["report"]
+        for name in ("fp_max", "fn_max", "fp_min", "fn_min", "asc_order_violations", "desc_order_violations"):
+            assert rep[name].tolist() == ref[name], (k, name)
+        assert rep["wrong_label_count"] == ref["wrong_label_count"], k
+
+
+def test_golden_field_and_label_files(golden):
+    """test_codec.py:15-26,228-235: the reference's golden field / label file
+    hashes, reproduced through this codec from the oracle's Perlin and
+    segmentation."""
+    import paper_2601_01787_b200 as pm
+    meta, _ = golden
+    g = meta["golden_labels"]
+    f = pm.ScalarField((8, 8, 8), orc.perlin((8, 8, 8), 42))
+    assert hashlib.sha256(codec.write_field(f)).hexdigest() == g["field_file_sha256"]
+    assert hashlib.sha256(codec.write_field(f, precision="f32")).hexdigest() == g["field_f32_file_sha256"]
+    a, d = orc.segmentation(f.values, f.dims)
+    assert hashlib.sha256(codec.write_labels(f.dims, a)).hexdigest() == g["asc_file_sha256"]
+    assert hashlib.sha256(codec.write_labels(f.dims, d)).hexdigest() == g["desc_file_sha256"]
+
+
+def test_field_and_label_codec_round_trips():
+    import paper_2601_01787_b200 as pm
+    f = pm.ScalarField((6, 5, 4), orc.perlin((6, 5, 4), 0))
+    back = codec.read_field(codec.write_field(f))
+    assert back.dims == f.dims and np.array_equal(back.values, f.values)
+    b32 = codec.read_field(codec.write_field(f, precision="f32"))
+    assert np.array_equal(b32.values, f.values.astype(np.float32).astype(np.float64))
+    f2 = pm.ScalarField((4, 3), orc.perlin((4, 3, 1), 3))
+    data2 = codec.write_field(f2, precision="f32")
+    assert data2[8] == 2 and codec.read_field(data2).dims == (4, 3, 1)
+    a, _ = orc.segmentation(f.values, f.dims)
+    dims, lab = codec.read_labels(codec.write_labels(f.dims, a))
+    assert dims == f.dims and np.array_equal(lab, a)
+    with pytest.raises(codec.FormatError):
+        codec.read_labels(codec.write_field(f))
+    with pytest.raises(codec.FormatError):
+        codec.read_field(codec.write_labels(f.dims, a))
+    with pytest.raises(ValueError):
+        codec.write_labels((2, 2, 1), np.array([0, 1, 2]))
+    with pytest.raises(ValueError):
+        codec.write_labels((2, 2, 1), np.array([0, 1, 2, 4]))
+    with pytest.raises(codec.FormatError):
+        codec.read_field(codec.write_field(f) + b"\x00")
