@@ -256,6 +256,12 @@ pmsz_status pmsz_quantize(const void* f_dev, int32_t is_f32, int64_t n, double o
 pmsz_status pmsz_bounded_noise(const void* f_dev, int32_t is_f32, int64_t nx, int64_t ny,
                                int64_t nz, const int64_t gdims[3], const int64_t lo[3],
                                double xi, uint64_t seed, double* out_dev, void* stream);
+/* HEDM-like Gaussian-peak stack (BASELINE config 5; not in the reference):
+ * sparse Gaussian spots in (64,64,32)-voxel cells over a faint hash-noise
+ * background, for the sub-box [lo, lo+ext) of a global grid; f64 or f32
+ * output.  Bit-identical to the oracle's orc_peaks (det_exp, no FMA). */
+pmsz_status pmsz_gaussian_peaks(const int64_t gdims[3], const int64_t lo[3], const int64_t ext[3], uint64_t seed,
+                                int32_t out_f32, void* out_dev, void* stream);
 /* Copy a sub-box of a global device array into a contiguous domain array (f64 or f32). */
 pmsz_status pmsz_box_extract(const int64_t gdims[3], const void* src_dev, int32_t is_f32,
                              const int64_t lo[3], const int64_t ext[3], void* dst_dev, void* stream);

@@ -452,3 +452,60 @@ void orc_bounded_noise(const double* f, int64_t nx, int64_t ny, int64_t nz, cons
         out[i] = v;
     }
 }
+
+/* ---- HEDM-like Gaussian-peak stack (BASELINE config 5) ---------
+ * The generator is new (the reference has none); this is its CPU definition,
+ * written operation by operation like gen.cuh's peak_value so both produce
+ * the same bits (no contraction here, --fmad=false there). */
+static double det_exp(double x) {
+    if (x < -700.0) return 0.0;
+    const double kf = floor(x * 1.4426950408889634 + 0.5);
+    const double r = (x - kf * 0.6931471803691238) - kf * 1.9082149292705877e-10;
+    double p = 2.505210838544172e-08;
+    p = p * r + 2.755731922398589e-07;
+    p = p * r + 2.7557319223985893e-06;
+    p = p * r + 2.48015873015873e-05;
+    p = p * r + 0.0001984126984126984;
+    p = p * r + 0.001388888888888889;
+    p = p * r + 0.008333333333333333;
+    p = p * r + 0.041666666666666664;
+    p = p * r + 0.16666666666666666;
+    p = p * r + 0.5;
+    p = p * r + 1.0;
+    p = p * r + 1.0;
+    return ldexp(p, (int)kf);
+}
+
+static double peak_u(uint64_t seed, uint64_t cell, int k) {
+    return (double)(mix64(seed ^ 0x5EEDC0DEULL, cell * 8ull + (uint64_t)k) >> 11) * 0x1.0p-53;
+}
+
+static double peak_value(const int64_t* gd, uint64_t seed, int64_t x, int64_t y, int64_t z) {
+    const int64_t CX = 64, CY = 64, CZ = 32;
+    const int64_t ncx = (gd[0] + CX - 1) / CX, ncy = (gd[1] + CY - 1) / CY;
+    const int64_t cx = x / CX, cy = y / CY, cz = z / CZ;
+    const uint64_t cell = (uint64_t)(cx + ncx * (cy + ncy * cz));
+    const uint64_t gid = (uint64_t)(x + gd[0] * (y + gd[1] * z));
+    const double bg = 0.02 * ((double)(mix64(seed, gid) >> 11) * 0x1.0p-53);
+    if (!(peak_u(seed, cell, 0) < 0.6)) return bg;
+    const double amp = 0.2 + 0.8 * peak_u(seed, cell, 1);
+    const double sx = 1.0 + 2.0 * peak_u(seed, cell, 2);
+    const double sy = 1.0 + 2.0 * peak_u(seed, cell, 3);
+    const double sz = 0.7 + 1.3 * peak_u(seed, cell, 4);
+    const double px = (double)(cx * CX) + 12.0 + peak_u(seed, cell, 5) * (double)(CX - 24);
+    const double py = (double)(cy * CY) + 12.0 + peak_u(seed, cell, 6) * (double)(CY - 24);
+    const double pz = (double)(cz * CZ) + 8.0 + peak_u(seed, cell, 7) * (double)(CZ - 16);
+    const double dx = (double)x - px, dy = (double)y - py, dz = (double)z - pz;
+    if (fabs(dx) > 4.0 * sx || fabs(dy) > 4.0 * sy || fabs(dz) > 4.0 * sz) return bg;
+    const double q = (dx * dx) / (2.0 * sx * sx) + (dy * dy) / (2.0 * sy * sy) + (dz * dz) / (2.0 * sz * sz);
+    return bg + amp * det_exp(-q);
+}
+
+void orc_peaks(const int64_t* gdims, const int64_t* lo, const int64_t* ext, uint64_t seed, double* out) {
+    const int64_t n = ext[0] * ext[1] * ext[2];
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; ++i) {
+        const int64_t z = i / (ext[0] * ext[1]), r = i - z * ext[0] * ext[1], y = r / ext[0], x = r - y * ext[0];
+        out[i] = peak_value(gdims, seed, lo[0] + x, lo[1] + y, lo[2] + z);
+    }
+}

@@ -17,6 +17,6 @@ from .parallel import (Block, BlockDecomposition, ParallelStats, SyncStrategy, b
                        run_parallel)
 from .codec import (FormatError, decode_edits, decode_edits_meta, encode_edits, read_field, read_labels,
                     write_field, write_labels)
-from .inputs import NoiseSpec
+from .inputs import NoiseSpec, PeakSpec
 
 __version__ = "0.1.0"

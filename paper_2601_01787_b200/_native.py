@@ -103,6 +103,7 @@ SIGNATURES = {
     "pmsz_bounded_noise": (i32, [vp, i32, i64, i64, i64, i64p, i64p, ctypes.c_double, u64, vp, vp]),
     "pmsz_box_extract": (i32, [i64p, vp, i32, i64p, i64p, vp, vp]),
     "pmsz_segmentation": (i32, [i64, i64, i64, vp, i32, vp, vp, vp]),
+    "pmsz_gaussian_peaks": (i32, [i64p, i64p, i64p, u64, i32, vp, vp]),
     "pmsz_compare_plmss": (i32, [i64, i64, i64, vp, i32, vp, i32, vp, i64p, vp]),
     "pmsz_bits_to_ids": (i32, [vp, i64, vp, i64, i64p, vp]),
 }

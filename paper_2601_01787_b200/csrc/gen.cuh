@@ -159,4 +159,74 @@ __global__ void __launch_bounds__(256) k_bounded_noise(const FT* __restrict__ f,
     }
 }
 
+// ---- HEDM-like Gaussian-peak stack (BASELINE config 5) ----------
+// Not in the reference: a stack of detector frames (z) with sparse Gaussian
+// diffraction spots over a faint hash-noise background.  The domain is cut
+// into cells of (64, 64, 32) voxels; a cell holds one peak with probability
+// 0.6, of amplitude A in [0.2, 1), widths sx, sy in [1, 3), sz in [0.7, 2)
+// and a centre kept >= 4 sigma from the cell faces, truncated at 4 sigma:
+//   v = bg + A * exp(-(dx^2/(2 sx^2) + dy^2/(2 sy^2) + dz^2/(2 sz^2)))
+// All arithmetic is +, -, *, / in a fixed order plus det_exp (Cody-Waite
+// reduction + degree-11 Horner + ldexp), so the oracle (C, no contraction)
+// and this kernel (--fmad=false) produce identical bits.
+struct PeakArgs {
+    int64_t gnx, gny, gnz;        // global dims
+    int64_t lox, loy, loz;        // sub-box origin
+    int64_t nx, ny, nz;           // sub-box extents
+    uint64_t seed;
+};
+constexpr int64_t kPeakCX = 64, kPeakCY = 64, kPeakCZ = 32;
+
+__host__ __device__ __forceinline__ double det_exp(double x) {
+    if (x < -700.0) return 0.0;
+    const double kf = floor(x * 1.4426950408889634 + 0.5);
+    const double r = (x - kf * 0.6931471803691238) - kf * 1.9082149292705877e-10;
+    double p = 2.505210838544172e-08;
+    p = p * r + 2.755731922398589e-07;
+    p = p * r + 2.7557319223985893e-06;
+    p = p * r + 2.48015873015873e-05;
+    p = p * r + 0.0001984126984126984;
+    p = p * r + 0.001388888888888889;
+    p = p * r + 0.008333333333333333;
+    p = p * r + 0.041666666666666664;
+    p = p * r + 0.16666666666666666;
+    p = p * r + 0.5;
+    p = p * r + 1.0;
+    p = p * r + 1.0;
+    return ldexp(p, (int)kf);
+}
+
+__host__ __device__ __forceinline__ double peak_u(uint64_t seed, uint64_t cell, int k) {
+    return (double)(mix64(seed ^ 0x5EEDC0DEULL, cell * 8ull + (uint64_t)k) >> 11) * 0x1.0p-53;
+}
+
+__host__ __device__ __forceinline__ double peak_value(const PeakArgs& a, int64_t x, int64_t y, int64_t z) {
+    const int64_t ncx = (a.gnx + kPeakCX - 1) / kPeakCX, ncy = (a.gny + kPeakCY - 1) / kPeakCY;
+    const int64_t cx = x / kPeakCX, cy = y / kPeakCY, cz = z / kPeakCZ;
+    const uint64_t cell = (uint64_t)(cx + ncx * (cy + ncy * cz));
+    const uint64_t gid = (uint64_t)(x + a.gnx * (y + a.gny * z));
+    const double bg = 0.02 * ((double)(mix64(a.seed, gid) >> 11) * 0x1.0p-53);
+    if (!(peak_u(a.seed, cell, 0) < 0.6)) return bg;
+    const double amp = 0.2 + 0.8 * peak_u(a.seed, cell, 1);
+    const double sx = 1.0 + 2.0 * peak_u(a.seed, cell, 2);
+    const double sy = 1.0 + 2.0 * peak_u(a.seed, cell, 3);
+    const double sz = 0.7 + 1.3 * peak_u(a.seed, cell, 4);
+    const double px = (double)(cx * kPeakCX) + 12.0 + peak_u(a.seed, cell, 5) * (double)(kPeakCX - 24);
+    const double py = (double)(cy * kPeakCY) + 12.0 + peak_u(a.seed, cell, 6) * (double)(kPeakCY - 24);
+    const double pz = (double)(cz * kPeakCZ) + 8.0 + peak_u(a.seed, cell, 7) * (double)(kPeakCZ - 16);
+    const double dx = (double)x - px, dy = (double)y - py, dz = (double)z - pz;
+    if (fabs(dx) > 4.0 * sx || fabs(dy) > 4.0 * sy || fabs(dz) > 4.0 * sz) return bg;
+    const double q = (dx * dx) / (2.0 * sx * sx) + (dy * dy) / (2.0 * sy * sy) + (dz * dz) / (2.0 * sz * sz);
+    return bg + amp * det_exp(-q);
+}
+
+template <typename OT>
+__global__ void __launch_bounds__(256) k_peaks(PeakArgs a, OT* __restrict__ out) {
+    const int64_t n = a.nx * a.ny * a.nz;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t z = i / (a.nx * a.ny), r = i - z * a.nx * a.ny, y = r / a.nx, x = r - y * a.nx;
+        out[i] = (OT)peak_value(a, a.lox + x, a.loy + y, a.loz + z);
+    }
+}
+
 }  // namespace pmsz

@@ -1635,4 +1635,20 @@ pmsz_status pmsz_bits_to_ids(const uint32_t* bits, int64_t nbits, int64_t* ids, 
     return PMSZ_OK;
 }
 
+pmsz_status pmsz_gaussian_peaks(const int64_t gdims[3], const int64_t lo[3], const int64_t ext[3], uint64_t seed,
+                                int32_t out_f32, void* out, void* stream) {
+    if (!gdims || !lo || !ext || !out) return fail(PMSZ_ERR_INVALID, "null argument");
+    for (int a = 0; a < 3; ++a)
+        if (gdims[a] < 1 || ext[a] < 1 || lo[a] < 0 || lo[a] + ext[a] > gdims[a])
+            return fail(PMSZ_ERR_INVALID, "sub-box outside the global grid");
+    PeakArgs a{gdims[0], gdims[1], gdims[2], lo[0], lo[1], lo[2], ext[0], ext[1], ext[2], seed};
+    const int64_t n = ext[0] * ext[1] * ext[2];
+    cudaStream_t s = S(stream);
+    if (out_f32) k_peaks<float><<<grid_for(n, 256, 16), 256, 0, s>>>(a, (float*)out);
+    else k_peaks<double><<<grid_for(n, 256, 16), 256, 0, s>>>(a, (double*)out);
+    LAUNCHED();
+    CUDA_TRY(cudaGetLastError());
+    return PMSZ_OK;
+}
+
 }  // extern "C"

@@ -9,6 +9,9 @@
 * ``bounded_noise`` -- BASELINE config 1's seeded bounded-noise decompressed
   field (no reference counterpart; the oracle restates the same hash).
 * ``relative_to_absolute`` -- quantizer.py:99-113 from a device min/max.
+* ``gaussian_peaks`` -- BASELINE config 5's HEDM-like Gaussian-peak stack
+  (no reference counterpart; definition in csrc/gen.cuh, restated
+  bit for bit by the oracle's orc_peaks).
 """
 
 from __future__ import annotations
@@ -109,4 +112,25 @@ def bounded_noise_device(f: torch.Tensor, dims, xi: float, seed: int, *, gdims=N
     N.check(N.lib().pmsz_bounded_noise(N.ptr(f), int(f.dtype == torch.float32), nx, ny, nz,
                                        N.ivec(gd), N.ivec(lo), float(xi), int(seed) & (2**64 - 1),
                                        N.ptr(out), N.stream_handle()), "pmsz_bounded_noise")
+    return out
+
+
+@dataclass(frozen=True)
+class PeakSpec:
+    """HEDM-like Gaussian-peak stack: detector frames along z with sparse
+    spots in (64, 64, 32)-voxel cells over a faint background (gen.cuh)."""
+
+    dims: tuple[int, int, int]
+    seed: int
+
+
+def gaussian_peaks_device(spec: PeakSpec, *, lo=(0, 0, 0), ext=None, f32: bool = False,
+                          device=None) -> torch.Tensor:
+    """The sub-box [lo, lo+ext) of the peak stack (f64, or f32 if requested)."""
+    gd = tuple(int(v) for v in spec.dims)
+    e = tuple(int(v) for v in (ext if ext is not None else gd))
+    dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+    out = torch.empty(e[0] * e[1] * e[2], dtype=torch.float32 if f32 else torch.float64, device=dev)
+    N.check(N.lib().pmsz_gaussian_peaks(N.ivec(gd), N.ivec(lo), N.ivec(e), int(spec.seed) & (2**64 - 1), int(f32),
+                                        N.ptr(out), N.stream_handle()), "pmsz_gaussian_peaks")
     return out

@@ -246,6 +246,51 @@ def main():
         segs.append({"key": key, "dims": list(dims), "style": style, "report": rep.to_dict()})
     meta["segmentation"] = segs
 
+    # ---- extrema-only mode: the reference's own _iterate_array with
+    # its _kind_masks wrapped so the two order masks are always empty, iterated
+    # to a zero-edit pass.  Inputs: the (new) Gaussian-peak stack, stored, and
+    # a Perlin field; fhat from the reference quantizer.
+    import topocorrect.correction as tcc
+    orig_masks = tcc._kind_masks
+
+    def extrema_masks(f_scan, g_scan, center_mask=None):
+        m = orig_masks(f_scan, g_scan, center_mask)
+        z = np.zeros_like(m[0])
+        return (m[0], m[1], m[2], m[3], z, z)
+
+    ext = []
+    for name, dims, rel in [("peaks", (64, 64, 32), 1e-3), ("peaks_fine", (64, 64, 32), 1e-4),
+                            ("perlin", (20, 18, 16), 1e-2)]:
+        if name.startswith("peaks"):
+            f = tc.ScalarField(dims, orc.peaks(dims, 7))   # regenerated by the tests, pinned by f_sha256
+        else:
+            f = tc.perlin(tc.NoiseSpec(dims=dims, seed=11))
+        xi = tc.relative_to_absolute(f, rel)
+        _, fh = tc.quantize(f, xi)
+        cfg = tc.CorrectionConfig(xi_abs=xi)
+        f_scan = field_scan(f)
+        lower = BoundsField.from_field(f, xi).lower
+        g = fh.values.copy()
+        counts = np.zeros(g.size, np.int64)
+        hist = []
+        tcc._kind_masks = extrema_masks
+        try:
+            for _ in range(cfg.max_outer_iterations):
+                g, ed = _iterate_array(f.dims, f_scan, g, lower, cfg.tau)
+                counts += ed
+                hist.append(int(ed.sum()))
+                if not ed.any():
+                    break
+        finally:
+            tcc._kind_masks = orig_masks
+        rs, ts = field_scan(f), tc.scan_neighbors(g, f.dims)
+        ext.append({"name": name, "dims": list(dims), "rel": rel, "xi": xi, "tau": cfg.tau,
+                    "edits_per_iteration": hist, "max_vertex_edits": int(counts.max()),
+                    "corrected_sha256": sha(g), "fhat_sha256": sha(fh.values), "f_sha256": sha(f.values),
+                    "extrema_clean": bool(np.array_equal(rs.is_max, ts.is_max) and np.array_equal(rs.is_min, ts.is_min)),
+                    "order_violations_left": int(np.count_nonzero(~rs.is_max & (ts.nmax != rs.nmax)))})
+    meta["extrema_only"] = ext
+
     (OUT / "golden.json").write_text(json.dumps(meta, indent=1, sort_keys=True))
     np.savez_compressed(OUT / "golden.npz", **arrays)
     print("wrote", OUT / "golden.json", OUT / "golden.npz",

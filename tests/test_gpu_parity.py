@@ -356,3 +356,44 @@ def test_segmentation_and_plmss_match_oracle_at_scale(n):
     # the corrected field is clean against the original (correction.py:427-429)
     out = pm.run_correction_device(f32, fh, dims, pm.CorrectionConfig(xi_abs=xi))
     assert compare_plmss_device(f32, out.corrected, dims).is_clean
+
+
+# --- config 5: Gaussian-peak stack + extrema-only mode ----------------------------
+def test_gaussian_peaks_bit_exact():
+    spec = gen.PeakSpec((160, 130, 70), 3)
+    full = gen.gaussian_peaks_device(spec).cpu().numpy()
+    assert np.array_equal(full, orc.peaks(spec.dims, 3))
+    sub = gen.gaussian_peaks_device(spec, lo=(17, 64, 31), ext=(90, 40, 39), f32=True).cpu().numpy()
+    assert np.array_equal(sub, orc.peaks(spec.dims, 3, lo=(17, 64, 31), ext=(90, 40, 39)).astype(np.float32))
+
+
+@pytest.mark.parametrize("incremental", [True, False])
+def test_extrema_only_matches_reference(golden, incremental):
+    meta, _ = golden
+    for case in meta["extrema_only"]:
+        dims = tuple(case["dims"])
+        if case["name"].startswith("peaks"):
+            f = gen.gaussian_peaks_device(gen.PeakSpec(dims, 7))
+        else:
+            f = torch.from_numpy(orc.perlin(dims, 11)).to(DEV)
+        assert sha(f.cpu().numpy()) == case["f_sha256"]
+        fh = gen.quantize_device(f, case["xi"])
+        assert sha(fh.cpu().numpy()) == case["fhat_sha256"]
+        out = pm.run_correction_device(f, fh, dims, pm.CorrectionConfig(xi_abs=case["xi"]), extrema_only=True,
+                                       incremental=incremental)
+        assert list(out.edits_per_iteration) == case["edits_per_iteration"], case["name"]
+        assert out.max_vertex_edits == case["max_vertex_edits"]
+        assert sha(out.corrected.cpu().numpy()) == case["corrected_sha256"], case["name"]
+
+
+def test_extrema_only_peaks_at_scale_matches_oracle():
+    dims = (256, 256, 64)
+    f32 = gen.gaussian_peaks_device(gen.PeakSpec(dims, 1), f32=True)
+    xi = gen.relative_to_absolute_device(f32, 1e-4)
+    fh = gen.quantize_device(f32, xi)
+    out = pm.run_correction_device(f32, fh, dims, pm.CorrectionConfig(xi_abs=xi), extrema_only=True)
+    ref = orc.run_correction(dims, f32.double().cpu().numpy(), fh.cpu().numpy(), xi, extrema_only=True,
+                             check_segmentation=False)
+    assert ref.status == orc.ORC_OK
+    assert out.edits_per_iteration == ref.edits_per_iteration
+    assert np.array_equal(out.corrected.cpu().numpy(), ref.corrected)

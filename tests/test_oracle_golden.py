@@ -198,3 +198,30 @@ def test_field_and_label_codec_round_trips():
         codec.write_labels((2, 2, 1), np.array([0, 1, 2, 4]))
     with pytest.raises(codec.FormatError):
         codec.read_field(codec.write_field(f) + b"\x00")
+
+
+# --- extrema-only mode ------------------------------------------------
+def test_oracle_extrema_only_matches_reference_iteration(golden):
+    """orc_run_correction(extrema_only) == the reference's _iterate_array with
+    the order masks zeroed, iterated to a zero-edit pass."""
+    meta, _ = golden
+    for case in meta["extrema_only"]:
+        dims = tuple(case["dims"])
+        f = orc.peaks(dims, 7) if case["name"].startswith("peaks") else orc.perlin(dims, 11)
+        assert hashlib.sha256(f.tobytes()).hexdigest() == case["f_sha256"]
+        fh = orc.quantize(f, case["xi"])
+        assert hashlib.sha256(fh.tobytes()).hexdigest() == case["fhat_sha256"]
+        r = orc.run_correction(dims, f, fh, case["xi"], extrema_only=True, check_segmentation=False)
+        assert r.status == orc.ORC_OK, case["name"]
+        assert list(r.edits_per_iteration) == case["edits_per_iteration"], case["name"]
+        assert r.max_vertex_edits == case["max_vertex_edits"]
+        assert hashlib.sha256(r.corrected.tobytes()).hexdigest() == case["corrected_sha256"]
+        assert case["extrema_clean"] and case["order_violations_left"] > 0
+
+
+def test_peak_stack_properties():
+    v = orc.peaks((128, 128, 64), 3)
+    assert v.min() >= 0.0 and v.max() < 1.02
+    assert 0.0005 < (v > 0.05).mean() < 0.01          # sparse spots
+    sub = orc.peaks((128, 128, 64), 3, lo=(5, 70, 9), ext=(40, 30, 20))
+    assert np.array_equal(sub.reshape(20, 30, 40), v.reshape(64, 128, 128)[9:29, 70:100, 5:45])
