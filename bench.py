@@ -51,6 +51,9 @@ def parse():
     ap.add_argument("--cpu-sample-z", type=int, default=64, help="z-planes of the CPU baseline sample")
     ap.add_argument("--full-sweeps", action="store_true", help="disable incremental dirty-ring sweeps")
     ap.add_argument("--strategy", default="relaxed", choices=["relaxed", "lockstep"])
+    ap.add_argument("--workload", default="perlin", choices=["perlin", "strong", "hedm"],
+                    help="perlin: configs 2/3 (default); strong: config 4; hedm: config 5 (extrema-only)")
+    ap.add_argument("--decomp", default="slab", choices=["slab", "block"], help="strong scaling layout")
     return ap.parse_args()
 
 
@@ -114,29 +117,43 @@ def measured_peaks() -> dict:
 
 
 # ---------------------------------------------------------------------------
-def cpu_sample_inputs(size: int, zs: int, rel: float, seed: int):
-    """Bounded CPU sample of the workload: the first `zs` z-planes of the same
-    Perlin field (global coordinates), xi and the quantizer origin from the
-    whole field, so the sample equals the slice of the GPU inputs."""
+def _oracle_slab(kind: str, gdims, seed: int, z0: int, zs: int) -> np.ndarray:
+    """z-planes [z0, z0+zs) of the workload's f32 field, generated by the oracle."""
     from oracle import oracle as orc
-    gd = (size, size, size)
-    full = orc.perlin(gd, seed).astype(np.float32).astype(np.float64)
-    xi = orc.relative_to_absolute(full, rel)
-    origin = float(full.min())
-    f = np.ascontiguousarray(full[: size * size * zs])
-    del full
+    ext = (gdims[0], gdims[1], zs)
+    if kind == "hedm":
+        v = orc.peaks(gdims, seed, lo=(0, 0, z0), ext=ext)
+    else:
+        v = orc.perlin(gdims, seed, lo=(0, 0, z0), ext=ext)
+    return v.astype(np.float32).astype(np.float64)
+
+
+def cpu_sample_inputs(kind: str, gdims, zs: int, rel: float, seed: int, xi=None, origin=None):
+    """Bounded CPU sample of the workload: the first `zs` z-planes of the same
+    field (global coordinates).  xi and the quantizer origin belong to the
+    WHOLE field: passed in when the GPU already has them, else computed from
+    the oracle field slab by slab."""
+    from oracle import oracle as orc
+    if xi is None:
+        lo, hi = np.inf, -np.inf
+        for z0 in range(0, gdims[2], 32):
+            v = _oracle_slab(kind, gdims, seed, z0, min(32, gdims[2] - z0))
+            lo, hi = min(lo, float(v.min())), max(hi, float(v.max()))
+        xi = rel * (hi - lo) if hi > lo else rel * abs(hi)
+        origin = lo
+    f = _oracle_slab(kind, gdims, seed, 0, zs)
     fh = orc.quantize(f, xi, origin=origin)
-    return f, fh, xi, (size, size, zs)
+    return f, fh, xi, (gdims[0], gdims[1], zs)
 
 
-def time_cpu_oracle(f, fh, xi, dims, threads: int, reps: int = 1) -> tuple[float, dict]:
+def time_cpu_oracle(f, fh, xi, dims, threads: int, reps: int = 1, extrema_only: bool = False) -> tuple[float, dict]:
     from oracle import oracle as orc
     used = orc.set_threads(threads)
     times = []
     r = None
     for _ in range(reps):
         t0 = time.perf_counter()
-        r = orc.run_correction(dims, f, fh, xi, check_segmentation=True)
+        r = orc.run_correction(dims, f, fh, xi, check_segmentation=not extrema_only, extrema_only=extrema_only)
         times.append(time.perf_counter() - t0)
     n = dims[0] * dims[1] * dims[2]
     assert r.status == orc.ORC_OK, r
@@ -149,29 +166,33 @@ def run_reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    threads = os.cpu_count() or 1
-    f, fh, xi, dims = cpu_sample_inputs(args.size, args.cpu_sample_z, args.rel, args.seed)
+    from paper_2601_01787_b200.dist import workload
     from oracle import oracle as orc
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    wl = workload(args, max(world, 1))
+    threads = os.cpu_count() or 1
+    f, fh, xi, dims = cpu_sample_inputs(args.workload, wl["gdims"], args.cpu_sample_z, args.rel, args.seed)
     orc.set_threads(threads)
+    eo = wl["extrema_only"]
     n = dims[0] * dims[1] * dims[2]
     for _ in range(args.warmup):
-        orc.run_correction(dims, f, fh, xi, check_segmentation=True)
+        orc.run_correction(dims, f, fh, xi, check_segmentation=not eo, extrema_only=eo)
     t0 = time.perf_counter()
     iters = 0
     for _ in range(args.steps):
-        r = orc.run_correction(dims, f, fh, xi, check_segmentation=True)
+        r = orc.run_correction(dims, f, fh, xi, check_segmentation=not eo, extrema_only=eo)
         assert r.status == orc.ORC_OK
         iters = r.iterations
     dt = (time.perf_counter() - t0) / args.steps
     value = n / dt
-    sample = (f"{dims[0]}x{dims[1]}x{dims[2]} z-slab of the Perlin {args.size}^3 f32 field (seed {args.seed}), "
-              f"rel {args.rel}, quantizer; full run_correction incl. compare_plmss post-check; {iters} iterations")
-    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic (Perlin, seeded)",
+    sample = (f"{dims[0]}x{dims[1]}x{dims[2]} z-slab of the {wl['label']} field (seed {args.seed}, f32), "
+              f"rel {args.rel}, quantizer; full run_correction"
+              f"{' (extrema-only)' if eo else ' incl. compare_plmss post-check'}; {iters} iterations")
+    line = {"metric": wl["metric"] or METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": wl["scaling"],
+            "vs_baseline": None, "dtype": "f64", "data": f"synthetic ({wl['data']}, seeded)",
             "impl": "reference",
-            "config": {"workload": f"perlin{args.size}^3_f32_rel{args.rel:g}_quantizer", "sample": sample,
-                       "cpu_threads": threads},
+            "config": {"workload": wl["label"], "sample": sample, "cpu_threads": threads},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -186,24 +207,24 @@ def run_ours_single(args):
     from paper_2601_01787_b200 import inputs as gen
     from paper_2601_01787_b200.engine import DomainPlan, DomainSpec
 
+    from paper_2601_01787_b200.dist import workload
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
-    n1 = args.size
-    dims = (n1, n1, n1)
-    nvox = n1 ** 3
-    spec = gen.NoiseSpec(dims, args.seed)
-    f32 = gen.perlin_device(spec, f32=True)
+    wl = workload(args, 1)
+    dims = wl["gdims"]
+    nvox = dims[0] * dims[1] * dims[2]
+    f32 = wl["make"]((0, 0, 0), dims, dev)
     lo, hi = gen.minmax_device(f32)
     xi = gen.relative_to_absolute_range(lo, hi, args.rel)
     fh = gen.quantize_device(f32, xi, lo, hi)
     cfg = pm.CorrectionConfig(xi_abs=xi)
     plan = DomainPlan(DomainSpec.whole(dims), cfg.xi_abs, cfg.tau, cfg.max_outer_iterations,
-                      incremental=not args.full_sweeps, f32_original=True)
+                      incremental=not args.full_sweeps, f32_original=True, extrema_only=wl["extrema_only"])
     g = torch.empty_like(fh)
     stream = torch.cuda.current_stream()
 
     def step():
-        return pm.run_correction_device(f32, fh, dims, cfg, out=g, plan=plan)
+        return pm.run_correction_device(f32, fh, dims, cfg, out=g, plan=plan, extrema_only=wl["extrema_only"])
 
     for _ in range(max(args.warmup, 3)):
         res = step()
@@ -255,26 +276,28 @@ def run_ours_single(args):
              "full_sweeps": res.full_sweeps, "masked_sweeps": res.masked_sweeps,
              "sparse_sweeps": res.sparse_sweeps, "residual": 0}
 
-    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
-            "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic (Perlin seed 0 f32 + quantizer, on device)",
-            "config": {"workload": f"perlin{n1}^3_f32_rel{args.rel:g}_quantizer (BASELINE config 2)",
-                       "voxels": nvox, "xi_abs": xi, "tau": cfg.tau,
+    line = {"metric": wl["metric"] or METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True, "scaling": wl["scaling"],
+            "vs_baseline": None, "dtype": "f64",
+            "data": f"synthetic ({wl['data']} seed {args.seed} f32 + quantizer, generated on device)",
+            "config": {"workload": wl["label"], "dims": list(dims), "rel": args.rel,
+                       "voxels": nvox, "xi_abs": xi, "tau": cfg.tau, "extrema_only": wl["extrema_only"],
                        "mode": "full sweeps" if args.full_sweeps else "incremental dirty-ring sweeps",
-                       "l2": "inputs 1.5 GB > 126 MB L2 (no flush needed)", "parallelism": "single GPU"},
+                       "l2": f"inputs {nvox * 12 / 1e9:.1f} GB > 126 MB L2 (no flush needed)",
+                       "parallelism": "single GPU"},
             "roofline": roofline, "clocks": clk, "gpu_launches": launches, "result": check}
 
     if not args.no_e2e:
         line["e2e"] = e2e_host(args, plan, f32, fh, dims, nvox)
     if not args.no_cpu_baseline:
-        f, fhs, xic, sdims = cpu_sample_inputs(n1, args.cpu_sample_z, args.rel, args.seed)
-        assert xic == xi
+        f, fhs, xic, sdims = cpu_sample_inputs(args.workload, dims, args.cpu_sample_z, args.rel, args.seed,
+                                               xi=xi, origin=lo)
         threads = os.cpu_count() or 1
-        v, info = time_cpu_oracle(f, fhs, xic, sdims, threads)
+        v, info = time_cpu_oracle(f, fhs, xic, sdims, threads, extrema_only=wl["extrema_only"])
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": info["threads"], "kind": "port",
                                 "sample": f"{sdims[0]}x{sdims[1]}x{sdims[2]} z-slab of the same field, "
-                                          f"run_correction incl. compare_plmss, {info['iterations']} iterations, "
-                                          f"{info['seconds']:.1f} s"}
+                                          f"run_correction{' (extrema-only)' if wl['extrema_only'] else ' incl. compare_plmss'}, "
+                                          f"{info['iterations']} iterations, {info['seconds']:.1f} s"}
     print(json.dumps(line), flush=True)
     return 0
 

@@ -153,7 +153,8 @@ def run_local(engines, blocks, grid, lockstep: bool, cap: int) -> DistStats:
 class DeviceEngine:
     """One rank's block on its GPU: a libpmsz plan over the ext extent."""
 
-    def __init__(self, block: Block, gdims, f_ext: torch.Tensor, fhat_ext: torch.Tensor, config):
+    def __init__(self, block: Block, gdims, f_ext: torch.Tensor, fhat_ext: torch.Tensor, config,
+                 extrema_only: bool = False):
         from .engine import DomainPlan, raise_for
         from . import _native as N
         self.block = block
@@ -163,7 +164,8 @@ class DeviceEngine:
         self.fh = fhat_ext
         self.config = config
         self.plan = DomainPlan(self.spec, config.xi_abs, config.tau, config.max_outer_iterations,
-                               incremental=True, f32_original=f_ext.dtype == torch.float32)
+                               incremental=True, f32_original=f_ext.dtype == torch.float32,
+                               extrema_only=extrema_only)
         self.g = torch.empty_like(fhat_ext)
         self._N = N
         self._raise = raise_for
@@ -255,7 +257,49 @@ def _e2e_host(args, eng, blocks, grid, rank, lockstep, cap, dev, nvox_total) -> 
 
 
 # ---------------------------------------------------------------------------
-# bench.py --gpus N (torchrun): weak scaling, 512^3 per GPU, z-slabs
+# bench.py --gpus N (torchrun)
+def block_grid(world: int) -> tuple[int, int, int]:
+    """Near-cubic factorisation for the block decomposition (x fastest)."""
+    g = [1, 1, 1]
+    p, a = world, 0
+    while p > 1:
+        f = 2 if p % 2 == 0 else p
+        g[a % 3] *= f
+        p //= f
+        a += 1
+    return (g[0], g[1], g[2])
+
+
+def workload(args, world: int) -> dict:
+    """Global layout + generator of the bench workloads (BASELINE configs):
+    perlin  -- config 2/3: weak scaling, size^3 per GPU, z-slabs (1,1,P)
+    strong  -- config 4: 1024^3 Perlin fixed, slabs (1,1,P) or blocks (--decomp block)
+    hedm    -- config 5: 2048x2048x256 Gaussian-peak stack, extrema-only, y-slabs (1,P,1)"""
+    from . import inputs as gen
+    S = args.size
+    kind = getattr(args, "workload", "perlin")
+    if kind == "hedm":
+        gd = (2048, 2048, 256)
+        spec = gen.PeakSpec(gd, args.seed)
+        return {"gdims": gd, "grid": (1, world, 1), "decomp": "y-slabs", "scaling": "strong", "extrema_only": True,
+                "data": "HEDM-like Gaussian-peak stack", "label": "hedm 2048x2048x256 extrema-only (BASELINE config 5)",
+                "metric": "corrected voxels/sec (2048x2048x256 extrema-only)",
+                "make": lambda lo, ext, dev: gen.gaussian_peaks_device(spec, lo=lo, ext=ext, f32=True, device=dev)}
+    if kind == "strong":
+        gd = (1024, 1024, 1024)
+        block = getattr(args, "decomp", "slab") == "block"
+        grid = block_grid(world) if block else (1, 1, world)
+        spec = gen.NoiseSpec(gd, args.seed)
+        return {"gdims": gd, "grid": grid, "decomp": "blocks" if block else "z-slabs", "scaling": "strong",
+                "extrema_only": False, "data": "Perlin", "label": "perlin 1024^3 strong scaling (BASELINE config 4)",
+                "metric": "corrected voxels/sec (1024^3 strong scaling)",
+                "make": lambda lo, ext, dev: gen.perlin_device(spec, lo=lo, ext=ext, f32=True, device=dev)}
+    gd = (S, S, S * world)
+    spec = gen.NoiseSpec(gd, args.seed)
+    return {"gdims": gd, "grid": (1, 1, world), "decomp": "z-slabs", "scaling": "weak", "extrema_only": False,
+            "data": "Perlin", "label": f"perlin {S}^3 per GPU (BASELINE config 2/3)", "metric": None,
+            "make": lambda lo, ext, dev: gen.perlin_device(spec, lo=lo, ext=ext, f32=True, device=dev)}
+
 def bench_main(args, metric, unit, ClockSampler, measured_peaks, cpu_sample_inputs, time_cpu_oracle):
     import paper_2601_01787_b200 as pm
     from . import _native as N
@@ -268,14 +312,12 @@ def bench_main(args, metric, unit, ClockSampler, measured_peaks, cpu_sample_inpu
     dev = torch.device("cuda", local)
     if not dist.is_initialized():
         dist.init_process_group("nccl", device_id=dev)
-    S = args.size
-    gdims = (S, S, S * world)
-    grid = (1, 1, world)
+    wl = workload(args, world)
+    gdims, grid = wl["gdims"], wl["grid"]
     blocks = decompose(gdims, grid).blocks
     blk = blocks[rank]
     ext = blk.ext_dims
-    spec = gen.NoiseSpec(gdims, args.seed)
-    f32 = gen.perlin_device(spec, lo=blk.ext_start, ext=ext, f32=True, device=dev)
+    f32 = wl["make"](blk.ext_start, ext, dev)
     lo, hi = gen.minmax_device(f32)
     mm = torch.tensor([-lo, hi], dtype=torch.float64, device=dev)
     dist.all_reduce(mm, op=dist.ReduceOp.MAX)
@@ -283,7 +325,7 @@ def bench_main(args, metric, unit, ClockSampler, measured_peaks, cpu_sample_inpu
     xi = gen.relative_to_absolute_range(glo, ghi, args.rel)
     fh = gen.quantize_device(f32, xi, glo, ghi)
     cfg = pm.CorrectionConfig(xi_abs=xi)
-    eng = DeviceEngine(blk, gdims, f32, fh, cfg)
+    eng = DeviceEngine(blk, gdims, f32, fh, cfg, extrema_only=wl["extrema_only"])
     lockstep = args.strategy == "lockstep"
     cap = cfg.max_outer_iterations
 
@@ -318,18 +360,21 @@ def bench_main(args, metric, unit, ClockSampler, measured_peaks, cpu_sample_inpu
     ms = float(t.item())
     residual = torch.tensor([eng.residual()], dtype=torch.int64, device=dev)
     dist.all_reduce(residual)
-    e2e = None if args.no_e2e else _e2e_host(args, eng, blocks, grid, rank, lockstep, cap, dev, S ** 3 * world)
+    e2e = None if args.no_e2e else _e2e_host(args, eng, blocks, grid, rank, lockstep, cap, dev,
+                                              gdims[0] * gdims[1] * gdims[2])
     per_rank = [None] * world
     dist.all_gather_object(per_rank, {"rank": rank, "iterations": st.iterations, "edits": st.edit_total,
                                       "max_vertex_edits": st.max_vertex_edits, "ms": ms_local,
                                       "sent_bytes_per_step": st.exchanged_bytes, "clocks": clk})
-    nvox = S * S * S * world
+    nvox = gdims[0] * gdims[1] * gdims[2]
     if rank == 0:
         peaks = measured_peaks()
         peak = float(peaks.get("hbm_gbs", 6650.0))
         kernels = {}
         per_voxel = {"sweep_full": 9, "sweep_masked": 9, "prep": 4 + 8 + 8 + 1}
-        core = S ** 3
+        core = 1
+        for a in range(3):
+            core *= blk.core_stop[a] - blk.core_start[a]
         for name, (kms, cnt) in prof.items():
             if cnt == 0:
                 continue
@@ -340,11 +385,13 @@ def bench_main(args, metric, unit, ClockSampler, measured_peaks, cpu_sample_inpu
                 entry.update({"achieved_gbs": gbs, "frac": gbs / peak})
             kernels[name] = entry
         dk = kernels.get("sweep_full", {})
-        line = {"metric": metric, "value": nvox / (ms / 1e3), "unit": unit, "n_gpus": world, "steps": args.steps,
-                "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-                "vs_baseline": None, "dtype": "f64", "data": "synthetic (Perlin seed 0 f32 + quantizer, on device)",
-                "config": {"workload": f"perlin {S}^3 per GPU, global {gdims}, rel {args.rel:g}, quantizer",
-                           "decomposition": f"z-slabs {grid}", "strategy": st.strategy,
+        line = {"metric": wl["metric"] or metric, "value": nvox / (ms / 1e3), "unit": unit, "n_gpus": world,
+                "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True,
+                "scaling": wl["scaling"], "vs_baseline": None, "dtype": "f64",
+                "data": f"synthetic ({wl['data']}, f32, seed {args.seed}; quantizer; generated on device)",
+                "config": {"workload": wl["label"], "global_dims": list(gdims), "rel": args.rel,
+                           "extrema_only": wl["extrema_only"],
+                           "decomposition": f"{wl['decomp']} {grid}", "strategy": st.strategy,
                            "parallelism": f"block-parallel x{world} (NCCL ghost exchange)",
                            "xi_abs": xi, "l2": "inputs > L2"},
                 "roofline": {"bound": "hbm", "kernel": "sweep_full (rank 0)", "achieved": dk.get("achieved_gbs"),
