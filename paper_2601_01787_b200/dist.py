@@ -75,8 +75,19 @@ class DistStats:
     exchanged_bytes: int       # bytes this rank sent
 
 
+TRACE = {}   # PMSZ_DIST_TRACE=1: host seconds per phase of run_distributed (synchronised)
+
+
+def _tick(name, t0):
+    torch.cuda.synchronize()
+    t1 = time.perf_counter()
+    TRACE[name] = TRACE.get(name, 0.0) + (t1 - t0)
+    return t1
+
+
 def run_distributed(engine, blocks, grid, rank: int, lockstep: bool, cap: int, group=None) -> DistStats:
     """The round loop of run_parallel (parallel.py:289-322) across ranks."""
+    trace = os.environ.get("PMSZ_DIST_TRACE") == "1"
     xs = exchanges(blocks, rank)
     dev = engine.device
     rounds = syncs = 0
@@ -86,10 +97,15 @@ def run_distributed(engine, blocks, grid, rank: int, lockstep: bool, cap: int, g
         if rounds >= cap:
             raise ConvergenceError(f"no terminal round within {cap}")
         rounds += 1
+        t0 = time.perf_counter() if trace else 0.0
         e, dirty = engine.round(lockstep)
+        if trace:
+            t0 = _tick(f"round{rounds}", t0)
         t = torch.tensor([e, int(dirty)], dtype=torch.int64, device=dev)
         dist.all_reduce(t, group=group)
         round_edits, any_dirty = (int(v) for v in t.tolist())
+        if trace:
+            t0 = _tick("allreduce", t0)
         totals.append(round_edits)
         if not lockstep and (round_edits == 0 or any_dirty == 0):
             break
@@ -104,9 +120,13 @@ def run_distributed(engine, blocks, grid, rank: int, lockstep: bool, cap: int, g
         if ops:
             for req in dist.batch_isend_irecv(ops):
                 req.wait()
+        if trace:
+            t0 = _tick("exchange", t0)
         changed = 0
         for x in xs:
             changed += engine.merge(x, recv[x.peer])
+        if trace:
+            t0 = _tick("merge", t0)
         syncs += 1
         if lockstep:
             c = torch.tensor([changed], dtype=torch.int64, device=dev)
@@ -336,6 +356,7 @@ def bench_main(args, metric, unit, ClockSampler, measured_peaks, cpu_sample_inpu
     for _ in range(max(args.warmup, 3)):
         st = step()
     torch.cuda.synchronize()
+    TRACE.clear()
     eng.plan.profile(True)
     eng.plan.profile_read(reset=True)
     launches0 = N.launch_count()
@@ -398,6 +419,7 @@ def bench_main(args, metric, unit, ClockSampler, measured_peaks, cpu_sample_inpu
                              "peak": peak, "unit": "GB/s", "frac": dk.get("frac"), "traffic": None,
                              "per_kernel": kernels},
                 "clocks": clk, "gpu_launches": launches,
+                "trace_ms_per_step": {k: 1e3 * v / args.steps for k, v in TRACE.items()} if TRACE else None,
                 "result": {"rounds": st.rounds, "syncs": st.syncs, "edits_per_round": list(st.edits_per_round),
                            "residual": int(residual.item()), "per_rank": per_rank}}
         if e2e is not None:
