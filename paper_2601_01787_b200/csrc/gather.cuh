@@ -57,13 +57,38 @@ __global__ void __launch_bounds__(kGWarps * 32, 2) k_gather(Dom d, const double*
             reinterpret_cast<uint32_t*>(B + 15 * 32 + lane)[1] = 0xffffffffu;
             return;
         }
+        const double* p0 = g + c;
+        if (x > 0 && x + 1 < d.nx && y > 0 && y + 1 < d.ny && z > 0 && z + 1 < d.nz) {
+            // interior: the 14 sources are 3 rows of plane z-1/z/z+1 around p0
+            const double* dn = p0 - d.sz;
+            const double* up = p0 + d.sz;
+            const double* dnm = dn - d.sy;
+            const double* ctm = p0 - d.sy;
+            const double* ctp = p0 + d.sy;
+            const double* upp = up + d.sy;
+            cp_async8(B + 0 * 32 + lane, dnm - 1);   // (-1,-1,-1)
+            cp_async8(B + 1 * 32 + lane, dnm);       // ( 0,-1,-1)
+            cp_async8(B + 2 * 32 + lane, dn - 1);    // (-1, 0,-1)
+            cp_async8(B + 3 * 32 + lane, dn);        // ( 0, 0,-1)
+            cp_async8(B + 4 * 32 + lane, ctm - 1);   // (-1,-1, 0)
+            cp_async8(B + 5 * 32 + lane, ctm);       // ( 0,-1, 0)
+            cp_async8(B + 6 * 32 + lane, p0 - 1);    // (-1, 0, 0)
+            cp_async8(B + 7 * 32 + lane, p0 + 1);    // ( 1, 0, 0)
+            cp_async8(B + 8 * 32 + lane, ctp);       // ( 0, 1, 0)
+            cp_async8(B + 9 * 32 + lane, ctp + 1);   // ( 1, 1, 0)
+            cp_async8(B + 10 * 32 + lane, up);       // ( 0, 0, 1)
+            cp_async8(B + 11 * 32 + lane, up + 1);   // ( 1, 0, 1)
+            cp_async8(B + 12 * 32 + lane, upp);      // ( 0, 1, 1)
+            cp_async8(B + 13 * 32 + lane, upp + 1);  // ( 1, 1, 1)
+        } else {
 #pragma unroll
-        for (int r = 0; r < 14; ++r) {
-            const bool ok = in_dom(d, x + rank_dx(r), y + rank_dy(r), z + rank_dz(r));
-            if (ok) cp_async8(B + r * 32 + lane, g + c + rank_off(d, r));
-            else B[r * 32 + lane] = nanv;
+            for (int r = 0; r < 14; ++r) {
+                const bool ok = in_dom(d, x + rank_dx(r), y + rank_dy(r), z + rank_dz(r));
+                if (ok) cp_async8(B + r * 32 + lane, p0 + rank_off(d, r));
+                else B[r * 32 + lane] = nanv;
+            }
         }
-        cp_async8(B + 14 * 32 + lane, g + c);
+        cp_async8(B + 14 * 32 + lane, p0);
         uint32_t* cw = reinterpret_cast<uint32_t*>(B + 15 * 32 + lane);
         cp_async4(cw, reinterpret_cast<const uint32_t*>(w.code + (c & ~3ll)));
         cw[1] = (uint32_t)c;

@@ -427,6 +427,7 @@ struct pmsz_plan {
     int64_t sort_min = 65536;             // dirty lists above this are sorted (compacted from actbits)
     int64_t dense_min = 0;                // dirty lists above this take the pipelined gather (kMaskedList)
     bool bits_only = false;               // the pending dirty set is in actbits only (no list)
+    int64_t full_div = 8;                 // a full sweep follows when 15 x edits > ncore / full_div
     bool gather_on = true;                // masked iterations as sorted gathers (gather.cuh)
     // host-buffer entry point staging (pmsz_run_correction_host)
     void* stage_f = nullptr;
@@ -558,7 +559,7 @@ pmsz_status launch_apply(pmsz_plan* p, const void* f, double* g, cudaStream_t s,
 pmsz_status choose_next(pmsz_plan* p, cudaStream_t s, bool marked_bits, int64_t nedits, int nxt, int64_t nact,
                         bool appended, int64_t bound) {
     if (marked_bits) {
-        if (15 * nedits > p->ncore / 8) {
+        if (15 * nedits > p->ncore / p->full_div) {
             p->next_mode = kFull;
             CUDA_TRY(cudaMemsetAsync(p->w.iteredit, 0, p->nwords * 4, s));
         } else {
@@ -959,6 +960,7 @@ pmsz_status pmsz_plan_create(const pmsz_desc* desc, pmsz_plan** out) {
     p->dense_min = std::max<int64_t>(ncore / 96, 65536);
     if (const char* e = getenv("PMSZ_SORT_MIN")) p->sort_min = atoll(e);
     if (const char* e = getenv("PMSZ_DENSE_MIN")) p->dense_min = atoll(e);
+    if (const char* e = getenv("PMSZ_FULL_DIV")) p->full_div = std::max<int64_t>(1, atoll(e));
     if (const char* e = getenv("PMSZ_SWEEP")) p->gather_on = strcmp(e, "tiled") != 0;
     if (cudaFuncSetAttribute(k_gather<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGatherSmem) !=
             cudaSuccess ||
