@@ -428,6 +428,8 @@ struct pmsz_plan {
     int64_t dense_min = 0;                // dirty lists above this take the pipelined gather (kMaskedList)
     bool bits_only = false;               // the pending dirty set is in actbits only (no list)
     int64_t full_div = 8;                 // a full sweep follows when 15 x edits > ncore / full_div
+    const uint32_t* offsets_of = nullptr; // bitmap whose block offsets block_counts holds
+    int64_t edits_cached = -1;            // popcount(editbits) since the last iteration, -1 = unknown
     bool gather_on = true;                // masked iterations as sorted gathers (gather.cuh)
     // host-buffer entry point staging (pmsz_run_correction_host)
     void* stage_f = nullptr;
@@ -508,6 +510,7 @@ pmsz_status reset_iter(pmsz_plan* p, cudaStream_t s, int nxt) {
 // Set bits of a bitmap: per-block counts + one-block exclusive scan; the total
 // lands in *dst on the device.
 void launch_bits_total(pmsz_plan* p, const uint32_t* bits, unsigned long long* dst, cudaStream_t s) {
+    p->offsets_of = bits;
     k_bits_count<<<(unsigned)p->nblocks_compact, kCompactThreads, 0, s>>>(bits, p->nwords, p->block_counts);
     LAUNCHED();
     k_exclusive_scan<<<1, 1024, 0, s>>>(p->block_counts, p->nblocks_compact, dst);
@@ -592,6 +595,7 @@ pmsz_status choose_next(pmsz_plan* p, cudaStream_t s, bool marked_bits, int64_t 
 //   kList       -- gather sweep over the explicit dirty-centre list (short)
 pmsz_status iterate_once(pmsz_plan* p, const void* f, double* g, cudaStream_t s) {
     const int nxt = p->cur ^ 1;
+    p->edits_cached = -1;
     pmsz_status st = reset_iter(p, s, nxt);
     if (st) return st;
     const Dom& d = p->dom;
@@ -696,7 +700,8 @@ pmsz_status launch_tail(pmsz_plan* p, const void* f, double* g, cudaStream_t s, 
         int per = 0;
         CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_tail<FT>, 256, 0));
         if (per < 1) return fail(PMSZ_ERR_CUDA, "k_tail cannot be resident");
-        nb = std::min(per, 4) * num_sms();
+        static const int cap = getenv("PMSZ_TAIL_PER_SM") ? std::max(1, atoi(getenv("PMSZ_TAIL_PER_SM"))) : 1;
+        nb = std::min(per, cap) * num_sms();
     }
     unsigned long long sort_min = (unsigned long long)p->sort_min;
     Dom d = p->dom;
@@ -741,6 +746,7 @@ pmsz_status launch_tail(pmsz_plan* p, const void* f, double* g, cudaStream_t s, 
 // counts land in p->hthist[0 .. *k).
 pmsz_status tail_step(pmsz_plan* p, const void* f, double* g, cudaStream_t s, long long budget, int64_t* k,
                       bool* shared_any) {
+    p->edits_cached = -1;
     pmsz_status st = reset_iter(p, s, p->cur ^ 1);
     if (st) return st;
     const int sorted = sort_pending(p, s);
@@ -781,6 +787,7 @@ void tail_result(pmsz_plan* p, pmsz_result* r, int64_t k) {
 }
 
 pmsz_status reset_run_state(pmsz_plan* p, cudaStream_t s) {
+    p->edits_cached = -1;
     CUDA_TRY(cudaMemsetAsync(p->ctr, 0, sizeof(DevCounters), s));
     CUDA_TRY(cudaMemsetAsync(&p->ctr->bound_first, 0xff, sizeof(unsigned long long), s));
     CUDA_TRY(cudaMemsetAsync(p->w.editbits, 0, p->nwords * 4, s));
@@ -870,6 +877,10 @@ pmsz_status bits_total(pmsz_plan* p, const uint32_t* bits, cudaStream_t s, int64
 }
 
 pmsz_status edit_count(pmsz_plan* p, cudaStream_t s, int64_t* count) {
+    if (p->edits_cached >= 0 && p->offsets_of == p->w.editbits) {   // offsets still in block_counts
+        *count = p->edits_cached;
+        return PMSZ_OK;
+    }
     {
         ProfScope ps(p, s, PMSZ_K_COMPACT);
         launch_bits_total(p, p->w.editbits, &p->ctr->scratch[2], s);
@@ -878,6 +889,24 @@ pmsz_status edit_count(pmsz_plan* p, cudaStream_t s, int64_t* count) {
     pmsz_status st = sync_counters(p, s);
     if (st) return st;
     *count = (int64_t)p->hctr->scratch[2];
+    p->edits_cached = *count;
+    return PMSZ_OK;
+}
+
+// Residual detections and the edit count with one synchronisation; the edit
+// bitmap's block offsets stay in block_counts for the export.
+pmsz_status residual_and_edits(pmsz_plan* p, cudaStream_t s, int64_t* residual, int64_t* edits) {
+    {
+        ProfScope ps(p, s, PMSZ_K_COMPACT);
+        launch_bits_total(p, p->w.detbits, &p->ctr->scratch[1], s);
+        launch_bits_total(p, p->w.editbits, &p->ctr->scratch[2], s);
+    }
+    CUDA_TRY(cudaGetLastError());
+    pmsz_status st = sync_counters(p, s);
+    if (st) return st;
+    *residual = (int64_t)p->hctr->scratch[1];
+    *edits = (int64_t)p->hctr->scratch[2];
+    p->edits_cached = *edits;
     return PMSZ_OK;
 }
 
@@ -1249,20 +1278,15 @@ pmsz_status pmsz_run_correction(pmsz_plan* p, const void* f, const double* fh, d
     // changes (or by a full sweep), so the popcount equals the detections of
     // a full re-scan of the final field.  The per-kind split is only computed
     // when something survived.
-    int64_t residual = 0;
-    st = bits_total(p, p->w.detbits, s, &residual);
+    int64_t residual = 0, count = 0;
+    st = residual_and_edits(p, s, &residual, &count);
     if (st) return st;
     if (residual) {
         st = pmsz_verify(p, g, r, stream);
         if (st) return st;
-    }
-    if (residual) {
         r->convergence_kind = PMSZ_CONV_RESIDUAL;
         return fail(PMSZ_ERR_CONVERGENCE, "distortions survived a zero-edit iteration");
     }
-    int64_t count = 0;
-    st = edit_count(p, s, &count);
-    if (st) return st;
     r->edit_count = count;
     return PMSZ_OK;
 }
