@@ -105,154 +105,153 @@ __global__ void __launch_bounds__(256) k_bounds(int64_t n, const FT* __restrict_
     if ((threadIdx.x & 31) == 0 && mine) atomicAdd(count, mine);
 }
 
-// ---- edit-set compaction from the ever-edited bitmap -----------------------
+// ---- bitmap compaction (ascending id lists) ----------------------------------
+// The bitmap is cut into at most kMaxChunks contiguous chunks of whole warps'
+// words (one chunk per CTA).  k_chunk_count sums each chunk; k_chunk_scan
+// (one CTA) turns the sums into exclusive offsets in place and writes the
+// total; the list/write kernels then compact each chunk in rounds of 256
+// words with a block-wide scan, so ids come out ascending.
 constexpr int kCompactThreads = 256;
-constexpr int kWordsPerThread = 8;
-constexpr int kWordsPerBlock = kCompactThreads * kWordsPerThread;
+constexpr int kMaxChunks = 1024;
 
-__global__ void __launch_bounds__(kCompactThreads) k_bits_count(const uint32_t* __restrict__ bits, int64_t nwords,
-                                                                unsigned long long* block_counts) {
-    __shared__ unsigned long long warp_sums[kCompactThreads / 32];
-    const int64_t base = (int64_t)blockIdx.x * kWordsPerBlock;
-    unsigned c = 0;
-    for (int k = 0; k < kWordsPerThread; ++k) {
-        const int64_t wdx = base + (int64_t)k * kCompactThreads + threadIdx.x;
-        if (wdx < nwords) c += __popc(bits[wdx]);
-    }
-    c = __reduce_add_sync(0xffffffffu, c);
-    if ((threadIdx.x & 31) == 0) warp_sums[threadIdx.x >> 5] = c;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned long long t = 0;
-        for (int i = 0; i < kCompactThreads / 32; ++i) t += warp_sums[i];
-        block_counts[blockIdx.x] = t;
-    }
+struct Chunks {
+    int64_t nwords, chunk;   // words per chunk (multiple of kCompactThreads)
+    int n;                   // number of chunks
+};
+
+inline Chunks make_chunks(int64_t nwords, int sms) {
+    Chunks c;
+    c.nwords = nwords;
+    int64_t want = std::min<int64_t>(kMaxChunks, std::max<int64_t>(1, (int64_t)sms * 6));
+    int64_t per = (nwords + want - 1) / want;
+    per = std::max<int64_t>(kCompactThreads, (per + kCompactThreads - 1) / kCompactThreads * kCompactThreads);
+    c.chunk = per;
+    c.n = (int)std::max<int64_t>(1, (nwords + per - 1) / per);
+    return c;
 }
 
-__global__ void __launch_bounds__(1024) k_exclusive_scan(unsigned long long* v, int64_t n,
-                                                         unsigned long long* total) {
-    __shared__ unsigned long long carry;
-    __shared__ unsigned long long warp_tot[32];
-    if (threadIdx.x == 0) carry = 0;
-    __syncthreads();
-    for (int64_t base = 0; base < n; base += blockDim.x) {
-        const int64_t i = base + threadIdx.x;
-        const unsigned long long x = i < n ? v[i] : 0ull;
-        // inclusive warp scan
-        unsigned long long s = x;
-        for (int o = 1; o < 32; o <<= 1) {
-            const unsigned long long y = __shfl_up_sync(0xffffffffu, s, o);
-            if ((threadIdx.x & 31) >= o) s += y;
-        }
-        if ((threadIdx.x & 31) == 31) warp_tot[threadIdx.x >> 5] = s;
-        __syncthreads();
-        if (threadIdx.x < 32) {
-            unsigned long long t = threadIdx.x < (blockDim.x >> 5) ? warp_tot[threadIdx.x] : 0ull;
-            for (int o = 1; o < 32; o <<= 1) {
-                const unsigned long long y = __shfl_up_sync(0xffffffffu, t, o);
-                if (threadIdx.x >= o) t += y;
-            }
-            warp_tot[threadIdx.x] = t;   // inclusive over warps
-        }
-        __syncthreads();
-        const unsigned long long warp_off = (threadIdx.x >> 5) ? warp_tot[(threadIdx.x >> 5) - 1] : 0ull;
-        if (i < n) v[i] = carry + warp_off + s - x;
-        __syncthreads();
-        if (threadIdx.x == blockDim.x - 1) carry += warp_off + s;
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) *total = carry;
-}
-
-__global__ void __launch_bounds__(kCompactThreads) k_bits_write(const uint32_t* __restrict__ bits, int64_t nwords,
-                                                                int64_t n, const unsigned long long* block_offs,
-                                                                const double* __restrict__ g, int64_t* ids,
-                                                                double* vals, int64_t cap) {
-    __shared__ unsigned warp_sums[kCompactThreads / 32];
-    const int64_t base = (int64_t)blockIdx.x * kWordsPerBlock;
-    // Each thread owns kWordsPerThread CONSECUTIVE words so ids stay ascending.
-    const int64_t w0 = base + (int64_t)threadIdx.x * kWordsPerThread;
-    uint32_t wv[kWordsPerThread];
-    unsigned c = 0;
-    for (int k = 0; k < kWordsPerThread; ++k) {
-        wv[k] = (w0 + k < nwords) ? bits[w0 + k] : 0u;
-        c += __popc(wv[k]);
-    }
-    // exclusive scan of c across the block
-    unsigned s = c;
+__device__ __forceinline__ unsigned block_exclusive_scan(unsigned v, unsigned* warp_tot, unsigned& total) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    unsigned s = v;
+#pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         const unsigned y = __shfl_up_sync(0xffffffffu, s, o);
-        if ((threadIdx.x & 31) >= o) s += y;
+        if (lane >= o) s += y;
     }
-    if ((threadIdx.x & 31) == 31) warp_sums[threadIdx.x >> 5] = s;
+    if (lane == 31) warp_tot[wid] = s;
     __syncthreads();
-    if (threadIdx.x < 32) {
-        unsigned t = threadIdx.x < kCompactThreads / 32 ? warp_sums[threadIdx.x] : 0u;
-        for (int o = 1; o < 32; o <<= 1) {
-            const unsigned y = __shfl_up_sync(0xffffffffu, t, o);
-            if (threadIdx.x >= o) t += y;
+    unsigned before = 0;
+    total = 0;
+#pragma unroll
+    for (int q = 0; q < kCompactThreads / 32; ++q) {
+        const unsigned t = warp_tot[q];
+        before += q < wid ? t : 0u;
+        total += t;
+    }
+    __syncthreads();   // warp_tot is reused by the next round
+    return before + s - v;
+}
+
+__global__ void __launch_bounds__(kCompactThreads) k_chunk_count(const uint32_t* __restrict__ bits, Chunks c,
+                                                                 unsigned long long* counts) {
+    __shared__ unsigned long long ws[kCompactThreads / 32];
+    const int64_t w0 = (int64_t)blockIdx.x * c.chunk, w1 = min(w0 + c.chunk, c.nwords);
+    unsigned long long t = 0;
+    for (int64_t w = w0 + threadIdx.x; w < w1; w += kCompactThreads) t += __popc(__ldg(bits + w));
+    t = __reduce_add_sync(0xffffffffu, (unsigned)t);
+    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = t;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long s = 0;
+        for (int q = 0; q < kCompactThreads / 32; ++q) s += ws[q];
+        counts[blockIdx.x] = s;
+    }
+}
+
+// counts[0..n) -> exclusive offsets in place; the total -> *total (n <= 1024).
+__global__ void __launch_bounds__(kMaxChunks) k_chunk_scan(unsigned long long* counts, int n,
+                                                           unsigned long long* total) {
+    __shared__ unsigned long long wt[32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const unsigned long long v = threadIdx.x < n ? counts[threadIdx.x] : 0ull;
+    unsigned long long s = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(0xffffffffu, s, o);
+        if (lane >= o) s += y;
+    }
+    if (lane == 31) wt[wid] = s;
+    __syncthreads();
+    unsigned long long before = 0, all = 0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) {
+        before += q < wid ? wt[q] : 0ull;
+        all += wt[q];
+    }
+    if (threadIdx.x < n) counts[threadIdx.x] = before + s - v;
+    if (threadIdx.x == 0 && total) *total = all;
+}
+
+// Chunk of the bitmap -> ascending ids (bits cleared on the way when `clear`).
+template <typename IdT>
+__global__ void __launch_bounds__(kCompactThreads) k_chunk_list(uint32_t* __restrict__ bits, Chunks c,
+                                                                const unsigned long long* __restrict__ offs,
+                                                                IdT* __restrict__ list, int clear) {
+    __shared__ unsigned wt[kCompactThreads / 32];
+    const int64_t w0 = (int64_t)blockIdx.x * c.chunk, w1 = min(w0 + c.chunk, c.nwords);
+    unsigned long long pos0 = offs[blockIdx.x];
+    constexpr int kG = 4;   // rounds whose words are loaded together (latency)
+    for (int64_t base = w0; base < w1; base += kG * kCompactThreads) {
+        uint32_t mg[kG];
+#pragma unroll
+        for (int q = 0; q < kG; ++q) {
+            const int64_t w = base + q * kCompactThreads + threadIdx.x;
+            mg[q] = w < w1 ? bits[w] : 0u;
         }
-        if (threadIdx.x < kCompactThreads / 32) warp_sums[threadIdx.x] = t;
+#pragma unroll
+        for (int q = 0; q < kG; ++q) {
+            const int64_t w = base + q * kCompactThreads + threadIdx.x;
+            uint32_t m = mg[q];
+            if (clear && m) bits[w] = 0u;
+            unsigned total;
+            const unsigned before = block_exclusive_scan(__popc(m), wt, total);
+            unsigned long long pos = pos0 + before;
+            while (m) {
+                const int b = __ffs(m) - 1;
+                m &= m - 1;
+                list[pos++] = (IdT)(w * 32 + b);
+            }
+            pos0 += total;
+        }
     }
-    __syncthreads();
-    const unsigned warp_off = (threadIdx.x >> 5) ? warp_sums[(threadIdx.x >> 5) - 1] : 0u;
-    int64_t pos = (int64_t)block_offs[blockIdx.x] + warp_off + s - c;
-    for (int k = 0; k < kWordsPerThread; ++k) {
-        uint32_t m = wv[k];
+}
+
+// Export of the edit record: ids and the corrected values (EditSet.diff).
+__global__ void __launch_bounds__(kCompactThreads) k_chunk_write(const uint32_t* __restrict__ bits, Chunks c,
+                                                                 int64_t n, const unsigned long long* __restrict__ offs,
+                                                                 const double* __restrict__ g, int64_t* ids,
+                                                                 double* vals, int64_t cap) {
+    __shared__ unsigned wt[kCompactThreads / 32];
+    const int64_t w0 = (int64_t)blockIdx.x * c.chunk, w1 = min(w0 + c.chunk, c.nwords);
+    unsigned long long pos0 = offs[blockIdx.x];
+    uint32_t nxt = w0 + threadIdx.x < w1 ? __ldg(bits + w0 + threadIdx.x) : 0u;
+    for (int64_t base = w0; base < w1; base += kCompactThreads) {
+        const int64_t w = base + threadIdx.x;
+        uint32_t m = nxt;
+        nxt = w + kCompactThreads < w1 ? __ldg(bits + w + kCompactThreads) : 0u;
+        unsigned total;
+        const unsigned before = block_exclusive_scan(__popc(m), wt, total);
+        long long pos = (long long)(pos0 + before);
         while (m) {
             const int b = __ffs(m) - 1;
             m &= m - 1;
-            const int64_t id = (w0 + k) * 32 + b;
+            const int64_t id = w * 32 + b;
             if (id < n && pos < cap) {
                 ids[pos] = id;
                 vals[pos] = g[id];
             }
             ++pos;
         }
-    }
-}
-
-// Bitmap -> ascending u32 id list (the touched targets after a full sweep);
-// the words are cleared on the way (the touched bitmap is all-zero between
-// iterations).
-template <typename IdT>
-__global__ void __launch_bounds__(kCompactThreads) k_bits_list(uint32_t* __restrict__ bits, int64_t nwords,
-                                                               const unsigned long long* block_offs, IdT* list,
-                                                               int clear) {
-    __shared__ unsigned warp_sums[kCompactThreads / 32];
-    const int64_t w0 = (int64_t)blockIdx.x * kWordsPerBlock + (int64_t)threadIdx.x * kWordsPerThread;
-    uint32_t wv[kWordsPerThread];
-    unsigned c = 0;
-    for (int k = 0; k < kWordsPerThread; ++k) {
-        wv[k] = (w0 + k < nwords) ? bits[w0 + k] : 0u;
-        c += __popc(wv[k]);
-        if (clear && wv[k]) bits[w0 + k] = 0u;
-    }
-    unsigned s = c;
-    for (int o = 1; o < 32; o <<= 1) {
-        const unsigned y = __shfl_up_sync(0xffffffffu, s, o);
-        if ((threadIdx.x & 31) >= o) s += y;
-    }
-    if ((threadIdx.x & 31) == 31) warp_sums[threadIdx.x >> 5] = s;
-    __syncthreads();
-    if (threadIdx.x < 32) {
-        unsigned t = threadIdx.x < kCompactThreads / 32 ? warp_sums[threadIdx.x] : 0u;
-        for (int o = 1; o < 32; o <<= 1) {
-            const unsigned y = __shfl_up_sync(0xffffffffu, t, o);
-            if (threadIdx.x >= o) t += y;
-        }
-        if (threadIdx.x < kCompactThreads / 32) warp_sums[threadIdx.x] = t;
-    }
-    __syncthreads();
-    const unsigned warp_off = (threadIdx.x >> 5) ? warp_sums[(threadIdx.x >> 5) - 1] : 0u;
-    unsigned long long pos = block_offs[blockIdx.x] + warp_off + s - c;
-    for (int k = 0; k < kWordsPerThread; ++k) {
-        uint32_t m = wv[k];
-        while (m) {
-            const int b = __ffs(m) - 1;
-            m &= m - 1;
-            list[pos++] = (IdT)((w0 + k) * 32 + b);
-        }
+        pos0 += total;
     }
 }
 
@@ -398,7 +397,7 @@ struct pmsz_plan {
     DevCounters* ctr = nullptr;
     DevCounters* hctr = nullptr;   // pinned mirror
     unsigned long long* block_counts = nullptr;
-    int64_t nblocks_compact = 0;
+    Chunks ch{};              // bitmap compaction layout
     int64_t scratch_bytes = 0;
     int cur = 0;              // pending dirty list
     int next_mode = 0;        // kFull / kMasked / kList / kMaskedList for the next iteration
@@ -511,9 +510,9 @@ pmsz_status reset_iter(pmsz_plan* p, cudaStream_t s, int nxt) {
 // lands in *dst on the device.
 void launch_bits_total(pmsz_plan* p, const uint32_t* bits, unsigned long long* dst, cudaStream_t s) {
     p->offsets_of = bits;
-    k_bits_count<<<(unsigned)p->nblocks_compact, kCompactThreads, 0, s>>>(bits, p->nwords, p->block_counts);
+    k_chunk_count<<<(unsigned)p->ch.n, kCompactThreads, 0, s>>>(bits, p->ch, p->block_counts);
     LAUNCHED();
-    k_exclusive_scan<<<1, 1024, 0, s>>>(p->block_counts, p->nblocks_compact, dst);
+    k_chunk_scan<<<1, kMaxChunks, 0, s>>>(p->block_counts, p->ch.n, dst);
     LAUNCHED();
 }
 
@@ -525,8 +524,8 @@ int sort_pending(pmsz_plan* p, cudaStream_t s) {
     p->bits_only = false;
     ProfScope ps(p, s, PMSZ_K_COMPACT);
     launch_bits_total(p, p->w.actbits, &p->ctr->nact[p->cur], s);
-    k_bits_list<uint32_t><<<(unsigned)p->nblocks_compact, kCompactThreads, 0, s>>>(p->w.actbits, p->nwords, p->block_counts,
-                                                                       p->w.act[p->cur], 1);
+    k_chunk_list<uint32_t><<<(unsigned)p->ch.n, kCompactThreads, 0, s>>>(p->w.actbits, p->ch, p->block_counts,
+                                                                      p->w.act[p->cur], 1);
     LAUNCHED();
     return 1;
 }
@@ -538,8 +537,8 @@ pmsz_status launch_apply(pmsz_plan* p, const void* f, double* g, cudaStream_t s,
         // touched bitmap -> ascending target list (load-balanced apply)
         ProfScope ps(p, s, PMSZ_K_COMPACT);
         launch_bits_total(p, p->w.touched, &p->ctr->nwork, s);
-        k_bits_list<uint32_t><<<(unsigned)p->nblocks_compact, kCompactThreads, 0, s>>>(p->w.touched, p->nwords,
-                                                                           p->block_counts, p->w.work, 1);
+        k_chunk_list<uint32_t><<<(unsigned)p->ch.n, kCompactThreads, 0, s>>>(p->w.touched, p->ch, p->block_counts,
+                                                                      p->w.work, 1);
         LAUNCHED();
     }
     ProfScope ps(p, s, PMSZ_K_APPLY);
@@ -628,8 +627,8 @@ pmsz_status iterate_once(pmsz_plan* p, const void* f, double* g, cudaStream_t s)
             {
                 ProfScope ps(p, s, PMSZ_K_COMPACT);
                 launch_bits_total(p, p->w.actbits, &p->ctr->ndefer, s);
-                k_bits_list<uint32_t><<<(unsigned)p->nblocks_compact, kCompactThreads, 0, s>>>(p->w.actbits, p->nwords,
-                                                                                   p->block_counts, p->w.work, 1);
+                k_chunk_list<uint32_t><<<(unsigned)p->ch.n, kCompactThreads, 0, s>>>(p->w.actbits, p->ch, p->block_counts,
+                                                                      p->w.work, 1);
                 LAUNCHED();
             }
             if (nonempty) {
@@ -652,8 +651,8 @@ pmsz_status iterate_once(pmsz_plan* p, const void* f, double* g, cudaStream_t s)
         {
             ProfScope ps(p, s, PMSZ_K_COMPACT);
             launch_bits_total(p, p->w.detbits, &p->ctr->ndefer, s);
-            k_bits_list<uint32_t><<<(unsigned)p->nblocks_compact, kCompactThreads, 0, s>>>(p->w.detbits, p->nwords,
-                                                                               p->block_counts, p->w.work, 0);
+            k_chunk_list<uint32_t><<<(unsigned)p->ch.n, kCompactThreads, 0, s>>>(p->w.detbits, p->ch, p->block_counts,
+                                                                      p->w.work, 0);
             LAUNCHED();
         }
         ProfScope ps(p, s, PMSZ_K_DEFER);
@@ -965,7 +964,7 @@ pmsz_status pmsz_plan_create(const pmsz_desc* desc, pmsz_plan** out) {
         p->ring_delta.d[k++] = 0;
         for (int r = 0; r < 14; ++r) p->ring_delta.d[k++] = rank_off(p->dom, r);
     }
-    p->nblocks_compact = (p->nwords + kWordsPerBlock - 1) / kWordsPerBlock;
+    p->ch = make_chunks(p->nwords, num_sms());
     auto alloc = [&](void** ptr, size_t bytes) -> bool {
         if (cudaMalloc(ptr, bytes) != cudaSuccess) return false;
         p->scratch_bytes += (int64_t)bytes;
@@ -975,7 +974,7 @@ pmsz_status pmsz_plan_create(const pmsz_desc* desc, pmsz_plan** out) {
               alloc((void**)&p->w.editbits, p->nwords * 4) && alloc((void**)&p->w.counts, n * 2) &&
               alloc((void**)&p->w.touched, p->nwords * 4) && alloc((void**)&p->w.detbits, p->nwords * 4) &&
               alloc((void**)&p->w.code, n) && alloc((void**)&p->ctr, sizeof(DevCounters)) &&
-              alloc((void**)&p->block_counts, std::max<int64_t>(p->nblocks_compact, 1) * 8);
+              alloc((void**)&p->block_counts, kMaxChunks * 8);
     if (ok && p->w.incremental)
         ok = alloc((void**)&p->w.actbits, p->nwords * 4) && alloc((void**)&p->w.act[0], p->w.act_cap * 4) &&
              alloc((void**)&p->w.act[1], p->w.act_cap * 4) && alloc((void**)&p->w.iteredit, p->nwords * 4) &&
@@ -1301,8 +1300,8 @@ pmsz_status pmsz_edits_export(pmsz_plan* p, const double* g, int64_t* ids, doubl
     if (count_out) *count_out = count;
     if (ids && vals && cap > 0 && count > 0) {
         ProfScope ps(p, s, PMSZ_K_COMPACT);
-        k_bits_write<<<(unsigned)p->nblocks_compact, kCompactThreads, 0, s>>>(p->w.editbits, p->nwords, p->n,
-                                                                             p->block_counts, g, ids, vals, cap);
+        k_chunk_write<<<(unsigned)p->ch.n, kCompactThreads, 0, s>>>(p->w.editbits, p->ch, p->n, p->block_counts, g, ids,
+                                                                   vals, cap);
         LAUNCHED();
         CUDA_TRY(cudaGetLastError());
     }
@@ -1639,20 +1638,23 @@ pmsz_status pmsz_bits_to_ids(const uint32_t* bits, int64_t nbits, int64_t* ids, 
     if (!bits || nbits < 0 || !count) return fail(PMSZ_ERR_INVALID, "bad arguments");
     cudaStream_t s = S(stream);
     const int64_t nwords = (nbits + 31) / 32;
-    const int64_t nblocks = std::max<int64_t>((nwords + kWordsPerBlock - 1) / kWordsPerBlock, 1);
+    if (nwords == 0) {
+        *count = 0;
+        return PMSZ_OK;
+    }
+    const Chunks ch = make_chunks(nwords, num_sms());
     unsigned long long* bc = nullptr;
-    CUDA_TRY(cudaMallocAsync((void**)&bc, (nblocks + 1) * 8, s));
-    k_bits_count<<<(unsigned)nblocks, kCompactThreads, 0, s>>>(bits, nwords, bc);
+    CUDA_TRY(cudaMallocAsync((void**)&bc, (kMaxChunks + 1) * 8, s));
+    k_chunk_count<<<(unsigned)ch.n, kCompactThreads, 0, s>>>(bits, ch, bc);
     LAUNCHED();
-    k_exclusive_scan<<<1, 1024, 0, s>>>(bc, nblocks, bc + nblocks);
+    k_chunk_scan<<<1, kMaxChunks, 0, s>>>(bc, ch.n, bc + kMaxChunks);
     LAUNCHED();
     unsigned long long total = 0;
-    CUDA_TRY(cudaMemcpyAsync(&total, bc + nblocks, 8, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(&total, bc + kMaxChunks, 8, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
     *count = (int64_t)total;
     if (ids && (int64_t)total <= cap && total > 0) {
-        k_bits_list<int64_t><<<(unsigned)nblocks, kCompactThreads, 0, s>>>(const_cast<uint32_t*>(bits), nwords, bc,
-                                                                           ids, 0);
+        k_chunk_list<int64_t><<<(unsigned)ch.n, kCompactThreads, 0, s>>>(const_cast<uint32_t*>(bits), ch, bc, ids, 0);
         LAUNCHED();
     }
     cudaFreeAsync(bc, s);
