@@ -85,14 +85,113 @@ def _tick(name, t0):
     return t1
 
 
-def run_distributed(engine, blocks, grid, rank: int, lockstep: bool, cap: int, group=None) -> DistStats:
+class CollectiveTransport:
+    """Ghost exchange by batched send/recv and sums by allreduce through the
+    process group (NCCL between GPUs, gloo in the CPU tests)."""
+
+    def __init__(self, engine, blocks, rank: int, group=None):
+        self.engine, self.group = engine, group
+        self.xs = exchanges(blocks, rank)
+        self.sent = 0
+
+    def allreduce(self, vals: list[int]) -> list[int]:
+        t = torch.tensor(vals, dtype=torch.int64, device=self.engine.device)
+        dist.all_reduce(t, group=self.group)
+        return [int(v) for v in t.tolist()]
+
+    def exchange(self) -> int:
+        """Send my replica of every overlap, min-merge the peers'; returns changed."""
+        eng = self.engine
+        recv = {x.peer: eng.empty(x) for x in self.xs}
+        ops = []
+        for x in self.xs:
+            buf = eng.pack(x)
+            self.sent += buf.numel() * buf.element_size()
+            ops.append(dist.P2POp(dist.isend, buf, x.peer, group=self.group))
+            ops.append(dist.P2POp(dist.irecv, recv[x.peer], x.peer, group=self.group))
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+        return sum(eng.merge(x, recv[x.peer]) for x in self.xs)
+
+
+class PeerTransport:
+    """Ghost exchange over NVLink peer memory (torch symmetric memory): every
+    rank packs its overlap replicas into its own symmetric buffer, and after a
+    device-side barrier the merge kernel reads the peers' replicas straight
+    out of their buffers (P2P loads) -- no staging copy, no NCCL launch.  The
+    round sums go through the same buffers.  A second barrier at the start of
+    the next exchange keeps a rank from overwriting a buffer a peer is still
+    reading."""
+
+    def __init__(self, engine, blocks, rank: int, group=None):
+        import torch.distributed._symmetric_memory as symm
+        self.engine = engine
+        self.rank = rank
+        self.world = len(blocks)
+        self.xs = exchanges(blocks, rank)
+        self.sent = 0
+        # layout of every rank's buffer: its overlaps in ascending-peer order, then 8 sum slots
+        self.layout = []
+        for r in range(self.world):
+            offs, o = {}, 0
+            for x in exchanges(blocks, r):
+                offs[x.peer] = o
+                o += x.size
+            self.layout.append((offs, o))
+        n = max(o for _, o in self.layout) + 8
+        self.buf = symm.empty(n, dtype=torch.float64, device=engine.device)
+        grp = (group or dist.group.WORLD).group_name
+        self.h = symm.rendezvous(self.buf, grp)
+        self.sums = [self.h.get_buffer(r, (n,), torch.float64)[n - 8:] for r in range(self.world)]
+        self.n = n
+        self.peer_views = {}
+        for x in self.xs:
+            offs, _ = self.layout[x.peer]
+            o = offs[self.rank]          # the peer's replica of the same overlap box
+            self.peer_views[x.peer] = self.h.get_buffer(x.peer, (n,), torch.float64)[o:o + x.size]
+        self.h.barrier(channel=0)
+
+    def allreduce(self, vals: list[int]) -> list[int]:
+        k = len(vals)
+        self.sums[self.rank][:k].copy_(torch.tensor(vals, dtype=torch.float64))
+        self.h.barrier(channel=0)
+        tot = torch.stack([s[:k] for s in self.sums]).sum(0)
+        out = [int(v) for v in tot.tolist()]
+        self.h.barrier(channel=0)     # nobody rewrites a slot before all have read it
+        return out
+
+    def exchange(self) -> int:
+        eng = self.engine
+        offs, _ = self.layout[self.rank]
+        for x in self.xs:
+            dst = self.buf[offs[x.peer]:offs[x.peer] + x.size]
+            dst.copy_(eng.pack(x))
+            self.sent += x.size * 8
+        self.h.barrier(channel=0)         # replicas of every rank are in place
+        changed = sum(eng.merge(x, self.peer_views[x.peer]) for x in self.xs)
+        self.h.barrier(channel=0)         # all peers are done reading my buffer
+        return changed
+
+
+def make_transport(engine, blocks, rank: int, group=None):
+    """Peer-memory transport on CUDA devices (PMSZ_P2P=0 forces the collectives)."""
+    if engine.device.type == "cuda" and os.environ.get("PMSZ_P2P", "1") != "0" and len(blocks) > 1:
+        try:
+            return PeerTransport(engine, blocks, rank, group)
+        except Exception:   # no P2P / symmetric memory on this system
+            pass
+    return CollectiveTransport(engine, blocks, rank, group)
+
+
+def run_distributed(engine, blocks, grid, rank: int, lockstep: bool, cap: int, group=None,
+                    transport=None) -> DistStats:
     """The round loop of run_parallel (parallel.py:289-322) across ranks."""
     trace = os.environ.get("PMSZ_DIST_TRACE") == "1"
-    xs = exchanges(blocks, rank)
-    dev = engine.device
+    tp = transport if transport is not None else CollectiveTransport(engine, blocks, rank, group)
+    sent0 = tp.sent
     rounds = syncs = 0
     totals: list[int] = []
-    sent = 0
     while True:
         if rounds >= cap:
             raise ConvergenceError(f"no terminal round within {cap}")
@@ -101,38 +200,21 @@ def run_distributed(engine, blocks, grid, rank: int, lockstep: bool, cap: int, g
         e, dirty = engine.round(lockstep)
         if trace:
             t0 = _tick(f"round{rounds}", t0)
-        t = torch.tensor([e, int(dirty)], dtype=torch.int64, device=dev)
-        dist.all_reduce(t, group=group)
-        round_edits, any_dirty = (int(v) for v in t.tolist())
+        round_edits, any_dirty = tp.allreduce([e, int(dirty)])
         if trace:
             t0 = _tick("allreduce", t0)
         totals.append(round_edits)
         if not lockstep and (round_edits == 0 or any_dirty == 0):
             break
-        # ghost exchange: send my replica of every overlap, min-merge theirs
-        recv = {x.peer: engine.empty(x) for x in xs}
-        ops = []
-        for x in xs:
-            buf = engine.pack(x)
-            sent += buf.numel() * buf.element_size()
-            ops.append(dist.P2POp(dist.isend, buf, x.peer, group=group))
-            ops.append(dist.P2POp(dist.irecv, recv[x.peer], x.peer, group=group))
-        if ops:
-            for req in dist.batch_isend_irecv(ops):
-                req.wait()
+        changed = tp.exchange()
         if trace:
-            t0 = _tick("exchange", t0)
-        changed = 0
-        for x in xs:
-            changed += engine.merge(x, recv[x.peer])
-        if trace:
-            t0 = _tick("merge", t0)
+            t0 = _tick("exchange+merge", t0)
         syncs += 1
         if lockstep:
-            c = torch.tensor([changed], dtype=torch.int64, device=dev)
-            dist.all_reduce(c, group=group)
-            if round_edits == 0 and int(c.item()) == 0:
+            (c,) = tp.allreduce([changed])
+            if round_edits == 0 and c == 0:
                 break
+    sent = tp.sent - sent0
     it, et, mve = engine.block_stats()
     return DistStats("lockstep" if lockstep else "relaxed", tuple(int(v) for v in grid), rounds, syncs,
                      tuple(totals), it, et, mve, sent)
@@ -234,7 +316,7 @@ class DeviceEngine:
         return self.plan.residual()
 
 
-def _e2e_host(args, eng, blocks, grid, rank, lockstep, cap, dev, nvox_total) -> dict:
+def _e2e_host(args, eng, blocks, grid, rank, lockstep, cap, dev, nvox_total, tp=None) -> dict:
     """End to end per rank: pinned host f32 original + f64 decompressed ext
     slab -> device, the distributed correction, the block's edit record
     (ids + values) -> pinned host.  Wall time per rank, max over ranks."""
@@ -248,7 +330,7 @@ def _e2e_host(args, eng, blocks, grid, rank, lockstep, cap, dev, nvox_total) -> 
         eng.f.copy_(f_host, non_blocking=True)
         eng.fh.copy_(fh_host, non_blocking=True)
         eng.prepare()
-        run_distributed(eng, blocks, grid, rank, lockstep, cap)
+        run_distributed(eng, blocks, grid, rank, lockstep, cap, transport=tp)
         ids, vals = eng.plan.export_edits(eng.g)
         hi = torch.empty(ids.numel(), dtype=torch.int64, pin_memory=True)
         hv = torch.empty(vals.numel(), dtype=torch.float64, pin_memory=True)
@@ -349,9 +431,11 @@ def bench_main(args, metric, unit, ClockSampler, measured_peaks, cpu_sample_inpu
     lockstep = args.strategy == "lockstep"
     cap = cfg.max_outer_iterations
 
+    tp = make_transport(eng, blocks, rank)
+
     def step():
         eng.prepare()
-        return run_distributed(eng, blocks, grid, rank, lockstep, cap)
+        return run_distributed(eng, blocks, grid, rank, lockstep, cap, transport=tp)
 
     for _ in range(max(args.warmup, 3)):
         st = step()
@@ -382,7 +466,7 @@ def bench_main(args, metric, unit, ClockSampler, measured_peaks, cpu_sample_inpu
     residual = torch.tensor([eng.residual()], dtype=torch.int64, device=dev)
     dist.all_reduce(residual)
     e2e = None if args.no_e2e else _e2e_host(args, eng, blocks, grid, rank, lockstep, cap, dev,
-                                              gdims[0] * gdims[1] * gdims[2])
+                                              gdims[0] * gdims[1] * gdims[2], tp)
     per_rank = [None] * world
     dist.all_gather_object(per_rank, {"rank": rank, "iterations": st.iterations, "edits": st.edit_total,
                                       "max_vertex_edits": st.max_vertex_edits, "ms": ms_local,
@@ -413,7 +497,7 @@ def bench_main(args, metric, unit, ClockSampler, measured_peaks, cpu_sample_inpu
                 "config": {"workload": wl["label"], "global_dims": list(gdims), "rel": args.rel,
                            "extrema_only": wl["extrema_only"],
                            "decomposition": f"{wl['decomp']} {grid}", "strategy": st.strategy,
-                           "parallelism": f"block-parallel x{world} (NCCL ghost exchange)",
+                           "parallelism": f"block-parallel x{world} ({'NVLink peer-memory' if isinstance(tp, PeerTransport) else 'NCCL'} ghost exchange)",
                            "xi_abs": xi, "l2": "inputs > L2"},
                 "roofline": {"bound": "hbm", "kernel": "sweep_full (rank 0)", "achieved": dk.get("achieved_gbs"),
                              "peak": peak, "unit": "GB/s", "frac": dk.get("frac"), "traffic": None,
