@@ -109,6 +109,20 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(self.rows)}
 
 
+def ncu_traffic(kernel: str, workload: str):
+    """DRAM bytes per launch of `kernel` from the committed ncu --set full
+    capture (profiles/*_ncu_traffic.json), when it was taken on this workload."""
+    best = None
+    for p in sorted((ROOT / "profiles").glob("*_ncu_traffic.json")):
+        try:
+            d = json.loads(p.read_text())
+        except Exception:
+            continue
+        if d.get("workload") == workload and kernel in d:
+            best = (d[kernel]["traffic_bytes"], p.name)
+    return best
+
+
 def measured_peaks() -> dict:
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -268,7 +282,13 @@ def run_ours_single(args):
                 "achieved": dk["achieved_gbs"], "peak": peak, "unit": "GB/s", "frac": dk["achieved_gbs"] / peak,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)" if not peaks.get("fallback")
                 else "fallback 6650 GB/s", "traffic": None,
+                "traffic_source": None,
                 "bytes_per_voxel": 9, "per_kernel": kernels}
+
+    tr = ncu_traffic("sweep_full", wl["label"])
+    if tr is not None:
+        roofline["traffic"] = tr[0]
+        roofline["traffic_source"] = f"profiles/{tr[1]} (dram__bytes_read+write per launch, ncu --set full)"
 
     # correctness evidence of the timed run
     check = {"iterations": res.iterations, "edits_per_iteration": list(res.edits_per_iteration),
