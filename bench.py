@@ -265,7 +265,7 @@ def run_ours_single(args):
     # roofline of the dominant kernels (algorithmic bytes per launch / event time)
     peaks = measured_peaks()
     peak = float(peaks.get("hbm_gbs", 6650.0))
-    per_voxel = {"sweep_full": 9, "sweep_masked": 9, "verify": 9, "prep": 4 + 8 + 8 + 1}
+    per_voxel = {"sweep_full": 9, "verify": 9, "prep": 4 + 8 + 8 + 1}   # full-domain kernels only
     kernels = {}
     for name, (kms, cnt) in prof.items():
         if cnt == 0:

@@ -476,7 +476,7 @@ def bench_main(args, metric, unit, ClockSampler, measured_peaks, cpu_sample_inpu
         peaks = measured_peaks()
         peak = float(peaks.get("hbm_gbs", 6650.0))
         kernels = {}
-        per_voxel = {"sweep_full": 9, "sweep_masked": 9, "prep": 4 + 8 + 8 + 1}
+        per_voxel = {"sweep_full": 9, "prep": 4 + 8 + 8 + 1}   # full-domain kernels only
         core = 1
         for a in range(3):
             core *= blk.core_stop[a] - blk.core_start[a]
