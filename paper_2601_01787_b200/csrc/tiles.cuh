@@ -179,10 +179,12 @@ __device__ __forceinline__ void count_kinds(const Dom& d, const Work& w, const S
 // Ops: what happens to a finalised centre.  fetch() issues the per-centre
 // global loads (two planes ahead); center() consumes them.
 
-// K1 / K4: detection against the f-code.  `dirty` (optional) restricts the
+// K1 / K4: detection against the f-code.  kMasked: `dirty` restricts the
 // centres to those whose bit is set (masked sweep of an incremental
-// iteration); their detection bits were cleared by the dilation kernel.
-template <bool kCount>
+// iteration; their detection bits were cleared by the dilation kernel).
+// kExtrema: the extrema-only mismatch test.  Both are template
+// parameters so the plain full sweep carries none of their logic.
+template <bool kCount, bool kMasked = false, bool kExtrema = false>
 struct DetectOp {
     Work w;
     const uint32_t* dirty;
@@ -196,15 +198,21 @@ struct DetectOp {
     // loads issued now, consumed two planes later
     __device__ __forceinline__ Pre fetch(int64_t c, bool live) const {
         if (!live) return Pre{0x100u, 0u, 0u};
-        return Pre{ld_nc_u8(w.code + c), dirty ? ld_nc_u32(dirty + (c >> 5)) : 1u, dirty ? (uint32_t)(c & 31) : 0u};
+        if (!kMasked) return Pre{ld_nc_u8(w.code + c), 1u, 0u};
+        return Pre{ld_nc_u8(w.code + c), ld_nc_u32(dirty + (c >> 5)), (uint32_t)(c & 31)};
     }
     __device__ __forceinline__ bool wants(const Pre& p) const {
+        if (!kMasked) return !(p.code & 0x100u);
         return !(p.code & 0x100u) && ((p.word >> p.sh) & 1u);
     }
-    __device__ __forceinline__ bool skippable() const { return dirty != nullptr; }
+    __device__ __forceinline__ bool skippable() const { return kMasked; }
     __device__ __forceinline__ void center(const Dom& d, int64_t c, const Scan& s, const Pre& p) {
         const uint8_t fc = (uint8_t)p.code;
-        if (!code_mismatch(d, scan_code(s), fc)) return;
+        const uint8_t gc = scan_code(s);
+        const bool mismatch = kExtrema ? (((gc & 15) == kExtremum) != ((fc & 15) == kExtremum) ||
+                                          ((gc >> 4) == kExtremum) != ((fc >> 4) == kExtremum))
+                                       : gc != fc;
+        if (!mismatch) return;
         ++ndet;
         if (kCount) count_kinds(d, w, s, fc);
         else atomicOr(w.detbits + (c >> 5), 1u << (c & 31));   // RED; k_defer picks it up
@@ -510,14 +518,25 @@ inline void tiled_grid(const Dom& d, dim3& grid, int& zchunk) {
     grid = dim3((unsigned)((cx + kTX - 1) / kTX), (unsigned)((cy + kRows - 1) / kRows), (unsigned)chunks);
 }
 
-template <bool kCount>
-inline void launch_sweep_full(const Dom& d, const double* g, const Work& w, cudaStream_t s,
-                              const uint32_t* dirty = nullptr) {
+template <bool kCount, bool kMasked, bool kExtrema>
+inline void launch_detect(const Dom& d, const double* g, const Work& w, cudaStream_t s, const uint32_t* dirty) {
     dim3 grid;
     int zchunk;
     tiled_grid(d, grid, zchunk);
-    DetectOp<kCount> op{w, dirty, 0};
-    k_tiled<double, DetectOp<kCount>><<<grid, dim3(kTX, kTY, 1), 0, s>>>(d, g, op, zchunk);
+    using Op = DetectOp<kCount, kMasked, kExtrema>;
+    Op op{w, dirty, 0};
+    k_tiled<double, Op><<<grid, dim3(kTX, kTY, 1), 0, s>>>(d, g, op, zchunk);
+}
+
+// kCount: the K4 count sweep (all six kinds, unmasked).
+template <bool kCount>
+inline void launch_sweep_full(const Dom& d, const double* g, const Work& w, cudaStream_t s,
+                              const uint32_t* dirty = nullptr) {
+    if (kCount) launch_detect<true, false, false>(d, g, w, s, nullptr);
+    else if (dirty && d.extrema_only) launch_detect<false, true, true>(d, g, w, s, dirty);
+    else if (dirty) launch_detect<false, true, false>(d, g, w, s, dirty);
+    else if (d.extrema_only) launch_detect<false, false, true>(d, g, w, s, nullptr);
+    else launch_detect<false, false, false>(d, g, w, s, nullptr);
 }
 
 template <typename FT>
