@@ -131,31 +131,35 @@ def measured_peaks() -> dict:
 
 
 # ---------------------------------------------------------------------------
-def _oracle_slab(kind: str, gdims, seed: int, z0: int, zs: int) -> np.ndarray:
-    """z-planes [z0, z0+zs) of the workload's f32 field, generated by the oracle."""
+def _oracle_slab(kind: str, gdims, seed: int, z0: int, zs: int, norm=None) -> np.ndarray:
+    """z-planes [z0, z0+zs) of the workload's f32 field, generated by the oracle
+    (`norm`: the Perlin normalisation extents when they differ from gdims)."""
     from oracle import oracle as orc
     ext = (gdims[0], gdims[1], zs)
     if kind == "hedm":
         v = orc.peaks(gdims, seed, lo=(0, 0, z0), ext=ext)
     else:
-        v = orc.perlin(gdims, seed, lo=(0, 0, z0), ext=ext)
+        v = orc.perlin(norm or gdims, seed, lo=(0, 0, z0), ext=ext)
     return v.astype(np.float32).astype(np.float64)
 
 
-def cpu_sample_inputs(kind: str, gdims, zs: int, rel: float, seed: int, xi=None, origin=None):
+def cpu_sample_inputs(kind: str, gdims, zs: int, rel: float, seed: int, xi=None, origin=None, norm=None,
+                      stat_planes=None):
     """Bounded CPU sample of the workload: the first `zs` z-planes of the same
     field (global coordinates).  xi and the quantizer origin belong to the
-    WHOLE field: passed in when the GPU already has them, else computed from
-    the oracle field slab by slab."""
+    whole field: passed in when the GPU already has them, else computed from
+    the oracle field slab by slab over the first `stat_planes` planes (all by
+    default)."""
     from oracle import oracle as orc
     if xi is None:
         lo, hi = np.inf, -np.inf
-        for z0 in range(0, gdims[2], 32):
-            v = _oracle_slab(kind, gdims, seed, z0, min(32, gdims[2] - z0))
+        nzs = gdims[2] if stat_planes is None else min(stat_planes, gdims[2])
+        for z0 in range(0, nzs, 32):
+            v = _oracle_slab(kind, gdims, seed, z0, min(32, nzs - z0), norm)
             lo, hi = min(lo, float(v.min())), max(hi, float(v.max()))
         xi = rel * (hi - lo) if hi > lo else rel * abs(hi)
         origin = lo
-    f = _oracle_slab(kind, gdims, seed, 0, zs)
+    f = _oracle_slab(kind, gdims, seed, 0, zs, norm)
     fh = orc.quantize(f, xi, origin=origin)
     return f, fh, xi, (gdims[0], gdims[1], zs)
 
@@ -185,7 +189,10 @@ def run_reference_arm(args):
     world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     wl = workload(args, max(world, 1))
     threads = os.cpu_count() or 1
-    f, fh, xi, dims = cpu_sample_inputs(args.workload, wl["gdims"], args.cpu_sample_z, args.rel, args.seed)
+    # weak scaling: xi from the first GPU's block (every block has its statistics)
+    f, fh, xi, dims = cpu_sample_inputs(args.workload, wl["gdims"], args.cpu_sample_z, args.rel, args.seed,
+                                        norm=wl.get("norm"),
+                                        stat_planes=args.size if wl["scaling"] == "weak" else None)
     orc.set_threads(threads)
     eo = wl["extrema_only"]
     n = dims[0] * dims[1] * dims[2]
@@ -311,7 +318,7 @@ def run_ours_single(args):
         line["e2e"] = e2e_host(args, plan, f32, fh, dims, nvox)
     if not args.no_cpu_baseline:
         f, fhs, xic, sdims = cpu_sample_inputs(args.workload, dims, args.cpu_sample_z, args.rel, args.seed,
-                                               xi=xi, origin=lo)
+                                               xi=xi, origin=lo, norm=wl.get("norm"))
         threads = os.cpu_count() or 1
         v, info = time_cpu_oracle(f, fhs, xic, sdims, threads, extrema_only=wl["extrema_only"])
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": info["threads"], "kind": "port",

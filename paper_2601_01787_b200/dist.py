@@ -396,10 +396,16 @@ def workload(args, world: int) -> dict:
                 "extrema_only": False, "data": "Perlin", "label": "perlin 1024^3 strong scaling (BASELINE config 4)",
                 "metric": "corrected voxels/sec (1024^3 strong scaling)",
                 "make": lambda lo, ext, dev: gen.perlin_device(spec, lo=lo, ext=ext, f32=True, device=dev)}
+    # Weak scaling keeps the Perlin coordinates normalised by the PER-GPU cube
+    # (px = x * freq / S on every axis), so each GPU's S^3 block has the
+    # statistics of the 1-GPU field; normalising by the global extent instead
+    # would make the field smoother per voxel as N grows and
+    # change the work per voxel.  N = 1 is exactly synth.perlin(S^3).
     gd = (S, S, S * world)
-    spec = gen.NoiseSpec(gd, args.seed)
+    spec = gen.NoiseSpec((S, S, S), args.seed)
     return {"gdims": gd, "grid": (1, 1, world), "decomp": "z-slabs", "scaling": "weak", "extrema_only": False,
             "data": "Perlin", "label": f"perlin {S}^3 per GPU (BASELINE config 2/3)", "metric": None,
+            "norm": (S, S, S),
             "make": lambda lo, ext, dev: gen.perlin_device(spec, lo=lo, ext=ext, f32=True, device=dev)}
 
 def bench_main(args, metric, unit, ClockSampler, measured_peaks, cpu_sample_inputs, time_cpu_oracle):
@@ -496,6 +502,8 @@ def bench_main(args, metric, unit, ClockSampler, measured_peaks, cpu_sample_inpu
                 "data": f"synthetic ({wl['data']}, f32, seed {args.seed}; quantizer; generated on device)",
                 "config": {"workload": wl["label"], "global_dims": list(gdims), "rel": args.rel,
                            "extrema_only": wl["extrema_only"],
+                           "perlin_normalisation": (f"per-GPU cube {wl['norm']} (constant per-voxel frequency)"
+                                                    if wl.get("norm") else None),
                            "decomposition": f"{wl['decomp']} {grid}", "strategy": st.strategy,
                            "parallelism": f"block-parallel x{world} ({'NVLink peer-memory' if isinstance(tp, PeerTransport) else 'NCCL'} ghost exchange)",
                            "xi_abs": xi, "l2": "inputs > L2"},
