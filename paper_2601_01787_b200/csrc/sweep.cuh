@@ -212,11 +212,7 @@ __device__ __forceinline__ void sweep_sparse_range(const Dom& d, const double* _
         int64_t x, y, z;
         coords(d, c, x, y, z);
         double nv[14];
-#pragma unroll
-        for (int r = 0; r < 14; ++r) {
-            const bool ok = in_dom(d, x + rank_dx(r), y + rank_dy(r), z + rank_dz(r));
-            nv[r] = ok ? __ldcg(g + c + rank_off(d, r)) : nan64();
-        }
+        load_ring(d, g, c, x, y, z, nv, [](const double* q) { return __ldcg(q); });
         const Scan s = fold_scan(__ldcg(g + c), nv);
         const uint8_t fc = w.code[c];
         const uint32_t bit = 1u << (c & 31);
