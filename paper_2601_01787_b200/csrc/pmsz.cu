@@ -423,7 +423,7 @@ struct pmsz_plan {
     unsigned long long* thist = nullptr;  // per-iteration edits of one tail launch
     unsigned long long* hthist = nullptr; // pinned mirror
     int tail_blocks[2] = {0, 0};          // cooperative grid per FT (f64, f32)
-    int64_t sort_min = 65536;             // dirty lists above this are sorted (compacted from actbits)
+    int64_t sort_min = 262144;            // longer dirty lists are kept in actbits only and rebuilt sorted
     int64_t dense_min = 0;                // dirty lists above this take the pipelined gather (kMaskedList)
     bool bits_only = false;               // the pending dirty set is in actbits only (no list)
     int64_t full_div = 8;                 // a full sweep follows when 15 x edits > ncore / full_div
@@ -572,6 +572,7 @@ pmsz_status choose_next(pmsz_plan* p, cudaStream_t s, bool marked_bits, int64_t 
         p->pending = bound;
         p->bits_only = true;
         p->next_mode = (p->gather_on && bound > p->dense_min) ? kMaskedList : kList;
+        if (p->next_mode == kList && bound > (int64_t)p->w.act_cap) p->next_mode = kFull;   // list would overflow
     } else if (nact > (int64_t)p->w.act_cap) {
         p->next_mode = kFull;
     } else {
@@ -703,6 +704,8 @@ pmsz_status launch_tail(pmsz_plan* p, const void* f, double* g, cudaStream_t s, 
         nb = std::min(per, cap) * num_sms();
     }
     unsigned long long sort_min = (unsigned long long)p->sort_min;
+    unsigned long long dense_min = (unsigned long long)(p->gather_on ? p->dense_min : p->w.act_cap);
+    unsigned long long* cc = p->block_counts;
     Dom d = p->dom;
     const FT* fp = (const FT*)f;
     Work w = p->w;
@@ -719,7 +722,7 @@ pmsz_status launch_tail(pmsz_plan* p, const void* f, double* g, cudaStream_t s, 
         tr = trace_buf;
         CUDA_TRY(cudaMemsetAsync(tr, 0, 2 * 8 * 4096, s));
     }
-    void* args[] = {&d, &fp, &g, &w, &cur, &sorted, &sort_min, &budget, &h, &t, &tr};
+    void* args[] = {&d, &fp, &g, &w, &cur, &sorted, &sort_min, &dense_min, &cc, &budget, &h, &t, &tr};
     CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_tail<FT>, dim3(nb), dim3(256), args, 0, s));
     LAUNCHED();
     if (trace) {
@@ -811,7 +814,10 @@ pmsz_status restore_prop(pmsz_plan* p, cudaStream_t s) {
     return PMSZ_OK;
 }
 
-pmsz_status prep(pmsz_plan* p, const void* f, const double* fh, double* g, cudaStream_t s) {
+// K0.  sync == false leaves the validation counters on the device: the caller
+// reads them with the first iteration's counters (one synchronisation less)
+// and must call prep_checks() before trusting anything else.
+pmsz_status prep(pmsz_plan* p, const void* f, const double* fh, double* g, cudaStream_t s, bool sync = true) {
     pmsz_status st = reset_run_state(p, s);
     if (st) return st;
     {
@@ -823,11 +829,24 @@ pmsz_status prep(pmsz_plan* p, const void* f, const double* fh, double* g, cudaS
         LAUNCHED();
     }
     CUDA_TRY(cudaGetLastError());
+    p->prepared = true;
+    if (!sync) {
+        p->floor_viol = p->upper_viol = 0;   // unknown until prep_checks()
+        return PMSZ_OK;
+    }
     st = sync_counters(p, s);
     if (st) return st;
     p->floor_viol = (int64_t)p->hctr->floor_viol;
     p->upper_viol = (int64_t)p->hctr->upper_viol;
-    p->prepared = true;
+    return PMSZ_OK;
+}
+
+// The K0 verdicts from the (already synchronised) host counters.
+pmsz_status prep_checks(pmsz_plan* p) {
+    p->floor_viol = (int64_t)p->hctr->floor_viol;
+    p->upper_viol = (int64_t)p->hctr->upper_viol;
+    if (p->hctr->nonfinite) return fail(PMSZ_ERR_NONFINITE, "field values must all be finite");
+    if (p->hctr->bound_viol) return fail(PMSZ_ERR_BOUND, "error bound violated");
     return PMSZ_OK;
 }
 
@@ -1229,11 +1248,31 @@ pmsz_status pmsz_run_correction(pmsz_plan* p, const void* f, const double* fh, d
     pmsz_result local{};
     if (!r) r = &local;
     memset(r, 0, sizeof(*r));
-    pmsz_status st = pmsz_prepare(p, f, fh, g, r, stream);
+    // Out of place, K0's validation is read together with the first
+    // iteration's counters (g is an output buffer, so running one iteration
+    // on invalid input has no visible effect beyond the error).  In place
+    // (g aliases fhat) it is checked before anything is written.
+    const bool deferred = g != fh && p->desc.max_iterations > 0;
+    pmsz_status st = deferred ? prep(p, f, fh, g, s, false) : pmsz_prepare(p, f, fh, g, r, stream);
     if (st) return st;
     bool converged = false;
     int64_t it = 0;
-    for (; it < p->desc.max_iterations; ++it) {
+    if (deferred) {
+        st = pmsz_iterate(p, f, g, nullptr, r, stream);
+        if (st) return st;
+        fill_result(p, r);
+        st = prep_checks(p);
+        if (st) { restore_prop(p, s); return st; }
+        if (p->floor_viol > 0 && p->hctr->ndetect > 0) {   // correction.py:240-241
+            restore_prop(p, s);
+            return fail(PMSZ_ERR_MONOTONE, "edit raised a value; monotonicity broken");
+        }
+        const int64_t e = (int64_t)p->hctr->nedits;
+        if (history && history_cap > 0) history[0] = e;
+        it = 1;
+        if (e == 0) converged = true;
+    }
+    for (; !converged && it < p->desc.max_iterations; ++it) {
         if (tail_ok(p)) {
             int64_t k = 0;
             bool sh = false;

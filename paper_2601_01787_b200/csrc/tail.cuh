@@ -49,11 +49,89 @@ struct TailState {
     unsigned long long appended;     // the pending dirty set is listed (else: actbits only, `pending` a bound)
 };
 
+// In-tail rebuild of a long dirty list: the ascending compaction of actbits
+// into `list` (bits cleared).  Every WARP of the grid owns one contiguous
+// sub-chunk of words, so the walk needs only warp scans; the per-warp counts
+// stay in shared memory across the grid barrier that separates counting from
+// writing, the per-CTA totals go through `counts`.  Every CTA then knows the
+// total and takes the same decision.
+constexpr int kTailWarps = 8;
+
+__device__ __forceinline__ int64_t tail_warp_chunk(int64_t nwords) {
+    const int64_t nw = (int64_t)gridDim.x * kTailWarps;
+    return ((nwords + nw - 1) / nw + 31) / 32 * 32;
+}
+
+__device__ __forceinline__ unsigned long long tail_chunk_count(const uint32_t* bits, int64_t nwords,
+                                                               unsigned long long* counts, unsigned* warp_cnt) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int64_t chunk = tail_warp_chunk(nwords);
+    const int64_t w0 = ((int64_t)blockIdx.x * kTailWarps + wid) * chunk, w1 = min(w0 + chunk, nwords);
+    unsigned t = 0;
+    for (int64_t base = w0; base < w1; base += 8 * 32) {
+        uint32_t v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {   // 8 independent loads in flight
+            const int64_t q = base + k * 32 + lane;
+            v[k] = q < w1 ? __ldcg(bits + q) : 0u;
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) t += __popc(v[k]);
+    }
+    t = __reduce_add_sync(0xffffffffu, t);
+    if (lane == 0) warp_cnt[wid] = t;
+    __syncthreads();
+    unsigned long long s = 0;
+    for (int q = 0; q < kTailWarps; ++q) s += warp_cnt[q];
+    if (threadIdx.x == 0) counts[blockIdx.x] = s;
+    return s;
+}
+
+__device__ __forceinline__ void tail_chunk_write(uint32_t* bits, int64_t nwords, unsigned long long cta_pos,
+                                                 const unsigned* warp_cnt, uint32_t* list) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int64_t chunk = tail_warp_chunk(nwords);
+    const int64_t w0 = ((int64_t)blockIdx.x * kTailWarps + wid) * chunk, w1 = min(w0 + chunk, nwords);
+    unsigned long long pos0 = cta_pos;
+    for (int q = 0; q < wid; ++q) pos0 += warp_cnt[q];
+    for (int64_t base = w0; base < w1; base += 8 * 32) {
+        uint32_t v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int64_t q = base + k * 32 + lane;
+            v[k] = q < w1 ? __ldcg(bits + q) : 0u;
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int64_t q = base + k * 32 + lane;
+            uint32_t m = v[k];
+            if (m) bits[q] = 0u;
+            const unsigned c = __popc(m);
+            unsigned sc = c;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned y = __shfl_up_sync(0xffffffffu, sc, o);
+                if (lane >= o) sc += y;
+            }
+            unsigned long long pos = pos0 + sc - c;
+            while (m) {
+                const int b = __ffs(m) - 1;
+                m &= m - 1;
+                list[pos++] = (uint32_t)(q * 32 + b);
+            }
+            pos0 += __shfl_sync(0xffffffffu, sc, 31);
+        }
+    }
+}
+
 template <typename FT>
 __global__ void __launch_bounds__(256) k_tail(Dom d, const FT* __restrict__ f, double* g, Work w, int cur,
-                                              int sorted, unsigned long long sort_min, long long budget, unsigned long long* __restrict__ hist,
-                                              TailState* ts, unsigned long long* __restrict__ trace) {
+                                              int sorted, unsigned long long sort_min, unsigned long long dense_min,
+                                              unsigned long long* __restrict__ chunk_counts, long long budget,
+                                              unsigned long long* __restrict__ hist, TailState* ts,
+                                              unsigned long long* __restrict__ trace) {
     cg::grid_group grid = cg::this_grid();
+    __shared__ unsigned warp_cnt[kTailWarps];
     const unsigned long long tid = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
     const bool leader = tid == 0;
@@ -73,7 +151,7 @@ __global__ void __launch_bounds__(256) k_tail(Dom d, const FT* __restrict__ f, d
             c->nelist = 0;
             c->shared_dirty = 0;
         }
-        sweep_sparse_range(d, g, w, cur, sorted && it == 0, tid, stride);
+        sweep_sparse_range(d, g, w, cur, sorted != 0, tid, stride);
         grid.sync();
         if (trace && leader && it < 4) {
             unsigned long long t;
@@ -112,23 +190,47 @@ __global__ void __launch_bounds__(256) k_tail(Dom d, const FT* __restrict__ f, d
             trace[2 * it] = t;
             trace[2 * it + 1] = nact;
         }
-        unsigned long long exit = 0;
+        unsigned long long exit = 0, pending = append ? nact : nel * 15ull;   // a bound when only actbits was marked
+        bool listed = append;
         if (nedits == 0) exit = kTailConverged;
         else if (mark != kMarkList) exit = kTailBits;
         else if (nact > w.act_cap) exit = kTailOverflow;
         else if (it + 1 >= budget) exit = kTailBudget;
-        else if (!append || nact > sort_min) exit = kTailSort;   // large: the host sorts the list first
+        else if (!append || nact > sort_min) {
+            // a long dirty set: rebuild the list sorted from actbits here, or
+            // hand it to the host's gather path when it is longer still
+            tail_chunk_count(w.actbits, w.nwords, chunk_counts, warp_cnt);
+            grid.sync();
+            unsigned long long total = 0, before = 0;
+            for (unsigned q = 0; q < gridDim.x; ++q) {
+                const unsigned long long v = __ldcg(chunk_counts + q);
+                total += v;
+                before += q < blockIdx.x ? v : 0ull;
+            }
+            if (total > dense_min) {
+                exit = kTailSort;   // the set stays in actbits (exact count in `pending`)
+                pending = total;
+                listed = false;
+            } else {
+                tail_chunk_write(w.actbits, w.nwords, before, warp_cnt, w.act[nxt]);
+                if (leader) c->nact[nxt] = total;
+                grid.sync();
+                sorted = 1;
+            }
+        } else {
+            sorted = 0;
+        }
         if (exit) {
             if (leader) {
                 ts->iterations = (unsigned long long)(it + 1);
                 ts->exit = exit;
                 ts->cur = (unsigned long long)nxt;
-                ts->pending = append ? nact : nel * 15ull;   // a bound when only actbits was marked
+                ts->pending = pending;
                 ts->last_edits = nedits;
                 ts->last_detect = ndet;
                 ts->shared_or = shared_or;
                 ts->detections = detections;
-                ts->appended = append ? 1ull : 0ull;
+                ts->appended = listed ? 1ull : 0ull;
                 c->ndetect = ndet;   // the host reads the last iteration's counters
             }
             return;
