@@ -337,12 +337,12 @@ __device__ __forceinline__ void flush_acc(const Work& w, const ApplyAcc& a) {
 
 // K2 over the target list (compacted from the touched bitmap after a tiled
 // sweep, or appended by first touch in a sparse sweep).
-template <typename FT>
+// kB: targets in flight per thread (more memory parallelism, more registers).
+template <int kB, typename FT>
 __device__ __forceinline__ void apply_range(const Dom& d, const FT* __restrict__ f, double* __restrict__ g,
                                             const Work& w, int nxt, int mark, unsigned long long i0,
                                             unsigned long long stride) {
     const unsigned long long n = __ldcg(&w.ctr->nwork);
-    constexpr int kB = 4;   // targets in flight per thread
     ApplyAcc acc;
     for (; i0 < n; i0 += kB * stride) {
         int64_t t[kB];
@@ -376,7 +376,7 @@ template <typename FT>
 __global__ void __launch_bounds__(256) k_apply_list(Dom d, const FT* __restrict__ f, double* __restrict__ g,
                                                     Work w, int nxt) {
     const int mark = apply_marks(w);
-    apply_range(d, f, g, w, nxt, mark, (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x,
+    apply_range<8>(d, f, g, w, nxt, mark, (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x,
                 (unsigned long long)gridDim.x * blockDim.x);
 }
 

@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(256) k_tail(Dom d, const FT* __restrict__ f, d
         const unsigned long long ndet = __ldcg(&c->ndetect);
         if (leader) c->nact[nxt] = 0;
         const int mark = apply_marks(w);
-        apply_range(d, f, g, w, nxt, mark, tid, stride);
+        apply_range<4>(d, f, g, w, nxt, mark, tid, stride);
         grid.sync();
         if (trace && leader && it < 4) {
             unsigned long long t;
