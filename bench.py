@@ -301,6 +301,7 @@ def run_ours_single(args):
     check = {"iterations": res.iterations, "edits_per_iteration": list(res.edits_per_iteration),
              "edit_count": int(res.edit_ids.numel()), "max_vertex_edits": res.max_vertex_edits,
              "full_sweeps": res.full_sweeps, "masked_sweeps": res.masked_sweeps,
+             "fragile_fraction": round(res.fragile / float(nvox), 4) if res.fragile >= 0 else None,
              "sparse_sweeps": res.sparse_sweeps, "residual": 0}
 
     line = {"metric": wl["metric"] or METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,

@@ -105,6 +105,7 @@ typedef struct {
     int64_t last_edits;            /* edits of the last iteration */
     int64_t last_detections;       /* centres with a detection in the last iteration */
     int64_t masked_sweeps;         /* tiled sweeps restricted to a dilated dirty bitmap */
+    int64_t fragile;               /* centres K0 found not robust (the only ones ever evaluated) */
 } pmsz_result;
 
 /* Error string of the last failing call on this thread. */

@@ -64,7 +64,7 @@ class PmszResult(ctypes.Structure):
         ("floor_violations", i64), ("nonfinite", i64),
         ("residual", i64 * 6), ("convergence_kind", i64),
         ("full_sweeps", i64), ("sparse_sweeps", i64), ("shared_dirty", i64),
-        ("last_edits", i64), ("last_detections", i64), ("masked_sweeps", i64),
+        ("last_edits", i64), ("last_detections", i64), ("masked_sweeps", i64), ("fragile", i64),
     ]
 
 

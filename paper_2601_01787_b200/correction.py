@@ -184,6 +184,7 @@ class DeviceCorrection:
     full_sweeps: int
     sparse_sweeps: int
     masked_sweeps: int = 0
+    fragile: int = -1     # centres K0 left fragile (robust ones are never evaluated)
 
 
 _PLAN_CACHE: dict = {}
@@ -235,7 +236,7 @@ def run_correction_device(f: torch.Tensor, fhat: torch.Tensor, dims, config: Cor
                             iterations=int(res.iterations), edits_per_iteration=tuple(hist),
                             max_vertex_edits=int(res.max_vertex_edits),
                             full_sweeps=int(res.full_sweeps), sparse_sweeps=int(res.sparse_sweeps),
-                            masked_sweeps=int(res.masked_sweeps))
+                            masked_sweeps=int(res.masked_sweeps), fragile=int(res.fragile))
 
 
 def run_correction(original: ScalarField, decompressed: ScalarField, config: CorrectionConfig,

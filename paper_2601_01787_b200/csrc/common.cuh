@@ -35,6 +35,8 @@ __host__ __device__ constexpr int rank_dz(int r) { return (int)((kPackDZ >> (2 *
 // Centre sorts above ranks 0..6 and below ranks 7..13.
 constexpr int kCenterBelow = 6;
 constexpr uint8_t kExtremum = 15;
+// f-code of a robust centre (tiles.cuh, acc_robust): never evaluated
+constexpr uint8_t kRobust = 0xEE;
 
 struct Dom {
     int64_t nx, ny, nz;   // domain (ext) extents

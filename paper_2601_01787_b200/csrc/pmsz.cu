@@ -28,6 +28,7 @@
 #include "tiles.cuh"
 #include "tail.cuh"
 #include "gather.cuh"
+#include "qsweep.cuh"
 #include "segment.cuh"
 
 using namespace pmsz;
@@ -353,7 +354,8 @@ struct RingDelta {
 // The masked sweep re-evaluates exactly the dirty centres, so their detection
 // bits are cleared here and set again by the sweep for those that still fire.
 __global__ void __launch_bounds__(256) k_dilate(const uint32_t* __restrict__ e, uint32_t* __restrict__ out,
-                                                uint32_t* __restrict__ det, int64_t nwords, RingDelta rd) {
+                                                uint32_t* __restrict__ det, const uint32_t* __restrict__ frag,
+                                                int64_t nwords, RingDelta rd) {
     for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nwords;
          w += (int64_t)gridDim.x * blockDim.x) {
         uint32_t acc = 0;
@@ -366,6 +368,7 @@ __global__ void __launch_bounds__(256) k_dilate(const uint32_t* __restrict__ e, 
             const uint32_t hi = (q + 1 >= 0 && q + 1 < nwords) ? __ldg(e + q + 1) : 0u;
             acc |= __funnelshift_r(lo, hi, sh);
         }
+        if (frag) acc &= __ldg(frag + w);   // robust centres are never evaluated
         out[w] = acc;
         if (acc) det[w] &= ~acc;
     }
@@ -430,7 +433,11 @@ struct pmsz_plan {
     const uint32_t* offsets_of = nullptr; // bitmap whose block offsets block_counts holds
     int64_t edits_cached = -1;            // popcount(editbits) since the last iteration, -1 = unknown
     bool gather_on = true;                // masked iterations as sorted gathers (gather.cuh)
+    bool robust_on = true;                // K0 classifies robust centres (never evaluated afterwards)
+    bool qsweep_on = true;                // tiled sweeps evaluate a per-plane queue of fragile centres (qsweep.cuh)
+    uint32_t* frag = nullptr;             // fragile-centre bitmap written by K0
     // host-buffer entry point staging (pmsz_run_correction_host)
+    uint32_t* frag_out() const { return robust_on ? frag : nullptr; }
     void* stage_f = nullptr;
     double* stage_g = nullptr;
     int64_t* stage_ids = nullptr;
@@ -611,7 +618,7 @@ pmsz_status iterate_once(pmsz_plan* p, const void* f, double* g, cudaStream_t s)
         p->w.track = 0;
         if (nonempty) {
             ProfScope ps(p, s, PMSZ_K_SWEEP_FULL);
-            launch_sweep_full<false>(d, g, p->w, s);
+            if (!(p->qsweep_on && launch_sweep_q<false>(d, g, p->w, s))) launch_sweep_full<false>(d, g, p->w, s);
             LAUNCHED();
         }
     } else if (mode == kMasked || mode == kMaskedList) {
@@ -619,7 +626,7 @@ pmsz_status iterate_once(pmsz_plan* p, const void* f, double* g, cudaStream_t s)
         if (mode == kMasked) {   // dirty set = dilation of the previous iteration's edits
             ProfScope ps(p, s, PMSZ_K_OTHER);
             k_dilate<<<grid_for(p->nwords, 256, 8), 256, 0, s>>>(p->w.iteredit, p->w.actbits, p->w.detbits,
-                                                               p->nwords, p->ring_delta);
+                                                               p->w.frag, p->nwords, p->ring_delta);
             LAUNCHED();
             CUDA_TRY(cudaMemsetAsync(p->w.iteredit, 0, p->nwords * 4, s));
         }                        // kMaskedList: the dirty set is actbits as marked (list dropped)
@@ -641,7 +648,8 @@ pmsz_status iterate_once(pmsz_plan* p, const void* f, double* g, cudaStream_t s)
         } else {
             if (nonempty) {
                 ProfScope ps(p, s, PMSZ_K_SWEEP_MASKED);
-                launch_sweep_full<false>(d, g, p->w, s, p->w.actbits);
+                if (!(p->qsweep_on && launch_sweep_q<false>(d, g, p->w, s, p->w.actbits)))
+                    launch_sweep_full<false>(d, g, p->w, s, p->w.actbits);
                 LAUNCHED();
             }
             CUDA_TRY(cudaMemsetAsync(p->w.actbits, 0, p->nwords * 4, s));
@@ -822,10 +830,12 @@ pmsz_status prep(pmsz_plan* p, const void* f, const double* fh, double* g, cudaS
     if (st) return st;
     {
         ProfScope ps(p, s, PMSZ_K_PREP);
+        p->w.frag = p->robust_on ? p->frag : nullptr;
+        if (p->robust_on) CUDA_TRY(cudaMemsetAsync(p->frag, 0, p->nwords * 4, s));
         if (p->f32)
-            launch_prep<float>(p->dom, (const float*)f, fh, g, p->w.code, p->ctr, s);
+            launch_prep<float>(p->dom, (const float*)f, fh, g, p->w.code, p->frag_out(), p->ctr, s);
         else
-            launch_prep<double>(p->dom, (const double*)f, fh, g, p->w.code, p->ctr, s);
+            launch_prep<double>(p->dom, (const double*)f, fh, g, p->w.code, p->frag_out(), p->ctr, s);
         LAUNCHED();
     }
     CUDA_TRY(cudaGetLastError());
@@ -856,7 +866,7 @@ pmsz_status verify_sweep(pmsz_plan* p, const double* g, cudaStream_t s, int64_t 
     const int64_t cx = d.hi[0] - d.lo[0], cy = d.hi[1] - d.lo[1], cz = d.hi[2] - d.lo[2];
     if (cx > 0 && cy > 0 && cz > 0) {
         ProfScope ps(p, s, PMSZ_K_VERIFY);
-        launch_sweep_full<true>(d, g, p->w, s);
+        if (!(p->qsweep_on && launch_sweep_q<true>(d, g, p->w, s))) launch_sweep_full<true>(d, g, p->w, s);
         LAUNCHED();
     }
     CUDA_TRY(cudaGetLastError());
@@ -934,6 +944,7 @@ void fill_result(pmsz_plan* p, pmsz_result* r) {
     r->bound_first_index = (int64_t)p->hctr->bound_first;
     r->floor_violations = p->floor_viol;
     r->nonfinite = (int64_t)p->hctr->nonfinite;
+    r->fragile = p->robust_on ? (int64_t)p->hctr->nfragile : p->n;
     r->max_vertex_edits = (int64_t)p->hctr->maxcount;
 }
 
@@ -992,7 +1003,8 @@ pmsz_status pmsz_plan_create(const pmsz_desc* desc, pmsz_plan** out) {
     bool ok = alloc((void**)&p->w.prop, n * 8) && alloc((void**)&p->w.work, n * 4) &&
               alloc((void**)&p->w.editbits, p->nwords * 4) && alloc((void**)&p->w.counts, n * 2) &&
               alloc((void**)&p->w.touched, p->nwords * 4) && alloc((void**)&p->w.detbits, p->nwords * 4) &&
-              alloc((void**)&p->w.code, n) && alloc((void**)&p->ctr, sizeof(DevCounters)) &&
+              alloc((void**)&p->w.code, n) && alloc((void**)&p->frag, p->nwords * 4) &&
+              alloc((void**)&p->ctr, sizeof(DevCounters)) &&
               alloc((void**)&p->block_counts, kMaxChunks * 8);
     if (ok && p->w.incremental)
         ok = alloc((void**)&p->w.actbits, p->nwords * 4) && alloc((void**)&p->w.act[0], p->w.act_cap * 4) &&
@@ -1009,6 +1021,8 @@ pmsz_status pmsz_plan_create(const pmsz_desc* desc, pmsz_plan** out) {
     if (const char* e = getenv("PMSZ_DENSE_MIN")) p->dense_min = atoll(e);
     if (const char* e = getenv("PMSZ_FULL_DIV")) p->full_div = std::max<int64_t>(1, atoll(e));
     if (const char* e = getenv("PMSZ_SWEEP")) p->gather_on = strcmp(e, "tiled") != 0;
+    if (const char* e = getenv("PMSZ_ROBUST")) p->robust_on = atoi(e) != 0;
+    if (const char* e = getenv("PMSZ_QSWEEP")) p->qsweep_on = atoi(e) != 0;
     if (cudaFuncSetAttribute(k_gather<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGatherSmem) !=
             cudaSuccess ||
         cudaFuncSetAttribute(k_gather<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGatherSmem) !=
@@ -1037,7 +1051,7 @@ pmsz_status pmsz_plan_create(const pmsz_desc* desc, pmsz_plan** out) {
 void pmsz_plan_destroy(pmsz_plan* p) {
     if (!p) return;
     cudaFree(p->w.prop); cudaFree(p->w.work); cudaFree(p->w.touched); cudaFree(p->w.detbits); cudaFree(p->w.editbits); cudaFree(p->w.counts);
-    cudaFree(p->w.code); cudaFree(p->ctr); cudaFree(p->block_counts);
+    cudaFree(p->w.code); cudaFree(p->frag); cudaFree(p->ctr); cudaFree(p->block_counts);
     cudaFree(p->w.actbits); cudaFree(p->w.act[0]); cudaFree(p->w.act[1]); cudaFree(p->w.iteredit);
     cudaFree(p->w.elist);
     if (p->hctr) cudaFreeHost(p->hctr);

@@ -36,6 +36,7 @@ struct DevCounters {
     unsigned long long floor_viol;
     unsigned long long upper_viol;
     unsigned long long nonfinite;
+    unsigned long long nfragile;     // K0: centres that are not robust
     unsigned long long changed;      // merge helpers
     unsigned long long scratch[4];
 };
@@ -52,6 +53,7 @@ struct Work {
     uint32_t* elist;            // edits of a list-mode iteration (ring marking input)
     uint16_t* counts;           // per-vertex edit counts
     uint8_t* code;              // packed f-code
+    const uint32_t* frag;       // n bits: fragile centres (K0); null = every centre is evaluated
     uint8_t* edited_mask;       // optional per-iteration mask
     DevCounters* ctr;
     unsigned long long act_cap;
@@ -108,6 +110,7 @@ struct EmitList {
 
 // Mismatch between the g-scan and the f-code, i.e. "some rule fires".
 __device__ __forceinline__ bool code_mismatch(const Dom& d, uint8_t gcode, uint8_t fcode) {
+    if (fcode == kRobust) return false;   // robust centres never mismatch (tiles.cuh, acc_robust)
     if (!d.extrema_only) return gcode != fcode;
     const bool gx = (gcode & 15) == kExtremum, fx = (fcode & 15) == kExtremum;
     const bool gn = (gcode >> 4) == kExtremum, fn = (fcode >> 4) == kExtremum;
@@ -255,6 +258,7 @@ __device__ __forceinline__ void mark_ring(const Dom& d, const Work& w, int64_t v
         if (!in_core(d, px, py, pz)) continue;
         const int64_t u = px + py * d.sy + pz * d.sz;
         const uint32_t bit = 1u << (u & 31);
+        if (w.frag && !(__ldg(w.frag + (u >> 5)) & bit)) continue;   // robust: never evaluated
         if (__ldcg(w.actbits + (u >> 5)) & bit) continue;
         const uint32_t old = atomicOr(w.actbits + (u >> 5), bit);
         if (old & bit) continue;
@@ -403,6 +407,7 @@ __device__ __forceinline__ void mark_list_range(const Dom& d, const Work& w, int
         if (!in_core(d, px, py, pz)) continue;
         const int64_t u = px + py * d.sy + pz * d.sz;
         const uint32_t bit = 1u << (u & 31);
+        if (w.frag && !(__ldg(w.frag + (u >> 5)) & bit)) continue;   // robust: never evaluated
         if (!append) {
             atomicOr(w.actbits + (u >> 5), bit);
             continue;

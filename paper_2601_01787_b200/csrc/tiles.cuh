@@ -83,6 +83,7 @@ template <typename V>
 struct Pair {
     V mx, mn;
     int bx, bn;
+    V sx, sn;   // the loser of each side (second extrema, K0's robustness test)
 };
 template <typename V>
 __device__ __forceinline__ Pair<V> xpair(const Leaf<V>& l, const Leaf<V>& r) {
@@ -93,16 +94,21 @@ __device__ __forceinline__ Pair<V> xpair(const Leaf<V>& l, const Leaf<V>& r) {
     const bool tn = r.mn < l.mn;    // ties -> smaller id
     p.mn = tn ? r.mn : l.mn;
     p.bn = tn;
+    p.sx = min(l.mx, r.mx);
+    p.sn = max(l.mn, r.mn);
     return p;
 }
 
 // 2x2 box from the x-pairs of rows r (lo) and r+1 (hi): corner 0..3 in id order.
+// sx / sn: the second largest / smallest value of the group (K0's robustness
+// test).
 template <typename V>
 struct Quad {
     V mx, mn;
     int cx, cn;
+    V sx, sn;
 };
-template <typename V>
+template <bool kSecond, typename V>
 __device__ __forceinline__ Quad<V> ybox(const Pair<V>& lo, const Pair<V>& hi) {
     Quad<V> b;
     const bool tx = hi.mx >= lo.mx;
@@ -111,21 +117,32 @@ __device__ __forceinline__ Quad<V> ybox(const Pair<V>& lo, const Pair<V>& hi) {
     const bool tn = hi.mn < lo.mn;
     b.mn = tn ? hi.mn : lo.mn;
     b.cn = tn ? 2 + hi.bn : lo.bn;
+    if (kSecond) {
+        b.sx = max(min(lo.mx, hi.mx), max(lo.sx, hi.sx));
+        b.sn = min(max(lo.mn, hi.mn), min(lo.sn, hi.sn));
+    }
     return b;
 }
 template <typename V>
-__device__ __forceinline__ Quad<V> missing_quad() { return Quad<V>{-vinf<V>(), vinf<V>(), 0, 0}; }
+__device__ __forceinline__ Quad<V> missing_quad() {
+    return Quad<V>{-vinf<V>(), vinf<V>(), 0, 0, -vinf<V>(), vinf<V>()};
+}
 
-// Running fold in ascending rank order.
+// Running fold in ascending rank order (sx / sn: running second extrema).
 template <typename V>
 struct Acc {
     V mx, mn;
     int rx, rn;
+    V sx, sn;
 };
 template <typename V>
-__device__ __forceinline__ Acc<V> acc_from(const Quad<V>& b) { return Acc<V>{b.mx, b.mn, b.cx, b.cn}; }
-template <typename V>
+__device__ __forceinline__ Acc<V> acc_from(const Quad<V>& b) { return Acc<V>{b.mx, b.mn, b.cx, b.cn, b.sx, b.sn}; }
+template <bool kSecond, typename V>
 __device__ __forceinline__ void acc_pair(Acc<V>& a, const Pair<V>& p, int base) {
+    if (kSecond) {
+        a.sx = max(max(a.sx, p.sx), min(a.mx, p.mx));
+        a.sn = min(min(a.sn, p.sn), max(a.mn, p.mn));
+    }
     const bool tx = p.mx >= a.mx;
     a.mx = tx ? p.mx : a.mx;
     a.rx = tx ? base + p.bx : a.rx;
@@ -133,8 +150,12 @@ __device__ __forceinline__ void acc_pair(Acc<V>& a, const Pair<V>& p, int base) 
     a.mn = tn ? p.mn : a.mn;
     a.rn = tn ? base + p.bn : a.rn;
 }
-template <typename V>
+template <bool kSecond, typename V>
 __device__ __forceinline__ void acc_leaf(Acc<V>& a, const Leaf<V>& l, int rank) {
+    if (kSecond) {
+        a.sx = max(a.sx, min(a.mx, l.mx));
+        a.sn = min(a.sn, max(a.mn, l.mn));
+    }
     const bool tx = l.mx >= a.mx;
     a.mx = tx ? l.mx : a.mx;
     a.rx = tx ? rank : a.rx;
@@ -142,8 +163,12 @@ __device__ __forceinline__ void acc_leaf(Acc<V>& a, const Leaf<V>& l, int rank) 
     a.mn = tn ? l.mn : a.mn;
     a.rn = tn ? rank : a.rn;
 }
-template <typename V>
+template <bool kSecond, typename V>
 __device__ __forceinline__ void acc_quad(Acc<V>& a, const Quad<V>& b, int base) {
+    if (kSecond) {
+        a.sx = max(max(a.sx, b.sx), min(a.mx, b.mx));
+        a.sn = min(min(a.sn, b.sn), max(a.mn, b.mn));
+    }
     const bool tx = b.mx >= a.mx;
     a.mx = tx ? b.mx : a.mx;
     a.rx = tx ? base + b.cx : a.rx;
@@ -164,7 +189,24 @@ __device__ __forceinline__ Scan acc_scan(const Acc<V>& a, V vc) {
     return s;
 }
 
+// Robustness of a centre (K0): the largest and the smallest member of its
+// closed 1-ring lead the runners-up by more than 2 xi (plus rounding slack).
+// Every g of the loop satisfies L <= g <= fhat with |f - fhat| <= xi, i.e.
+// f - xi <= g <= f + xi up to rounding, so such a centre's steepest ascent and
+// descent (and extremum flags) are those of f in every iteration: it can never
+// mismatch, its rules never fire, and no sweep needs to evaluate it.
+__device__ __forceinline__ double robust_margin(double xi, double v) {
+    return 2.0 * xi * (1.0 + 0x1p-40) + 0x1p-40 * fabs(v) + 0x1p-1000;
+}
+template <typename V>
+__device__ __forceinline__ bool acc_robust(const Acc<V>& a, V vc, double xi) {
+    const double mxc = (double)max(a.mx, vc), sxc = (double)max(a.sx, min(a.mx, vc));
+    const double mnc = (double)min(a.mn, vc), snc = (double)min(a.sn, max(a.mn, vc));
+    return (mxc - sxc > robust_margin(xi, mxc)) && (snc - mnc > robust_margin(xi, mnc));
+}
+
 __device__ __forceinline__ void count_kinds(const Dom& d, const Work& w, const Scan& s, uint8_t fcode) {
+    if (fcode == kRobust) return;
     const int fr = fcode & 15, fs = fcode >> 4;
     const bool fmax = fr == kExtremum, fmin = fs == kExtremum;
     if (s.is_max && !fmax) atomicAdd(&w.ctr->kinds[0], 1ull);
@@ -186,6 +228,7 @@ __device__ __forceinline__ void count_kinds(const Dom& d, const Work& w, const S
 // parameters so the plain full sweep carries none of their logic.
 template <bool kCount, bool kMasked = false, bool kExtrema = false>
 struct DetectOp {
+    static constexpr bool kSecond = false;
     Work w;
     const uint32_t* dirty;
     unsigned ndet;
@@ -201,13 +244,17 @@ struct DetectOp {
         if (!kMasked) return Pre{ld_nc_u8(w.code + c), 1u, 0u};
         return Pre{ld_nc_u8(w.code + c), ld_nc_u32(dirty + (c >> 5)), (uint32_t)(c & 31)};
     }
+    // robust centres (K0) never mismatch and are never evaluated
     __device__ __forceinline__ bool wants(const Pre& p) const {
-        if (!kMasked) return !(p.code & 0x100u);
-        return !(p.code & 0x100u) && ((p.word >> p.sh) & 1u);
+        if (!kMasked) return !(p.code & 0x100u) && p.code != kRobust;
+        return !(p.code & 0x100u) && p.code != kRobust && ((p.word >> p.sh) & 1u);
     }
     __device__ __forceinline__ bool skippable() const { return kMasked; }
-    __device__ __forceinline__ void center(const Dom& d, int64_t c, const Scan& s, const Pre& p) {
-        const uint8_t fc = (uint8_t)p.code;
+    __device__ __forceinline__ void center(const Dom& d, int64_t c, const Acc<double>& a, double vc, const Pre& p) {
+        evaluate(d, c, acc_scan(a, vc), (uint8_t)p.code);
+    }
+    // the g-scan s of centre c against its f-code fc
+    __device__ __forceinline__ void evaluate(const Dom& d, int64_t c, const Scan& s, uint8_t fc) {
         const uint8_t gc = scan_code(s);
         const bool mismatch = kExtrema ? (((gc & 15) == kExtremum) != ((fc & 15) == kExtremum) ||
                                           ((gc >> 4) == kExtremum) != ((fc >> 4) == kExtremum))
@@ -228,21 +275,24 @@ struct DetectOp {
 // K0: validate the pair (correction.py:52-60, hazard H6), build the f-code
 // (field_scan(original), correction.py:404) and copy g <- fhat (:405).
 struct PrepOp {
+    static constexpr bool kSecond = true;   // second extrema for the robustness test
     const double* fh;
     double* g;
     uint8_t* code;
+    uint32_t* frag;   // fragile bitmap (zeroed by the caller); null: robustness off
     DevCounters* ctr;
     double xi;
-    unsigned bound, floorv, upper, nonfin;
+    unsigned bound, floorv, upper, nonfin, nfrag;
     struct Pre {
         double hv;
     };
-    __device__ __forceinline__ void begin() { bound = floorv = upper = nonfin = 0; }
+    __device__ __forceinline__ void begin() { bound = floorv = upper = nonfin = nfrag = 0; }
     __device__ __forceinline__ Pre fetch(int64_t c, bool live) const { return Pre{live ? ld_nc_f64(fh + c) : 0.0}; }
     __device__ __forceinline__ bool wants(const Pre&) const { return true; }
     __device__ __forceinline__ bool skippable() const { return false; }
-    __device__ __forceinline__ void center(const Dom&, int64_t c, const Scan& s, const Pre& p) {
-        const double fv = s.vc;
+    template <typename V>
+    __device__ __forceinline__ void center(const Dom&, int64_t c, const Acc<V>& a, V vc, const Pre& p) {
+        const double fv = (double)vc;
         const double hv = p.hv;
         nonfin += (!isfinite(fv) || !isfinite(hv)) ? 1u : 0u;
         if (fabs(fv - hv) > xi) {
@@ -252,14 +302,34 @@ struct PrepOp {
         floorv += hv < fv - xi ? 1u : 0u;
         upper += hv > fv + xi ? 1u : 0u;
         if (g != fh) g[c] = hv;
-        code[c] = scan_code(s);
+        const bool robust = frag != nullptr && acc_robust(a, vc, xi);
+        code[c] = robust ? kRobust : scan_code(acc_scan(a, vc));
+        if (frag) {
+            // fragile bitmap: a full warp holds 32 consecutive ids of one row
+            // (lane = x - x0), i.e. at most two words -> two RED.OR by lane 0
+            nfrag += robust ? 0u : 1u;
+            const unsigned lane = threadIdx.x & 31;
+            if (__activemask() == 0xffffffffu) {
+                const unsigned bal = __ballot_sync(0xffffffffu, !robust);
+                const int64_t c0 = c - lane;
+                const unsigned sh = (unsigned)(c0 & 31);
+                if (lane == 0 && bal) {
+                    if (bal << sh) atomicOr(frag + (c0 >> 5), bal << sh);
+                    if (sh && (bal >> (32 - sh))) atomicOr(frag + (c0 >> 5) + 1, bal >> (32 - sh));
+                }
+            } else if (!robust) {
+                atomicOr(frag + (c >> 5), 1u << (c & 31));
+            }
+        }
     }
     __device__ __forceinline__ void finish() {
         const unsigned b = __reduce_add_sync(0xffffffffu, bound);
         const unsigned fl = __reduce_add_sync(0xffffffffu, floorv);
         const unsigned up = __reduce_add_sync(0xffffffffu, upper);
         const unsigned nf = __reduce_add_sync(0xffffffffu, nonfin);
+        const unsigned nfr = __reduce_add_sync(0xffffffffu, nfrag);
         if ((threadIdx.x & 31) == 0) {
+            if (nfr) atomicAdd(&ctr->nfragile, (unsigned long long)nfr);
             if (b) atomicAdd(&ctr->bound_viol, (unsigned long long)b);
             if (fl) atomicAdd(&ctr->floor_viol, (unsigned long long)fl);
             if (up) atomicAdd(&ctr->upper_viol, (unsigned long long)up);
@@ -280,7 +350,7 @@ struct PlaneOut {
     V fa, fb;                 // centre values at plane p
 };
 
-template <bool kEdge, typename V>
+template <bool kEdge, bool kSecond, typename V>
 __device__ __forceinline__ PlaneOut<V> plane_work(const V* __restrict__ s, int cell, bool mxl, bool mxr, bool myl,
                                                   bool myb, bool my2) {
     // column x-1: rows ya-1, ya, yb; column x: ya-1..ya+2; column x+1: ya..ya+2
@@ -303,10 +373,10 @@ __device__ __forceinline__ PlaneOut<V> plane_work(const V* __restrict__ s, int c
     const Pair<V> h4 = xpair(f, i);   // (x, ya)
     o.h5 = xpair(g, j);   // (x, yb)
     o.h6 = xpair(h, k);   // (x, ya+2)
-    o.ua = ybox(h4, o.h5);
-    o.ub = ybox(o.h5, o.h6);
-    o.da = ybox(o.h1, o.h2);
-    o.db = ybox(o.h2, h3);
+    o.ua = ybox<kSecond>(h4, o.h5);
+    o.ub = ybox<kSecond>(o.h5, o.h6);
+    o.da = ybox<kSecond>(o.h1, o.h2);
+    o.db = ybox<kSecond>(o.h2, h3);
     o.b = b; o.c = c; o.i = i; o.j = j;
     o.fa = fv;
     o.fb = gv;
@@ -314,22 +384,22 @@ __device__ __forceinline__ PlaneOut<V> plane_work(const V* __restrict__ s, int c
 }
 
 // Partial fold of the groups of ranks 0..9 (D, in-plane).
-template <typename V>
+template <bool kSecond, typename V>
 __device__ __forceinline__ Acc<V> partial_a(const Quad<V>& d, const PlaneOut<V>& o) {
     Acc<V> a = acc_from(d);
-    acc_pair(a, o.h1, 4);
-    acc_leaf(a, o.b, 6);
-    acc_leaf(a, o.i, 7);
-    acc_pair(a, o.h5, 8);
+    acc_pair<kSecond>(a, o.h1, 4);
+    acc_leaf<kSecond>(a, o.b, 6);
+    acc_leaf<kSecond>(a, o.i, 7);
+    acc_pair<kSecond>(a, o.h5, 8);
     return a;
 }
-template <typename V>
+template <bool kSecond, typename V>
 __device__ __forceinline__ Acc<V> partial_b(const Quad<V>& d, const PlaneOut<V>& o) {
     Acc<V> a = acc_from(d);
-    acc_pair(a, o.h2, 4);
-    acc_leaf(a, o.c, 6);
-    acc_leaf(a, o.j, 7);
-    acc_pair(a, o.h6, 8);
+    acc_pair<kSecond>(a, o.h2, 4);
+    acc_leaf<kSecond>(a, o.c, 6);
+    acc_leaf<kSecond>(a, o.j, 7);
+    acc_pair<kSecond>(a, o.h6, 8);
     return a;
 }
 
@@ -383,6 +453,7 @@ struct Stager {
 template <bool kEdge, typename T, class Op>
 __device__ __forceinline__ void tiled_body(const Dom& d, T (*sm)[kPlane], Stager<T>& st, Op& op, int64_t x0,
                                            int64_t y0, int64_t zb, int64_t ze) {
+    constexpr bool kSecond = Op::kSecond;
     const int tx = threadIdx.x, ty = threadIdx.y;
     const int64_t x = x0 + tx, ya = y0 + 2 * ty, yb = ya + 1;
     const int cell = (2 * ty + 1) * kPX + (tx + 1);
@@ -405,7 +476,7 @@ __device__ __forceinline__ void tiled_body(const Dom& d, T (*sm)[kPlane], Stager
     __syncthreads();
     Quad<T> da, db;
     if (zb - 1 >= 0) {
-        const PlaneOut<T> o = plane_work<kEdge>(sm[0], cell, mxl, mxr, myl, myb, my2);
+        const PlaneOut<T> o = plane_work<kEdge, kSecond>(sm[0], cell, mxl, mxr, myl, myb, my2);
         da = o.da;
         db = o.db;
     } else {
@@ -414,9 +485,9 @@ __device__ __forceinline__ void tiled_body(const Dom& d, T (*sm)[kPlane], Stager
     Acc<T> pa, pb;
     T fa, fb;
     {
-        const PlaneOut<T> o = plane_work<kEdge>(sm[1], cell, mxl, mxr, myl, myb, my2);
-        pa = partial_a(da, o);
-        pb = partial_b(db, o);
+        const PlaneOut<T> o = plane_work<kEdge, kSecond>(sm[1], cell, mxl, mxr, myl, myb, my2);
+        pa = partial_a<kSecond>(da, o);
+        pb = partial_b<kSecond>(db, o);
         da = o.da;
         db = o.db;
         fa = o.fa;
@@ -443,20 +514,20 @@ __device__ __forceinline__ void tiled_body(const Dom& d, T (*sm)[kPlane], Stager
             work = __any_sync(0xffffffffu, op.wants(pa0) || op.wants(pb0) || op.wants(pa1) || op.wants(pb1) ||
                                                op.wants(pa2) || op.wants(pb2));
         PlaneOut<T> o;
-        if (kUp && work) o = plane_work<kEdge>(sm[(k + 2) & (kSlots - 1)], cell, mxl, mxr, myl, myb, my2);
+        if (kUp && work) o = plane_work<kEdge, kSecond>(sm[(k + 2) & (kSlots - 1)], cell, mxl, mxr, myl, myb, my2);
         if (work && live_a && op.wants(pa0)) {
             Acc<T> a = pa;
-            if (kUp) acc_quad(a, o.ua, 10);
-            op.center(d, ca, acc_scan(a, fa), pa0);
+            if (kUp) acc_quad<kSecond>(a, o.ua, 10);
+            op.center(d, ca, a, fa, pa0);
         }
         if (work && live_b && op.wants(pb0)) {
             Acc<T> a = pb;
-            if (kUp) acc_quad(a, o.ub, 10);
-            op.center(d, ca + sy, acc_scan(a, fb), pb0);
+            if (kUp) acc_quad<kSecond>(a, o.ub, 10);
+            op.center(d, ca + sy, a, fb, pb0);
         }
         if (kUp && work) {
-            pa = partial_a(da, o);
-            pb = partial_b(db, o);
+            pa = partial_a<kSecond>(da, o);
+            pb = partial_b<kSecond>(db, o);
             da = o.da;
             db = o.db;
             fa = o.fa;
@@ -540,8 +611,8 @@ inline void launch_sweep_full(const Dom& d, const double* g, const Work& w, cuda
 }
 
 template <typename FT>
-inline void launch_prep(const Dom& d, const FT* f, const double* fh, double* g, uint8_t* code, DevCounters* ctr,
-                        cudaStream_t s) {
+inline void launch_prep(const Dom& d, const FT* f, const double* fh, double* g, uint8_t* code, uint32_t* frag,
+                        DevCounters* ctr, cudaStream_t s) {
     // K0 scans the whole domain (ghost layers included): the f-code of a block's
     // ext field is scan_neighbors(f_ext, ext_dims) (parallel.py:212).
     Dom all = d;
@@ -552,7 +623,7 @@ inline void launch_prep(const Dom& d, const FT* f, const double* fh, double* g, 
     dim3 grid;
     int zchunk;
     tiled_grid(all, grid, zchunk);
-    PrepOp op{fh, g, code, ctr, d.xi, 0, 0, 0, 0};
+    PrepOp op{fh, g, code, frag, ctr, d.xi, 0, 0, 0, 0, 0};
     k_tiled<FT, PrepOp><<<grid, dim3(kTX, kTY, 1), 0, s>>>(all, f, op, zchunk);
 }
 

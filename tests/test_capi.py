@@ -49,7 +49,7 @@ def test_structs_match_header_layout():
     import ctypes
     # pmsz_desc: 3 + 3 + 3 int64, 3 + 3 int32, 2 double, int64, 2 int32
     assert ctypes.sizeof(N.PmszDesc) == 9 * 8 + 6 * 4 + 2 * 8 + 8 + 2 * 4
-    assert ctypes.sizeof(N.PmszResult) == 20 * 8
+    assert ctypes.sizeof(N.PmszResult) == 21 * 8
 
 
 def test_no_cpu_fallback_without_device():

@@ -397,3 +397,50 @@ def test_extrema_only_peaks_at_scale_matches_oracle():
     assert ref.status == orc.ORC_OK
     assert out.edits_per_iteration == ref.edits_per_iteration
     assert np.array_equal(out.corrected.cpu().numpy(), ref.corrected)
+
+
+# --- robust-centre skipping and the TMA queue sweep ----------------------------
+@pytest.mark.parametrize("dims,f32", [((97, 64, 40), True), ((64, 72, 33), False), ((130, 34, 20), True),
+                                      ((48, 40, 36), False), ((32, 32, 70), True)])
+def test_ragged_shapes_match_oracle(dims, f32):
+    """Odd / non-multiple-of-16 extents exercise every staging path of the
+    detection sweeps (TMA f-code tiles, per-thread f-codes, cp.async fallback)
+    against the oracle, with K0's robust-centre classification on."""
+    spec = gen.NoiseSpec(dims, 11)
+    f = gen.perlin_device(spec, f32=f32)
+    xi = gen.relative_to_absolute_device(f, 1e-3)
+    fh = gen.quantize_device(f, xi)
+    cfg = pm.CorrectionConfig(xi_abs=xi)
+    out = pm.run_correction_device(f, fh, dims, cfg)
+    ref = orc.run_correction(dims, f.cpu().numpy().astype(np.float64), fh.cpu().numpy(), xi,
+                             check_segmentation=False)
+    assert ref.status == orc.ORC_OK
+    assert out.edits_per_iteration == ref.edits_per_iteration
+    assert np.array_equal(out.corrected.cpu().numpy(), ref.corrected)
+    assert 0 <= out.fragile <= dims[0] * dims[1] * dims[2]
+
+
+def test_robust_skipping_changes_nothing(monkeypatch):
+    """PMSZ_ROBUST=0 / PMSZ_QSWEEP=0 (every centre evaluated by the shared-fold
+    sweep) and the default (robust centres never evaluated, queue sweep) give
+    identical trajectories, fields and edit records."""
+    from paper_2601_01787_b200.engine import DomainPlan, DomainSpec
+    dims = (96, 80, 64)
+    f32 = gen.perlin_device(gen.NoiseSpec(dims, 4), f32=True)
+    xi = gen.relative_to_absolute_device(f32, 1e-4)
+    fh = gen.quantize_device(f32, xi)
+    cfg = pm.CorrectionConfig(xi_abs=xi)
+    outs = []
+    for env in ({}, {"PMSZ_ROBUST": "0", "PMSZ_QSWEEP": "0"}):
+        for k in ("PMSZ_ROBUST", "PMSZ_QSWEEP"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        plan = DomainPlan(DomainSpec.whole(dims), xi, cfg.tau, cfg.max_outer_iterations, f32_original=True)
+        outs.append(pm.run_correction_device(f32, fh, dims, cfg, plan=plan))
+        plan.close()
+    a, b = outs
+    assert a.fragile < b.fragile == dims[0] * dims[1] * dims[2]
+    assert a.edits_per_iteration == b.edits_per_iteration
+    assert torch.equal(a.corrected, b.corrected)
+    assert torch.equal(a.edit_ids, b.edit_ids) and torch.equal(a.edit_values, b.edit_values)
