@@ -29,6 +29,7 @@
 #include "tail.cuh"
 #include "gather.cuh"
 #include "qsweep.cuh"
+#include "prep.cuh"
 #include "segment.cuh"
 
 using namespace pmsz;
@@ -435,6 +436,7 @@ struct pmsz_plan {
     bool gather_on = true;                // masked iterations as sorted gathers (gather.cuh)
     bool robust_on = true;                // K0 classifies robust centres (never evaluated afterwards)
     bool qsweep_on = true;                // tiled sweeps evaluate a per-plane queue of fragile centres (qsweep.cuh)
+    bool qprep_on = true;                 // K0 as screen + queue (prep.cuh)
     uint32_t* frag = nullptr;             // fragile-centre bitmap written by K0
     // host-buffer entry point staging (pmsz_run_correction_host)
     uint32_t* frag_out() const { return robust_on ? frag : nullptr; }
@@ -832,10 +834,16 @@ pmsz_status prep(pmsz_plan* p, const void* f, const double* fh, double* g, cudaS
         ProfScope ps(p, s, PMSZ_K_PREP);
         p->w.frag = p->robust_on ? p->frag : nullptr;
         if (p->robust_on) CUDA_TRY(cudaMemsetAsync(p->frag, 0, p->nwords * 4, s));
-        if (p->f32)
-            launch_prep<float>(p->dom, (const float*)f, fh, g, p->w.code, p->frag_out(), p->ctr, s);
-        else
-            launch_prep<double>(p->dom, (const double*)f, fh, g, p->w.code, p->frag_out(), p->ctr, s);
+        bool queued = false;
+        if (p->qprep_on)
+            queued = p->f32 ? launch_prep_q<float>(p->dom, (const float*)f, fh, g, p->w.code, p->frag_out(), p->ctr, s)
+                            : launch_prep_q<double>(p->dom, (const double*)f, fh, g, p->w.code, p->frag_out(), p->ctr, s);
+        if (!queued) {
+            if (p->f32)
+                launch_prep<float>(p->dom, (const float*)f, fh, g, p->w.code, p->frag_out(), p->ctr, s);
+            else
+                launch_prep<double>(p->dom, (const double*)f, fh, g, p->w.code, p->frag_out(), p->ctr, s);
+        }
         LAUNCHED();
     }
     CUDA_TRY(cudaGetLastError());
@@ -1023,6 +1031,7 @@ pmsz_status pmsz_plan_create(const pmsz_desc* desc, pmsz_plan** out) {
     if (const char* e = getenv("PMSZ_SWEEP")) p->gather_on = strcmp(e, "tiled") != 0;
     if (const char* e = getenv("PMSZ_ROBUST")) p->robust_on = atoi(e) != 0;
     if (const char* e = getenv("PMSZ_QSWEEP")) p->qsweep_on = atoi(e) != 0;
+    if (const char* e = getenv("PMSZ_QPREP")) p->qprep_on = atoi(e) != 0;
     if (cudaFuncSetAttribute(k_gather<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGatherSmem) !=
             cudaSuccess ||
         cudaFuncSetAttribute(k_gather<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGatherSmem) !=
