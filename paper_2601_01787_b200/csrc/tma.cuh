@@ -6,9 +6,11 @@
 // column (its halo included) with ONE instruction issued by one thread; cells
 // outside the field are filled with NaN by the TMA unit (OOB fill), which is
 // exactly the "missing neighbour" encoding of fold_scan (common.cuh).
-// Restriction of the hardware: every global stride (nx * elem, nx * ny * elem
-// bytes) must be a multiple of 16; plans whose field does not qualify use the
-// cp.async stager of tiles.cuh.
+// Restrictions of the hardware: every global stride (nx * elem, nx * ny * elem
+// bytes) must be a multiple of 16 (plans whose field does not qualify use the
+// cp.async stager of tiles.cuh), and the innermost box origin must be 16-byte
+// aligned -- an odd x origin of an f64 box is an illegal instruction, so the
+// boxes start at the even (f64) / multiple-of-4 (f32) column left of x0 - 1.
 #pragma once
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -78,13 +80,16 @@ __device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier
 __device__ __forceinline__ void mbar_expect_tx(unsigned bar, unsigned bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
 }
+// Wait for the phase with `parity` to complete.  The suspend-time hint lets
+// the hardware park the warp until the phase flips instead of spinning (a
+// spinning producer or consumer would steal issue slots from the others).
 __device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
     unsigned done;
     do {
         asm volatile(
-            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}\n"
             : "=r"(done)
-            : "r"(bar), "r"(parity)
+            : "r"(bar), "r"(parity), "r"(0x989680u)
             : "memory");
     } while (!done);
 }
