@@ -437,6 +437,8 @@ struct pmsz_plan {
     bool robust_on = true;                // K0 classifies robust centres (never evaluated afterwards)
     bool qsweep_on = true;                // tiled sweeps evaluate a per-plane queue of fragile centres (qsweep.cuh)
     bool qprep_on = true;                 // K0 as screen + queue (prep.cuh)
+    bool fuse_on = true;                  // K0 also runs the first detection sweep (prep.cuh)
+    bool k0_detected = false;             // detbits / ndetect of the first iteration come from K0
     uint32_t* frag = nullptr;             // fragile-centre bitmap written by K0
     // host-buffer entry point staging (pmsz_run_correction_host)
     uint32_t* frag_out() const { return robust_on ? frag : nullptr; }
@@ -605,10 +607,14 @@ pmsz_status choose_next(pmsz_plan* p, cudaStream_t s, bool marked_bits, int64_t 
 pmsz_status iterate_once(pmsz_plan* p, const void* f, double* g, cudaStream_t s) {
     const int nxt = p->cur ^ 1;
     p->edits_cached = -1;
-    pmsz_status st = reset_iter(p, s, nxt);
-    if (st) return st;
     const Dom& d = p->dom;
     const int mode = p->w.incremental ? p->next_mode : kFull;
+    // the first full sweep ran inside K0 (detbits and ndetect are set; every
+    // other per-iteration counter is still zero from reset_run_state)
+    const bool predetected = mode == kFull && p->k0_detected;
+    p->k0_detected = false;
+    pmsz_status st = predetected ? PMSZ_OK : reset_iter(p, s, nxt);
+    if (st) return st;
     const int64_t cx = d.hi[0] - d.lo[0], cy = d.hi[1] - d.lo[1], cz = d.hi[2] - d.lo[2];
     const bool nonempty = cx > 0 && cy > 0 && cz > 0;
     int64_t apply_bound = p->n;   // upper bound of the targets, sizes the apply grid
@@ -616,9 +622,9 @@ pmsz_status iterate_once(pmsz_plan* p, const void* f, double* g, cudaStream_t s)
     if (mode != kList) p->bits_only = false;   // actbits is consumed (compacted or cleared) below
     if (mode == kFull) {
         if (p->w.incremental) CUDA_TRY(cudaMemsetAsync(p->w.actbits, 0, p->nwords * 4, s));
-        CUDA_TRY(cudaMemsetAsync(p->w.detbits, 0, p->nwords * 4, s));
+        if (!predetected) CUDA_TRY(cudaMemsetAsync(p->w.detbits, 0, p->nwords * 4, s));
         p->w.track = 0;
-        if (nonempty) {
+        if (nonempty && !predetected) {
             ProfScope ps(p, s, PMSZ_K_SWEEP_FULL);
             if (!(p->qsweep_on && launch_sweep_q<false>(d, g, p->w, s))) launch_sweep_full<false>(d, g, p->w, s);
             LAUNCHED();
@@ -834,10 +840,14 @@ pmsz_status prep(pmsz_plan* p, const void* f, const double* fh, double* g, cudaS
         ProfScope ps(p, s, PMSZ_K_PREP);
         p->w.frag = p->robust_on ? p->frag : nullptr;
         if (p->robust_on) CUDA_TRY(cudaMemsetAsync(p->frag, 0, p->nwords * 4, s));
+        // K0 also runs the first detection sweep (g = fhat) unless told otherwise
+        uint32_t* det = p->fuse_on ? p->w.detbits : nullptr;
+        if (det) CUDA_TRY(cudaMemsetAsync(det, 0, p->nwords * 4, s));
         bool queued = false;
         if (p->qprep_on)
-            queued = p->f32 ? launch_prep_q<float>(p->dom, (const float*)f, fh, g, p->w.code, p->frag_out(), p->ctr, s)
-                            : launch_prep_q<double>(p->dom, (const double*)f, fh, g, p->w.code, p->frag_out(), p->ctr, s);
+            queued = p->f32 ? launch_prep_q<float>(p->dom, (const float*)f, fh, g, p->w.code, p->frag_out(), p->ctr, det, s)
+                            : launch_prep_q<double>(p->dom, (const double*)f, fh, g, p->w.code, p->frag_out(), p->ctr, det, s);
+        p->k0_detected = queued && det != nullptr;
         if (!queued) {
             if (p->f32)
                 launch_prep<float>(p->dom, (const float*)f, fh, g, p->w.code, p->frag_out(), p->ctr, s);
@@ -1032,6 +1042,7 @@ pmsz_status pmsz_plan_create(const pmsz_desc* desc, pmsz_plan** out) {
     if (const char* e = getenv("PMSZ_ROBUST")) p->robust_on = atoi(e) != 0;
     if (const char* e = getenv("PMSZ_QSWEEP")) p->qsweep_on = atoi(e) != 0;
     if (const char* e = getenv("PMSZ_QPREP")) p->qprep_on = atoi(e) != 0;
+    if (const char* e = getenv("PMSZ_FUSE")) p->fuse_on = atoi(e) != 0;
     if (cudaFuncSetAttribute(k_gather<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGatherSmem) !=
             cudaSuccess ||
         cudaFuncSetAttribute(k_gather<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGatherSmem) !=
@@ -1173,6 +1184,7 @@ pmsz_status pmsz_block_round(pmsz_plan* p, const void* f, double* g, int32_t loc
 pmsz_status pmsz_mark_all_dirty(pmsz_plan* p, void* stream) {
     (void)stream;
     if (!p) return fail(PMSZ_ERR_INVALID, "null plan");
+    p->k0_detected = false;   // g may change before the first iteration: K0's detections are stale
     p->next_mode = kFull;
     return PMSZ_OK;
 }
@@ -1199,6 +1211,7 @@ static pmsz_status after_mark(pmsz_plan* p, cudaStream_t s) {
 
 pmsz_status pmsz_mark_dirty_ids(pmsz_plan* p, const uint32_t* ids, int64_t count, void* stream) {
     if (!p) return fail(PMSZ_ERR_INVALID, "null plan");
+    p->k0_detected = false;   // g may change before the first iteration: K0's detections are stale
     if (!p->w.incremental || p->next_mode == kFull || count <= 0) return PMSZ_OK;
     cudaStream_t s = S(stream);
     k_mark_ids<<<grid_for(count, 256), 256, 0, s>>>(p->dom, p->w, ids, count, p->cur, p->next_mode == kMasked);
@@ -1209,6 +1222,7 @@ pmsz_status pmsz_mark_dirty_ids(pmsz_plan* p, const uint32_t* ids, int64_t count
 pmsz_status pmsz_box_mark_changed(pmsz_plan* p, const int64_t lo[3], const int64_t hi[3], const double* before,
                                   const double* g, void* stream) {
     if (!p) return fail(PMSZ_ERR_INVALID, "null plan");
+    p->k0_detected = false;   // g may change before the first iteration: K0's detections are stale
     if (!p->w.incremental || p->next_mode == kFull) return PMSZ_OK;
     cudaStream_t s = S(stream);
     Box b{p->dom.nx, p->dom.ny, {lo[0], lo[1], lo[2]}, {hi[0] - lo[0], hi[1] - lo[1], hi[2] - lo[2]}};
@@ -1224,6 +1238,7 @@ static bool make_box(int64_t nx, int64_t ny, int64_t nz, const int64_t lo[3], co
 pmsz_status pmsz_box_merge_min(pmsz_plan* p, double* g, const int64_t lo[3], const int64_t hi[3], const double* buf,
                                int64_t* changed_out, void* stream) {
     if (!p || !g || !buf) return fail(PMSZ_ERR_INVALID, "null argument");
+    p->k0_detected = false;   // g may change before the first iteration: K0's detections are stale
     cudaStream_t s = S(stream);
     Box b;
     if (!make_box(p->dom.nx, p->dom.ny, p->dom.nz, lo, hi, b)) return fail(PMSZ_ERR_INVALID, "box outside the domain");

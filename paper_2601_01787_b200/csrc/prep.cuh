@@ -143,14 +143,14 @@ template <typename T> struct PrepGeo {
     static constexpr int kPY = kQY + 2;
     static constexpr int kPlane = kPX * kPY;
     static constexpr int kStride = ((kPlane * (int)sizeof(T) + 127) / 128) * 128 / (int)sizeof(T);
-    static constexpr int kSlots = 6;   // planes in use k-1 .. k+2, two more in flight
-    static constexpr int kHSlots = 3;  // fhat tiles
+    static constexpr int kSlots = 5;   // f planes in use k-1 .. k+2, one more in flight
+    static constexpr int kHSlots = 4;  // fhat planes (with halo) in use k-1 .. k+1, one more in flight
 };
 template <typename T>
 struct PrepSmem {
     using G = PrepGeo<T>;
     T plane[G::kSlots][G::kStride];
-    double fh[G::kHSlots][kQX * kQY];
+    double fh[G::kHSlots][kQPlaneStride];   // fhat = g of iteration 1, staged like qsweep.cuh
     uint16_t queue[2][kQX * kQY];   // code-tile index (row * 32 + x) of fragile centres
     unsigned long long bar[G::kSlots];
     unsigned long long hbar[G::kHSlots];
@@ -165,6 +165,11 @@ struct PrepArgs {
     double xi;
     double thr;         // RU(2 xi (1 + 2^-30)) in the field's precision (f32 fields: rounded up)
     int frag_direct;    // nx % 32 == 0: a warp's ballot is exactly one bitmap word
+    // fused first detection sweep (g = fhat): the fragile centres of the core
+    // box are compared with their f-code right here (null: not fused)
+    uint32_t* det;
+    int extrema_only;
+    int64_t core_lo[3], core_hi[3];
 };
 
 template <typename FT>
@@ -184,7 +189,9 @@ __global__ void __launch_bounds__(256, sizeof(FT) == 4 ? 3 : 2) k_prep_q(Dom d, 
     const int xo = (int)(x0 - 1 - xs);   // column of x0 - 1 in a staged row
     const unsigned bar0 = smem_u32(&S.bar[0]), hbar0 = smem_u32(&S.hbar[0]);
     const unsigned pl0 = smem_u32(&S.plane[0][0]), fh0 = smem_u32(&S.fh[0][0]);
-    // f plane index i = p - (zb - 1), i in [0, K + 1]; fhat tile j = centre plane zb + j
+    // plane index i = p - (zb - 1), i in [0, K + 1], for f and fhat alike
+    const int64_t xh = (x0 - 1) & ~int64_t(1);   // fhat boxes (f64): even origin
+    const int xho = (int)(x0 - 1 - xh);
     auto issue = [&](int i) {
         const int s = i % G::kSlots;
         mbar_expect_tx(bar0 + 8 * s, G::kPlane * (unsigned)sizeof(FT));
@@ -193,8 +200,8 @@ __global__ void __launch_bounds__(256, sizeof(FT) == 4 ? 3 : 2) k_prep_q(Dom d, 
     };
     auto issue_h = [&](int j) {
         const int s = j % G::kHSlots;
-        mbar_expect_tx(hbar0 + 8 * s, kQX * kQY * 8);
-        tma_load_3d(fh0 + s * kQX * kQY * 8, &th, (int)x0, (int)y0, (int)(zb + j), hbar0 + 8 * s);
+        mbar_expect_tx(hbar0 + 8 * s, kQPlane * 8);
+        tma_load_3d(fh0 + s * kQPlaneStride * 8, &th, (int)xh, (int)(y0 - 1), (int)(zb - 1 + j), hbar0 + 8 * s);
     };
     auto wait_plane = [&](int i) { mbar_wait(bar0 + 8 * (i % G::kSlots), (unsigned)((i / G::kSlots) & 1)); };
     auto wait_h = [&](int j) { mbar_wait(hbar0 + 8 * (j % G::kHSlots), (unsigned)((j / G::kHSlots) & 1)); };
@@ -203,8 +210,8 @@ __global__ void __launch_bounds__(256, sizeof(FT) == 4 ? 3 : 2) k_prep_q(Dom d, 
         for (int s = 0; s < G::kHSlots; ++s) mbar_init(hbar0 + 8 * s, 1);
         mbar_fence_init();
         S.cnt[0] = S.cnt[1] = S.cnt[2] = 0;
-        for (int i = 0; i <= 3 && i <= K + 1; ++i) issue(i);
-        for (int j = 0; j < 2 && j < K; ++j) issue_h(j);
+        for (int i = 0; i <= 2 && i <= K + 1; ++i) issue(i);
+        for (int j = 0; j <= 1 && j <= K + 1; ++j) issue_h(j);
     }
     const int64_t x = x0 + tx, yr = y0 + kQRowsPerThread * ty;
     const bool live_x = x < d.nx;
@@ -214,7 +221,7 @@ __global__ void __launch_bounds__(256, sizeof(FT) == 4 ? 3 : 2) k_prep_q(Dom d, 
     const uint32_t c0 = (uint32_t)(x + yr * (int64_t)sy + zb * (int64_t)sz);   // row-0 centre at plane zb
     const int col = xo + tx;                 // staged column of x - 1
     const int row0 = kQRowsPerThread * ty;   // staged row of y_0 - 1
-    unsigned nbound = 0, nfloor = 0, nupper = 0, nnonfin = 0, nfrag = 0;
+    unsigned nbound = 0, nfloor = 0, nupper = 0, nnonfin = 0, nfrag = 0, ndet = 0;
     using V = FT;
 
     // Plane p's shared groups for this thread's four centres, streamed row by
@@ -245,6 +252,7 @@ __global__ void __launch_bounds__(256, sizeof(FT) == 4 ? 3 : 2) k_prep_q(Dom d, 
     T2<V> lbprev[kQRowsPerThread], acc[kQRowsPerThread];
     wait_plane(0);
     wait_plane(1);
+    wait_h(0);
     plane_groups(S.plane[0], [&](int r, const T2<V>& lb, const T2<V>&, const P2<V>&, V) { lbprev[r] = lb; });
     plane_groups(S.plane[1], [&](int r, const T2<V>& lb, const T2<V>&, const P2<V>& rp, V leaf) {
         acc[r] = lbprev[r];
@@ -256,19 +264,17 @@ __global__ void __launch_bounds__(256, sizeof(FT) == 4 ? 3 : 2) k_prep_q(Dom d, 
     for (int k = 0; k <= K; ++k) {
         // step k: finalise + enqueue centre plane zb + k (needs f plane index k + 2),
         //         exact codes of the queue of plane zb + k - 1 (indices k - 1 .. k + 1)
-        if (k < K) {
-            wait_plane(k + 2);
-            wait_h(k);
-        }
+        if (k < K) wait_plane(k + 2);
+        wait_h(k + 1);
         __syncthreads();
         if (tid == 0) {
-            if (k + 4 <= K + 1) issue(k + 4);
-            if (k + 2 < K) issue_h(k + 2);
+            if (k + 3 <= K + 1) issue(k + 3);
+            if (k + 2 <= K + 1) issue_h(k + 2);
             S.cnt[(k + 1) % 3] = 0;
         }
         if (k < K) {
             const V* ctr_plane = S.plane[(k + 1) % G::kSlots];
-            const double* fht = S.fh[k % G::kHSlots];
+            const double* fht = S.fh[(k + 1) % G::kHSlots] + kQPX + xho + 1 + tx;   // fhat at (x, y_0 - 1)
             const uint32_t cz = c0 + (uint32_t)k * sz;
             bool want[kQRowsPerThread];
             plane_groups(S.plane[(k + 2) % G::kSlots],
@@ -280,7 +286,7 @@ __global__ void __launch_bounds__(256, sizeof(FT) == 4 ? 3 : 2) k_prep_q(Dom d, 
                 if (live[r]) {
                     // validation (correction.py:52-60), hazard H6, g <- fhat
                     const double fv = (double)ctr_plane[(row0 + r + 1) * G::kPX + col + 1];
-                    const double hv = fht[(row0 + r) * kQX + tx];
+                    const double hv = fht[(row0 + r) * kQPX];
                     nnonfin += (!isfinite(fv) || !isfinite(hv)) ? 1u : 0u;
                     if (fabs(fv - hv) > a.xi) {
                         ++nbound;
@@ -301,7 +307,7 @@ __global__ void __launch_bounds__(256, sizeof(FT) == 4 ? 3 : 2) k_prep_q(Dom d, 
             if (a.g != nullptr) {
 #pragma unroll
                 for (int r = 0; r < kQRowsPerThread; ++r)
-                    if (live[r]) a.g[cz + r * sy] = fht[(row0 + r) * kQX + tx];
+                    if (live[r]) a.g[cz + r * sy] = fht[(row0 + r) * kQPX];
             }
             // fragile bitmap and queue
             unsigned bal[kQRowsPerThread], tot = 0;
@@ -354,7 +360,28 @@ __global__ void __launch_bounds__(256, sizeof(FT) == 4 ? 3 : 2) k_prep_q(Dom d, 
                 nv[8] = ct[cell + G::kPX]; nv[9] = ct[cell + G::kPX + 1];
                 nv[10] = up[cell]; nv[11] = up[cell + 1]; nv[12] = up[cell + G::kPX]; nv[13] = up[cell + G::kPX + 1];
                 const V vc = ct[cell];
-                a.code[cpl + ly * sy + lx] = edge ? fold_code<V>(vc, nv) : tree_code<V>(vc, nv);
+                const uint8_t fc = edge ? fold_code<V>(vc, nv) : tree_code<V>(vc, nv);
+                const uint32_t c = cpl + ly * sy + lx;
+                a.code[c] = fc;
+                if (a.det != nullptr) {
+                    // the first detection sweep (g = fhat) of this centre
+                    const int64_t gx = x0 + lx, gy = y0 + ly;
+                    if (gx >= a.core_lo[0] && gx < a.core_hi[0] && gy >= a.core_lo[1] && gy < a.core_hi[1] &&
+                        zc >= a.core_lo[2] && zc < a.core_hi[2]) {
+                        double hv[14], hc;
+                        ring_from_smem(S.fh[(k - 1) % G::kHSlots], S.fh[k % G::kHSlots], S.fh[(k + 1) % G::kHSlots],
+                                       (ly + 1) * kQPX + xho + 1 + lx, hv, hc);
+                        const uint8_t gc = scan_code(edge ? fold_scan(hc, hv) : tree_scan(hc, hv));
+                        const bool mismatch = a.extrema_only
+                                                  ? (((gc & 15) == kExtremum) != ((fc & 15) == kExtremum) ||
+                                                     ((gc >> 4) == kExtremum) != ((fc >> 4) == kExtremum))
+                                                  : gc != fc;
+                        if (mismatch) {
+                            atomicOr(a.det + (c >> 5), 1u << (c & 31));
+                            ++ndet;
+                        }
+                    }
+                }
             }
         }
     }
@@ -363,7 +390,9 @@ __global__ void __launch_bounds__(256, sizeof(FT) == 4 ? 3 : 2) k_prep_q(Dom d, 
     const unsigned up = __reduce_add_sync(0xffffffffu, nupper);
     const unsigned nf = __reduce_add_sync(0xffffffffu, nnonfin);
     const unsigned nfr = __reduce_add_sync(0xffffffffu, nfrag);
+    const unsigned nd = __reduce_add_sync(0xffffffffu, ndet);
     if (lane == 0) {
+        if (nd) atomicAdd(&a.ctr->ndetect, (unsigned long long)nd);
         if (b) atomicAdd(&a.ctr->bound_viol, (unsigned long long)b);
         if (fl) atomicAdd(&a.ctr->floor_viol, (unsigned long long)fl);
         if (up) atomicAdd(&a.ctr->upper_viol, (unsigned long long)up);
@@ -378,11 +407,11 @@ __global__ void __launch_bounds__(256, sizeof(FT) == 4 ? 3 : 2) k_prep_q(Dom d, 
 // the shared-fold K0 of tiles.cuh).
 template <typename FT>
 inline bool launch_prep_q(const Dom& d, const FT* f, const double* fh, double* g, uint8_t* code, uint32_t* frag,
-                          DevCounters* ctr, cudaStream_t s) {
+                          DevCounters* ctr, uint32_t* det, cudaStream_t s) {
     using G = PrepGeo<FT>;
     CUtensorMap tf, th;
     if (!tma_field_map(&tf, f, sizeof(FT) == 4, d.nx, d.ny, d.nz, G::kPX, G::kPY)) return false;
-    if (!tma_field_map(&th, fh, false, d.nx, d.ny, d.nz, kQX, kQY)) return false;
+    if (!tma_field_map(&th, fh, false, d.nx, d.ny, d.nz, kQPX, kQPY)) return false;
     static bool attr = false;
     if (!attr)
         attr = cudaFuncSetAttribute(k_prep_q<FT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -402,6 +431,9 @@ inline bool launch_prep_q(const Dom& d, const FT* f, const double* fh, double* g
         a.thr = nextafter(t, INFINITY);
     }
     a.frag_direct = (d.nx % 32) == 0;
+    a.det = det;
+    a.extrema_only = d.extrema_only;
+    for (int ax = 0; ax < 3; ++ax) { a.core_lo[ax] = d.lo[ax]; a.core_hi[ax] = d.hi[ax]; }
     Dom all = d;
     for (int ax = 0; ax < 3; ++ax) all.lo[ax] = 0;
     all.hi[0] = d.nx; all.hi[1] = d.ny; all.hi[2] = d.nz;

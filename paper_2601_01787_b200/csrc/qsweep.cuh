@@ -84,6 +84,16 @@ constexpr int kQX = 32, kQY = 32, kQRowsPerThread = 4;
 // x0 - 1 - (x0 - 1 odd) .. + 35 (36 f64 = 288 B), the halo column x0 - 1 at xo.
 constexpr int kQPX = kQX + 4, kQPY = kQY + 2, kQPlane = kQPX * kQPY;   // 36 x 34
 constexpr int kQPlaneStride = ((kQPlane * 8 + 127) / 128) * 128 / 8;   // doubles, 128-B aligned slots
+// Closed ring of the staged cell `cell` (kQPX-wide rows) of planes dn / ct / up.
+__device__ __forceinline__ void ring_from_smem(const double* dn, const double* ct, const double* up, int cell,
+                                               double (&nv)[14], double& vc) {
+    nv[0] = dn[cell - kQPX - 1]; nv[1] = dn[cell - kQPX]; nv[2] = dn[cell - 1]; nv[3] = dn[cell];
+    nv[4] = ct[cell - kQPX - 1]; nv[5] = ct[cell - kQPX]; nv[6] = ct[cell - 1]; nv[7] = ct[cell + 1];
+    nv[8] = ct[cell + kQPX]; nv[9] = ct[cell + kQPX + 1];
+    nv[10] = up[cell]; nv[11] = up[cell + 1]; nv[12] = up[cell + kQPX]; nv[13] = up[cell + kQPX + 1];
+    vc = ct[cell];
+}
+
 constexpr int kQSlots = 6;
 constexpr int kQConsumers = kQY / kQRowsPerThread;   // consumer warps (4 rows x 32 columns each)
 constexpr int kQThreads = (kQConsumers + 1) * 32;     // + one producer warp
@@ -223,12 +233,8 @@ __global__ void __launch_bounds__(kQThreads, 3) k_qsweep_tma(Dom d, const __grid
             const uint32_t ent = q[e];
             const int r = (int)((ent & 0xffffu) >> 5), lx = (int)(ent & 31u);
             const int cell = (kQRowsPerThread * ty + r + 1) * kQPX + xo + 1 + lx;
-            double nv[14];
-            nv[0] = dn[cell - kQPX - 1]; nv[1] = dn[cell - kQPX]; nv[2] = dn[cell - 1]; nv[3] = dn[cell];
-            nv[4] = ct[cell - kQPX - 1]; nv[5] = ct[cell - kQPX]; nv[6] = ct[cell - 1]; nv[7] = ct[cell + 1];
-            nv[8] = ct[cell + kQPX]; nv[9] = ct[cell + kQPX + 1];
-            nv[10] = up[cell]; nv[11] = up[cell + 1]; nv[12] = up[cell + kQPX]; nv[13] = up[cell + kQPX + 1];
-            const double vc = ct[cell];
+            double nv[14], vc;
+            ring_from_smem(dn, ct, up, cell, nv, vc);
             const Scan s = interior ? tree_scan(vc, nv) : fold_scan(vc, nv);   // NaN = outside the field
             op.evaluate(d, (int64_t)(cpl + (uint32_t)r * sy32 + (uint32_t)lx), s, (uint8_t)(ent >> 16));
         }
