@@ -283,16 +283,22 @@ def run_ours_single(args):
             gbs = per_voxel[name] * nvox / (kms / cnt / 1e3) / 1e9
             entry.update({"bytes_per_launch": per_voxel[name] * nvox, "achieved_gbs": gbs, "frac": gbs / peak})
         kernels[name] = entry
+    # the roofline object describes the full-domain kernel with the largest
+    # share of the step (K0 since it absorbed the first detection sweep)
     dominant = max((k for k in kernels if k in per_voxel), key=lambda k: kernels[k]["ms_total_per_step"])
-    dk = kernels["sweep_full"] if "sweep_full" in kernels else kernels[dominant]
-    roofline = {"bound": "hbm", "kernel": "sweep_full (K1 detect+propose, full domain)",
+    dk = kernels[dominant]
+    what = {"prep": "K0 k_prep_q (validation, g <- fhat, robust screen; exact f-codes and the first detection "
+                    "sweep for the fragile centres)",
+            "sweep_full": "K1 k_qsweep_tma (full detection sweep over the fragile centres)",
+            "verify": "K4 count sweep"}
+    roofline = {"bound": "hbm", "kernel": what.get(dominant, dominant),
                 "achieved": dk["achieved_gbs"], "peak": peak, "unit": "GB/s", "frac": dk["achieved_gbs"] / peak,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)" if not peaks.get("fallback")
                 else "fallback 6650 GB/s", "traffic": None,
                 "traffic_source": None,
-                "bytes_per_voxel": 9, "per_kernel": kernels}
+                "bytes_per_voxel": per_voxel[dominant], "per_kernel": kernels}
 
-    tr = ncu_traffic("sweep_full", wl["label"])
+    tr = ncu_traffic(dominant, wl["label"])
     if tr is not None:
         roofline["traffic"] = tr[0]
         roofline["traffic_source"] = f"profiles/{tr[1]} (dram__bytes_read+write per launch, ncu --set full)"
