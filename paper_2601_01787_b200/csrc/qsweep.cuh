@@ -100,7 +100,7 @@ constexpr int kQThreads = (kQConsumers + 1) * 32;     // + one producer warp
 struct QSmem {
     double plane[kQSlots][kQPlaneStride];
     uint8_t code[kQSlots][kQX * kQY];                  // f-code tiles (kCodeTma)
-    uint32_t queue[kQConsumers][kQRowsPerThread * 32]; // per-warp queue: tile index | f-code << 16
+    uint32_t queue[kQConsumers][kQRowsPerThread * 32 + 32];   // per-warp queue: tile index | f-code << 16 | plane bit << 24
     unsigned long long full[kQSlots];                  // TMA landed
     unsigned long long empty[kQSlots];                 // every consumer warp is done with the slot
 };
@@ -187,6 +187,12 @@ __global__ void __launch_bounds__(kQThreads, 3) k_qsweep_tma(Dom d, const __grid
     }
     uint32_t* q = S.queue[ty];
     const unsigned below = (1u << lane) - 1u;
+    // Carry-over: a step evaluates only whole batches of 32 queued centres;
+    // the (< 32) leftovers of plane zb + k wait for step k + 1 (entry bit 24
+    // marks them), so the lanes stay busy although a warp queues only ~26
+    // fragile centres per plane.  A carried entry needs planes k .. k + 2 one
+    // step longer: a warp releases index k - 1 after step k.
+    unsigned carry = 0;
     wait_plane(0);
     wait_plane(1);
     for (int k = 0; k < K; ++k) {
@@ -215,31 +221,46 @@ __global__ void __launch_bounds__(kQThreads, 3) k_qsweep_tma(Dom d, const __grid
                 p1[r] = p2[r];
             }
         }
-        unsigned n = 0;
+        // q[0 .. carry) holds plane k - 1's leftovers; append plane k behind them
+        unsigned n = carry;
 #pragma unroll
         for (int r = 0; r < kQRowsPerThread; ++r) {
             const unsigned bal = __ballot_sync(0xffffffffu, want[r]);
-            if (want[r]) q[n + __popc(bal & below)] = (uint32_t)(r * kQX + tx) | (code[r] << 16);
+            if (want[r]) q[n + __popc(bal & below)] = (uint32_t)(r * kQX + tx) | (code[r] << 16) | (1u << 24);
             n += __popc(bal);
         }
         __syncwarp();
-        const double* dn = S.plane[k % kQSlots];
-        const double* ct = S.plane[(k + 1) % kQSlots];
-        const double* up = S.plane[(k + 2) % kQSlots];
+        // whole batches (they include every carried entry: carry < 32); a short
+        // queue waits for the next plane unless it holds carried entries; all at the end
+        const unsigned m = (k == K - 1) ? n : (n >= 32 ? (n & ~31u) : (carry ? n : 0u));
         const int64_t zc = zb + k;
-        const bool interior = !edge_xy && zc >= 1 && zc + 1 < d.nz;
+        const bool int_cur = !edge_xy && zc >= 1 && zc + 1 < d.nz;
+        const bool int_prev = !edge_xy && zc - 1 >= 1 && zc < d.nz;
         const uint32_t cpl = ctile + (uint32_t)(kQRowsPerThread * ty) * sy32 + (uint32_t)k * sz32;
-        for (unsigned e = lane; e < n; e += 32) {
+        for (unsigned e = lane; e < m; e += 32) {
             const uint32_t ent = q[e];
+            const int cur = (int)((ent >> 24) & 1u);   // 1: plane k, 0: carried from plane k - 1
+            const int base = k - 1 + cur;               // plane index of the entry's z - 1
             const int r = (int)((ent & 0xffffu) >> 5), lx = (int)(ent & 31u);
             const int cell = (kQRowsPerThread * ty + r + 1) * kQPX + xo + 1 + lx;
             double nv[14], vc;
-            ring_from_smem(dn, ct, up, cell, nv, vc);
+            ring_from_smem(S.plane[base % kQSlots], S.plane[(base + 1) % kQSlots], S.plane[(base + 2) % kQSlots], cell,
+                           nv, vc);
+            const bool interior = cur ? int_cur : int_prev;
             const Scan s = interior ? tree_scan(vc, nv) : fold_scan(vc, nv);   // NaN = outside the field
-            op.evaluate(d, (int64_t)(cpl + (uint32_t)r * sy32 + (uint32_t)lx), s, (uint8_t)(ent >> 16));
+            op.evaluate(d, (int64_t)(cpl - (cur ? 0u : sz32) + (uint32_t)r * sy32 + (uint32_t)lx), s,
+                        (uint8_t)(ent >> 16));
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(empty0 + 8 * (k % kQSlots));   // index k is no longer needed
+        // leftovers of plane k move to the front, marked as carried
+        const unsigned left = n - m;
+        uint32_t mv = 0;
+        if (lane < left) mv = q[m + lane] & ~(1u << 24);
+        __syncwarp();
+        if (lane < left) q[lane] = mv;
+        carry = left;
+        __syncwarp();
+        if (lane == 0 && k >= 1) mbar_arrive(empty0 + 8 * ((k - 1) % kQSlots));   // index k - 1 is done
     }
     op.finish();
 }
@@ -263,6 +284,10 @@ inline bool launch_qsweep(const Dom& d, const double* g, const Work& w, cudaStre
     if (!tma_field_map(&tm, g, false, d.nx, d.ny, d.nz, kQPX, kQPY)) return false;
     // f-code tiles by TMA: 16-byte aligned tile origins and strides
     const bool code_tma = !kMasked && d.lo[0] % 16 == 0 && tma_u8_map(&tmc, w.code, d.nx, d.ny, d.nz, kQX, kQY);
+    // Without TMA f-code tiles the per-lane code (and dirty-word) loads sit on
+    // the critical path of every plane; the shared-fold cp.async sweep of
+    // tiles.cuh (which also skips robust centres) is faster there.
+    if (!code_tma && !getenv("PMSZ_QSWEEP_PERLANE")) return false;
     if (!code_tma) tmc = tm;
     using Op = DetectOp<kCount, kMasked, kExtrema>;
     dim3 grid;
