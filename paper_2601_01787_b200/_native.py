@@ -12,7 +12,7 @@ import os
 from pathlib import Path
 
 _HERE = Path(__file__).resolve().parent
-LIB_PATH = _HERE / "_lib" / "libpmsz.so"
+LIB_PATH = Path(os.environ["PMSZ_LIB"]) if os.environ.get("PMSZ_LIB") else _HERE / "_lib" / "libpmsz.so"   # A/B builds
 HEADER_PATH = _HERE.parent / "include" / "pmsz.h"
 
 PMSZ_OK = 0
