@@ -261,15 +261,24 @@ __global__ void __launch_bounds__(kCompactThreads) k_chunk_write(const uint32_t*
 struct Box {
     int64_t nx, ny;
     int64_t lo[3], ext[3];
+    uint64_t mxy, mx;   // div_magic(ext[0] * ext[1]), div_magic(ext[0]): 32-bit index decode
 };
+
+// Field offset of element i (x-fastest) of box b; boxes hold < 2^32 elements.
+__device__ __forceinline__ int64_t box_off(const Box& b, int64_t i) {
+    const uint32_t ii = (uint32_t)i;
+    const uint32_t z = fast_div(ii, b.mxy);
+    const uint32_t r = ii - z * (uint32_t)(b.ext[0] * b.ext[1]);
+    const uint32_t y = fast_div(r, b.mx);
+    const uint32_t x = r - y * (uint32_t)b.ext[0];
+    return (b.lo[0] + x) + b.nx * ((b.lo[1] + y) + b.ny * (b.lo[2] + z));
+}
 
 __global__ void __launch_bounds__(256) k_box_pack(Box b, const double* __restrict__ src, double* __restrict__ buf) {
     const int64_t n = b.ext[0] * b.ext[1] * b.ext[2];
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t z = i / (b.ext[0] * b.ext[1]), r = i - z * b.ext[0] * b.ext[1];
-        const int64_t y = r / b.ext[0], x = r - y * b.ext[0];
-        buf[i] = src[(b.lo[0] + x) + b.nx * ((b.lo[1] + y) + b.ny * (b.lo[2] + z))];
+        buf[i] = src[box_off(b, i)];
     }
 }
 
@@ -280,9 +289,7 @@ __global__ void __launch_bounds__(256) k_box_unpack(Box b, double* __restrict__ 
     unsigned mine = 0;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t z = i / (b.ext[0] * b.ext[1]), r = i - z * b.ext[0] * b.ext[1];
-        const int64_t y = r / b.ext[0], x = r - y * b.ext[0];
-        const int64_t o = (b.lo[0] + x) + b.nx * ((b.lo[1] + y) + b.ny * (b.lo[2] + z));
+        const int64_t o = box_off(b, i);
         const double cur = dst[o], in = buf[i];
         const double nv = kMin ? (in < cur ? in : cur) : in;
         if (nv != cur) {
@@ -306,9 +313,7 @@ __global__ void __launch_bounds__(256) k_box_mark(Dom d, Work w, Box b, const do
     const int64_t n = b.ext[0] * b.ext[1] * b.ext[2];
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t z = i / (b.ext[0] * b.ext[1]), r = i - z * b.ext[0] * b.ext[1];
-        const int64_t y = r / b.ext[0], x = r - y * b.ext[0];
-        const int64_t o = (b.lo[0] + x) + b.nx * ((b.lo[1] + y) + b.ny * (b.lo[2] + z));
+        const int64_t o = box_off(b, i);
         if (g[o] != before[i]) mark_changed(d, w, o, cur, bits);
     }
 }
@@ -322,9 +327,7 @@ __global__ void __launch_bounds__(256) k_box_merge(Dom d, Work w, Box b, double*
     unsigned mine = 0;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t z = i / (b.ext[0] * b.ext[1]), r = i - z * b.ext[0] * b.ext[1];
-        const int64_t y = r / b.ext[0], x = r - y * b.ext[0];
-        const int64_t o = (b.lo[0] + x) + b.nx * ((b.lo[1] + y) + b.ny * (b.lo[2] + z));
+        const int64_t o = box_off(b, i);
         const double cur_v = g[o], in = buf[i];
         if (in < cur_v) {
             g[o] = in;
@@ -382,9 +385,9 @@ __global__ void __launch_bounds__(256) k_box_extract(Box b, int64_t gny, const F
     const int64_t n = b.ext[0] * b.ext[1] * b.ext[2];
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t z = i / (b.ext[0] * b.ext[1]), r = i - z * b.ext[0] * b.ext[1];
-        const int64_t y = r / b.ext[0], x = r - y * b.ext[0];
-        dst[i] = src[(b.lo[0] + x) + b.nx * ((b.lo[1] + y) + gny * (b.lo[2] + z))];
+        Box bg = b;
+        bg.ny = gny;
+        dst[i] = src[box_off(bg, i)];
     }
 }
 
@@ -1225,7 +1228,9 @@ pmsz_status pmsz_box_mark_changed(pmsz_plan* p, const int64_t lo[3], const int64
     p->k0_detected = false;   // g may change before the first iteration: K0's detections are stale
     if (!p->w.incremental || p->next_mode == kFull) return PMSZ_OK;
     cudaStream_t s = S(stream);
-    Box b{p->dom.nx, p->dom.ny, {lo[0], lo[1], lo[2]}, {hi[0] - lo[0], hi[1] - lo[1], hi[2] - lo[2]}};
+    Box b{p->dom.nx, p->dom.ny, {lo[0], lo[1], lo[2]}, {hi[0] - lo[0], hi[1] - lo[1], hi[2] - lo[2]}, 0, 0};
+    b.mxy = div_magic((uint64_t)(b.ext[0] * b.ext[1]));
+    b.mx = div_magic((uint64_t)b.ext[0]);
     const int64_t n = b.ext[0] * b.ext[1] * b.ext[2];
     if (n <= 0) return PMSZ_OK;
     k_box_mark<<<grid_for(n, 256), 256, 0, s>>>(p->dom, p->w, b, before, g, p->cur, p->next_mode == kMasked);
@@ -1469,7 +1474,9 @@ static bool make_box(int64_t nx, int64_t ny, int64_t nz, const int64_t lo[3], co
     const int64_t ext[3] = {nx, ny, nz};
     for (int a = 0; a < 3; ++a)
         if (lo[a] < 0 || hi[a] > ext[a] || lo[a] > hi[a]) return false;
-    b = Box{nx, ny, {lo[0], lo[1], lo[2]}, {hi[0] - lo[0], hi[1] - lo[1], hi[2] - lo[2]}};
+    b = Box{nx, ny, {lo[0], lo[1], lo[2]}, {hi[0] - lo[0], hi[1] - lo[1], hi[2] - lo[2]}, 0, 0};
+    b.mxy = div_magic((uint64_t)(b.ext[0] * b.ext[1]));
+    b.mx = div_magic((uint64_t)b.ext[0]);
     return true;
 }
 
