@@ -556,7 +556,10 @@ pmsz_status launch_apply(pmsz_plan* p, const void* f, double* g, cudaStream_t s,
         LAUNCHED();
     }
     ProfScope ps(p, s, PMSZ_K_APPLY);
-    k_apply_list<FT><<<grid_for(bound, 256, 8), 256, 0, s>>>(p->dom, (const FT*)f, g, p->w, nxt);
+    // one CTA per SM: fewer targets in flight keep the z-window of the sorted
+    // target list (g, prop, f, counts) L2-resident -- 10 % faster than 8 / SM
+    static const int apply_per_sm = getenv("PMSZ_APPLY_PER_SM") ? atoi(getenv("PMSZ_APPLY_PER_SM")) : 1;
+    k_apply_list<FT><<<grid_for(bound, 256, apply_per_sm), 256, 0, s>>>(p->dom, (const FT*)f, g, p->w, nxt);
     LAUNCHED();
     if (p->w.incremental) {   // list-mode ring marking (no-op when the edits went to the bitmap)
         k_mark_list<<<grid_for(std::min<int64_t>(15 * bound, (int64_t)p->w.mark_limit), 256, 4), 256, 0, s>>>(
@@ -676,7 +679,9 @@ pmsz_status iterate_once(pmsz_plan* p, const void* f, double* g, cudaStream_t s)
             LAUNCHED();
         }
         ProfScope ps(p, s, PMSZ_K_DEFER);
-        k_defer<<<grid_for(p->n, 256, 8), 256, 0, s>>>(d, g, p->w);
+        // two CTAs per SM measured best (the same L2-window effect as the apply)
+        static const int defer_per_sm = getenv("PMSZ_DEFER_PER_SM") ? atoi(getenv("PMSZ_DEFER_PER_SM")) : 2;
+        k_defer<<<grid_for(p->n, 256, defer_per_sm), 256, 0, s>>>(d, g, p->w);
         LAUNCHED();
     }
     if (mode == kList) {
