@@ -172,7 +172,7 @@ struct PrepArgs {
     int64_t core_lo[3], core_hi[3];
 };
 
-template <typename FT>
+template <typename FT, bool kScreen, bool kDetect>
 __global__ void __launch_bounds__(256, sizeof(FT) == 4 ? 3 : 2) k_prep_q(Dom d, const __grid_constant__ CUtensorMap tf,
                                                    const __grid_constant__ CUtensorMap th, PrepArgs a, int zchunk) {
     using G = PrepGeo<FT>;
@@ -281,7 +281,7 @@ __global__ void __launch_bounds__(256, sizeof(FT) == 4 ? 3 : 2) k_prep_q(Dom d, 
                          [&](int r, const T2<V>& lb, const T2<V>& rb, const P2<V>& rp, V leaf) {
                 merge2(acc[r], rb);   // U group: the ring of centre r is complete
                 const uint32_t c = cz + r * sy;
-                const bool robust = a.frag != nullptr && robust2(acc[r], (V)a.thr, a.xi);
+                const bool robust = kScreen && robust2(acc[r], (V)a.thr, a.xi);
                 want[r] = live[r] && !robust;
                 if (live[r]) {
                     // validation (correction.py:52-60), hazard H6, g <- fhat
@@ -316,7 +316,7 @@ __global__ void __launch_bounds__(256, sizeof(FT) == 4 ? 3 : 2) k_prep_q(Dom d, 
                 bal[r] = __ballot_sync(0xffffffffu, want[r]);
                 tot += __popc(bal[r]);
             }
-            if (a.frag != nullptr && lane == 0) {
+            if (kScreen && lane == 0) {
 #pragma unroll
                 for (int r = 0; r < kQRowsPerThread; ++r) {
                     const uint32_t cw = cz + r * sy;   // id of lane 0's centre
@@ -363,7 +363,7 @@ __global__ void __launch_bounds__(256, sizeof(FT) == 4 ? 3 : 2) k_prep_q(Dom d, 
                 const uint8_t fc = edge ? fold_code<V>(vc, nv) : tree_code<V>(vc, nv);
                 const uint32_t c = cpl + ly * sy + lx;
                 a.code[c] = fc;
-                if (a.det != nullptr) {
+                if (kDetect) {
                     // the first detection sweep (g = fhat) of this centre
                     const int64_t gx = x0 + lx, gy = y0 + ly;
                     if (gx >= a.core_lo[0] && gx < a.core_hi[0] && gy >= a.core_lo[1] && gy < a.core_hi[1] &&
@@ -412,10 +412,6 @@ inline bool launch_prep_q(const Dom& d, const FT* f, const double* fh, double* g
     CUtensorMap tf, th;
     if (!tma_field_map(&tf, f, sizeof(FT) == 4, d.nx, d.ny, d.nz, G::kPX, G::kPY)) return false;
     if (!tma_field_map(&th, fh, false, d.nx, d.ny, d.nz, kQPX, kQPY)) return false;
-    static bool attr = false;
-    if (!attr)
-        attr = cudaFuncSetAttribute(k_prep_q<FT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)sizeof(PrepSmem<FT>)) == cudaSuccess;
     PrepArgs a;
     a.g = (g != fh) ? g : nullptr;
     a.code = code;
@@ -444,7 +440,16 @@ inline bool launch_prep_q(const Dom& d, const FT* f, const double* fh, double* g
     const int zchunk = (int)std::max<int64_t>(1, (d.nz + chunks - 1) / chunks);
     chunks = (d.nz + zchunk - 1) / zchunk;
     const dim3 grid((unsigned)((d.nx + kQX - 1) / kQX), (unsigned)((d.ny + kQY - 1) / kQY), (unsigned)chunks);
-    k_prep_q<FT><<<grid, dim3(kQX, kQY / kQRowsPerThread, 1), sizeof(PrepSmem<FT>), s>>>(all, tf, th, a, zchunk);
+    const dim3 block(kQX, kQY / kQRowsPerThread, 1);
+    const size_t smem = sizeof(PrepSmem<FT>);
+#define PMSZ_LAUNCH_PREP(R, D)                                                                          \
+    cudaFuncSetAttribute(k_prep_q<FT, R, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    k_prep_q<FT, R, D><<<grid, block, smem, s>>>(all, tf, th, a, zchunk)
+    if (frag && det) { PMSZ_LAUNCH_PREP(true, true); }
+    else if (frag) { PMSZ_LAUNCH_PREP(true, false); }
+    else if (det) { PMSZ_LAUNCH_PREP(false, true); }
+    else { PMSZ_LAUNCH_PREP(false, false); }
+#undef PMSZ_LAUNCH_PREP
     return true;
 }
 
