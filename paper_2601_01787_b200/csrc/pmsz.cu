@@ -111,13 +111,13 @@ __global__ void __launch_bounds__(256) k_bounds(int64_t n, const FT* __restrict_
 // The bitmap is cut into at most kMaxChunks contiguous chunks of whole warps'
 // words (one chunk per CTA).  k_chunk_count sums each chunk; k_chunk_scan
 // (one CTA) turns the sums into exclusive offsets in place and writes the
-// total; the list/write kernels then compact each chunk in rounds of 256
+// total; the list/write kernels then compact each chunk in rounds of 4 x 256
 // words with a block-wide scan, so ids come out ascending.
 constexpr int kCompactThreads = 256;
 constexpr int kMaxChunks = 1024;
 
 struct Chunks {
-    int64_t nwords, chunk;   // words per chunk (multiple of kCompactThreads)
+    int64_t nwords, chunk;   // words per chunk (multiple of 4 x kCompactThreads)
     int n;                   // number of chunks
 };
 
@@ -126,7 +126,8 @@ inline Chunks make_chunks(int64_t nwords, int sms) {
     c.nwords = nwords;
     int64_t want = std::min<int64_t>(kMaxChunks, std::max<int64_t>(1, (int64_t)sms * 6));
     int64_t per = (nwords + want - 1) / want;
-    per = std::max<int64_t>(kCompactThreads, (per + kCompactThreads - 1) / kCompactThreads * kCompactThreads);
+    constexpr int64_t kRound = 4 * kCompactThreads;   // words per round of the list / write kernels
+    per = std::max<int64_t>(kRound, (per + kRound - 1) / kRound * kRound);
     c.chunk = per;
     c.n = (int)std::max<int64_t>(1, (nwords + per - 1) / per);
     return c;
@@ -193,7 +194,19 @@ __global__ void __launch_bounds__(kMaxChunks) k_chunk_scan(unsigned long long* c
     if (threadIdx.x == 0 && total) *total = all;
 }
 
+// Four consecutive bitmap words w .. w + 3 of [.., w1) (one 16-byte load when whole).
+__device__ __forceinline__ uint4 load_words4(const uint32_t* bits, int64_t w, int64_t w1) {
+    if (w + 3 < w1) return *reinterpret_cast<const uint4*>(bits + w);
+    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+    if (w < w1) v.x = bits[w];
+    if (w + 1 < w1) v.y = bits[w + 1];
+    if (w + 2 < w1) v.z = bits[w + 2];
+    return v;
+}
+
 // Chunk of the bitmap -> ascending ids (bits cleared on the way when `clear`).
+// A round covers 4 x 256 words: thread t owns the four consecutive words
+// 4 t .. 4 t + 3 (one vector load), one block scan per round.
 template <typename IdT>
 __global__ void __launch_bounds__(kCompactThreads) k_chunk_list(uint32_t* __restrict__ bits, Chunks c,
                                                                 const unsigned long long* __restrict__ offs,
@@ -201,29 +214,29 @@ __global__ void __launch_bounds__(kCompactThreads) k_chunk_list(uint32_t* __rest
     __shared__ unsigned wt[kCompactThreads / 32];
     const int64_t w0 = (int64_t)blockIdx.x * c.chunk, w1 = min(w0 + c.chunk, c.nwords);
     unsigned long long pos0 = offs[blockIdx.x];
-    constexpr int kG = 4;   // rounds whose words are loaded together (latency)
-    for (int64_t base = w0; base < w1; base += kG * kCompactThreads) {
-        uint32_t mg[kG];
-#pragma unroll
-        for (int q = 0; q < kG; ++q) {
-            const int64_t w = base + q * kCompactThreads + threadIdx.x;
-            mg[q] = w < w1 ? bits[w] : 0u;
+    uint4 nxt = load_words4(bits, w0 + 4 * threadIdx.x, w1);
+    for (int64_t base = w0; base < w1; base += 4 * kCompactThreads) {
+        const int64_t w = base + 4 * threadIdx.x;
+        const uint4 v = nxt;
+        nxt = load_words4(bits, w + 4 * kCompactThreads, w1);   // next round in flight
+        if (clear && (v.x | v.y | v.z | v.w)) {
+            if (w + 3 < w1) *reinterpret_cast<uint4*>(bits + w) = make_uint4(0u, 0u, 0u, 0u);
+            else for (int q = 0; q < 3 && w + q < w1; ++q) bits[w + q] = 0u;
         }
+        unsigned total;
+        const unsigned before = block_exclusive_scan(__popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w), wt, total);
+        unsigned long long pos = pos0 + before;
+        const uint32_t m4[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-        for (int q = 0; q < kG; ++q) {
-            const int64_t w = base + q * kCompactThreads + threadIdx.x;
-            uint32_t m = mg[q];
-            if (clear && m) bits[w] = 0u;
-            unsigned total;
-            const unsigned before = block_exclusive_scan(__popc(m), wt, total);
-            unsigned long long pos = pos0 + before;
+        for (int q = 0; q < 4; ++q) {
+            uint32_t m = m4[q];
             while (m) {
                 const int b = __ffs(m) - 1;
                 m &= m - 1;
-                list[pos++] = (IdT)(w * 32 + b);
+                list[pos++] = (IdT)((w + q) * 32 + b);
             }
-            pos0 += total;
         }
+        pos0 += total;
     }
 }
 
@@ -235,23 +248,28 @@ __global__ void __launch_bounds__(kCompactThreads) k_chunk_write(const uint32_t*
     __shared__ unsigned wt[kCompactThreads / 32];
     const int64_t w0 = (int64_t)blockIdx.x * c.chunk, w1 = min(w0 + c.chunk, c.nwords);
     unsigned long long pos0 = offs[blockIdx.x];
-    uint32_t nxt = w0 + threadIdx.x < w1 ? __ldg(bits + w0 + threadIdx.x) : 0u;
-    for (int64_t base = w0; base < w1; base += kCompactThreads) {
-        const int64_t w = base + threadIdx.x;
-        uint32_t m = nxt;
-        nxt = w + kCompactThreads < w1 ? __ldg(bits + w + kCompactThreads) : 0u;
+    uint4 nxt = load_words4(bits, w0 + 4 * threadIdx.x, w1);
+    for (int64_t base = w0; base < w1; base += 4 * kCompactThreads) {
+        const int64_t w = base + 4 * threadIdx.x;
+        const uint4 v = nxt;
+        nxt = load_words4(bits, w + 4 * kCompactThreads, w1);
         unsigned total;
-        const unsigned before = block_exclusive_scan(__popc(m), wt, total);
+        const unsigned before = block_exclusive_scan(__popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w), wt, total);
         long long pos = (long long)(pos0 + before);
-        while (m) {
-            const int b = __ffs(m) - 1;
-            m &= m - 1;
-            const int64_t id = w * 32 + b;
-            if (id < n && pos < cap) {
-                ids[pos] = id;
-                vals[pos] = g[id];
+        const uint32_t m4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            uint32_t m = m4[q];
+            while (m) {
+                const int b = __ffs(m) - 1;
+                m &= m - 1;
+                const int64_t id = (w + q) * 32 + b;
+                if (id < n && pos < cap) {
+                    ids[pos] = id;
+                    vals[pos] = g[id];
+                }
+                ++pos;
             }
-            ++pos;
         }
         pos0 += total;
     }
