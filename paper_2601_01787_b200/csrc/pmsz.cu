@@ -196,11 +196,13 @@ __global__ void __launch_bounds__(kMaxChunks) k_chunk_scan(unsigned long long* c
 
 // Four consecutive bitmap words w .. w + 3 of [.., w1) (one 16-byte load when whole).
 __device__ __forceinline__ uint4 load_words4(const uint32_t* bits, int64_t w, int64_t w1) {
-    if (w + 3 < w1) return *reinterpret_cast<const uint4*>(bits + w);
-    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+    if (w + 3 < w1 && (reinterpret_cast<uintptr_t>(bits + w) & 15) == 0)
+        return *reinterpret_cast<const uint4*>(bits + w);
+    uint4 v = make_uint4(0u, 0u, 0u, 0u);   // tail of the bitmap, or a caller's unaligned view
     if (w < w1) v.x = bits[w];
     if (w + 1 < w1) v.y = bits[w + 1];
     if (w + 2 < w1) v.z = bits[w + 2];
+    if (w + 3 < w1) v.w = bits[w + 3];
     return v;
 }
 
@@ -220,8 +222,10 @@ __global__ void __launch_bounds__(kCompactThreads) k_chunk_list(uint32_t* __rest
         const uint4 v = nxt;
         nxt = load_words4(bits, w + 4 * kCompactThreads, w1);   // next round in flight
         if (clear && (v.x | v.y | v.z | v.w)) {
-            if (w + 3 < w1) *reinterpret_cast<uint4*>(bits + w) = make_uint4(0u, 0u, 0u, 0u);
-            else for (int q = 0; q < 3 && w + q < w1; ++q) bits[w + q] = 0u;
+            if (w + 3 < w1 && (reinterpret_cast<uintptr_t>(bits + w) & 15) == 0)
+                *reinterpret_cast<uint4*>(bits + w) = make_uint4(0u, 0u, 0u, 0u);
+            else
+                for (int q = 0; q < 4 && w + q < w1; ++q) bits[w + q] = 0u;
         }
         unsigned total;
         const unsigned before = block_exclusive_scan(__popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w), wt, total);
