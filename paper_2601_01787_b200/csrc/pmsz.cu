@@ -400,7 +400,8 @@ __global__ void __launch_bounds__(256) k_dilate(const uint32_t* __restrict__ e, 
     }
 }
 
-enum { kFull = 0, kMasked = 1, kList = 2, kMaskedList = 3 };
+// kMaskedQ: kMasked swept by the TMA queue sweep (dense dirty sets) instead of the gather
+enum { kFull = 0, kMasked = 1, kList = 2, kMaskedList = 3, kMaskedQ = 4 };
 
 template <typename FT>
 __global__ void __launch_bounds__(256) k_box_extract(Box b, int64_t gny, const FT* __restrict__ src, FT* __restrict__ dst) {
@@ -463,6 +464,7 @@ struct pmsz_plan {
     bool qsweep_on = true;                // tiled sweeps evaluate a per-plane queue of fragile centres (qsweep.cuh)
     bool qprep_on = true;                 // K0 as screen + queue (prep.cuh)
     bool fuse_on = true;                  // K0 also runs the first detection sweep (prep.cuh)
+    bool qmask_ok = false;                // dense masked iterations can use the TMA queue sweep (kMaskedQ)
     bool k0_detected = false;             // detbits / ndetect of the first iteration come from K0
     uint32_t* frag = nullptr;             // fragile-centre bitmap written by K0
     // host-buffer entry point staging (pmsz_run_correction_host)
@@ -601,8 +603,12 @@ pmsz_status choose_next(pmsz_plan* p, cudaStream_t s, bool marked_bits, int64_t 
                         bool appended, int64_t bound) {
     if (marked_bits) {
         if (15 * nedits > p->ncore / p->full_div) {
-            p->next_mode = kFull;
-            CUDA_TRY(cudaMemsetAsync(p->w.iteredit, 0, p->nwords * 4, s));
+            if (p->qmask_ok) {
+                p->next_mode = kMaskedQ;   // dense: masked queue sweep over the dilation
+            } else {
+                p->next_mode = kFull;
+                CUDA_TRY(cudaMemsetAsync(p->w.iteredit, 0, p->nwords * 4, s));
+            }
         } else {
             p->next_mode = kMasked;
         }
@@ -646,7 +652,7 @@ pmsz_status iterate_once(pmsz_plan* p, const void* f, double* g, cudaStream_t s)
     const int64_t cx = d.hi[0] - d.lo[0], cy = d.hi[1] - d.lo[1], cz = d.hi[2] - d.lo[2];
     const bool nonempty = cx > 0 && cy > 0 && cz > 0;
     int64_t apply_bound = p->n;   // upper bound of the targets, sizes the apply grid
-    const bool gather = p->gather_on && mode != kFull;
+    const bool gather = p->gather_on && mode != kFull && mode != kMaskedQ;
     if (mode != kList) p->bits_only = false;   // actbits is consumed (compacted or cleared) below
     if (mode == kFull) {
         if (p->w.incremental) CUDA_TRY(cudaMemsetAsync(p->w.actbits, 0, p->nwords * 4, s));
@@ -657,9 +663,9 @@ pmsz_status iterate_once(pmsz_plan* p, const void* f, double* g, cudaStream_t s)
             if (!(p->qsweep_on && launch_sweep_q<false>(d, g, p->w, s))) launch_sweep_full<false>(d, g, p->w, s);
             LAUNCHED();
         }
-    } else if (mode == kMasked || mode == kMaskedList) {
+    } else if (mode == kMasked || mode == kMaskedList || mode == kMaskedQ) {
         p->w.track = 0;
-        if (mode == kMasked) {   // dirty set = dilation of the previous iteration's edits
+        if (mode != kMaskedList) {   // dirty set = dilation of the previous iteration's edits
             ProfScope ps(p, s, PMSZ_K_OTHER);
             k_dilate<<<grid_for(p->nwords, 256, 8), 256, 0, s>>>(p->w.iteredit, p->w.actbits, p->w.detbits,
                                                                p->w.frag, p->nwords, p->ring_delta);
@@ -1073,6 +1079,10 @@ pmsz_status pmsz_plan_create(const pmsz_desc* desc, pmsz_plan** out) {
     if (const char* e = getenv("PMSZ_QSWEEP")) p->qsweep_on = atoi(e) != 0;
     if (const char* e = getenv("PMSZ_QPREP")) p->qprep_on = atoi(e) != 0;
     if (const char* e = getenv("PMSZ_FUSE")) p->fuse_on = atoi(e) != 0;
+    // measured: the dense masked queue sweep (0.45 ms) plus the dilation (0.08 ms)
+    // do not beat the plain queue sweep (0.49 ms) at 512^3, so it is opt-in
+    p->qmask_ok = p->qsweep_on && p->gather_on && qsweep_masked_ok(p->dom) && getenv("PMSZ_QMASK") &&
+                  atoi(getenv("PMSZ_QMASK")) != 0;
     if (cudaFuncSetAttribute(k_gather<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGatherSmem) !=
             cudaSuccess ||
         cudaFuncSetAttribute(k_gather<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGatherSmem) !=
@@ -1169,7 +1179,7 @@ pmsz_status pmsz_iterate(pmsz_plan* p, const void* f, double* g, uint8_t* edited
         r->iterations = p->iterations;
         r->edit_count = p->edit_total;
         if (p->last_mode == kFull) ++r->full_sweeps;
-        else if (p->last_mode == kMasked || p->last_mode == kMaskedList) ++r->masked_sweeps;
+        else if (p->last_mode == kMasked || p->last_mode == kMaskedList || p->last_mode == kMaskedQ) ++r->masked_sweeps;
         else ++r->sparse_sweeps;
     }
     return PMSZ_OK;
@@ -1244,7 +1254,8 @@ pmsz_status pmsz_mark_dirty_ids(pmsz_plan* p, const uint32_t* ids, int64_t count
     p->k0_detected = false;   // g may change before the first iteration: K0's detections are stale
     if (!p->w.incremental || p->next_mode == kFull || count <= 0) return PMSZ_OK;
     cudaStream_t s = S(stream);
-    k_mark_ids<<<grid_for(count, 256), 256, 0, s>>>(p->dom, p->w, ids, count, p->cur, p->next_mode == kMasked);
+    k_mark_ids<<<grid_for(count, 256), 256, 0, s>>>(p->dom, p->w, ids, count, p->cur,
+                                                   p->next_mode == kMasked || p->next_mode == kMaskedQ);
     LAUNCHED();
     return after_mark(p, s);
 }
@@ -1260,7 +1271,8 @@ pmsz_status pmsz_box_mark_changed(pmsz_plan* p, const int64_t lo[3], const int64
     b.mx = div_magic((uint64_t)b.ext[0]);
     const int64_t n = b.ext[0] * b.ext[1] * b.ext[2];
     if (n <= 0) return PMSZ_OK;
-    k_box_mark<<<grid_for(n, 256), 256, 0, s>>>(p->dom, p->w, b, before, g, p->cur, p->next_mode == kMasked);
+    k_box_mark<<<grid_for(n, 256), 256, 0, s>>>(p->dom, p->w, b, before, g, p->cur,
+                                                p->next_mode == kMasked || p->next_mode == kMaskedQ);
     LAUNCHED();
     return after_mark(p, s);
 }
@@ -1278,7 +1290,8 @@ pmsz_status pmsz_box_merge_min(pmsz_plan* p, double* g, const int64_t lo[3], con
     CUDA_TRY(cudaMemsetAsync(&p->ctr->changed, 0, sizeof(unsigned long long), s));
     if (n > 0) {
         const int mode = !p->w.incremental ? 0
-                         : (p->next_mode == kMasked ? 1 : ((p->next_mode == kList || p->next_mode == kMaskedList) ? 2 : 0));
+                         : ((p->next_mode == kMasked || p->next_mode == kMaskedQ) ? 1
+                            : ((p->next_mode == kList || p->next_mode == kMaskedList) ? 2 : 0));
         ProfScope ps(p, s, PMSZ_K_OTHER);
         k_box_merge<<<grid_for(n, 256), 256, 0, s>>>(p->dom, p->w, b, g, buf, p->cur, mode, &p->ctr->changed);
         LAUNCHED();

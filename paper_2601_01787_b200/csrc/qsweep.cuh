@@ -100,6 +100,7 @@ constexpr int kQThreads = (kQConsumers + 1) * 32;     // + one producer warp
 struct QSmem {
     double plane[kQSlots][kQPlaneStride];
     uint8_t code[kQSlots][kQX * kQY];                  // f-code tiles (kCodeTma)
+    uint32_t dirty[kQSlots][kQY * 4];                  // dirty-bitmap tiles (kCodeTma && kMasked): 4 words / row
     uint32_t queue[kQConsumers][kQRowsPerThread * 32 + 32];   // per-warp queue: tile index | f-code << 16 | plane bit << 24
     unsigned long long full[kQSlots];                  // TMA landed
     unsigned long long empty[kQSlots];                 // every consumer warp is done with the slot
@@ -123,9 +124,9 @@ __device__ __forceinline__ void mbar_arrive(unsigned bar) {
 template <bool kCount, bool kMasked, bool kExtrema, bool kCodeTma>
 __global__ void __launch_bounds__(kQThreads, 3) k_qsweep_tma(Dom d, const __grid_constant__ CUtensorMap tm,
                                                              const __grid_constant__ CUtensorMap tmc,
+                                                             const __grid_constant__ CUtensorMap tmd,
                                                              DetectOp<kCount, kMasked, kExtrema> op, int zchunk) {
     using Op = DetectOp<kCount, kMasked, kExtrema>;
-    static_assert(!(kCodeTma && kMasked), "masked sweeps load their dirty words per thread");
     extern __shared__ __align__(1024) unsigned char qraw[];   // TMA destinations: 128-B aligned slots
     QSmem& S = *reinterpret_cast<QSmem*>(qraw);
     const int tx = threadIdx.x, ty = threadIdx.y;   // ty = warp
@@ -155,11 +156,15 @@ __global__ void __launch_bounds__(kQThreads, 3) k_qsweep_tma(Dom d, const __grid
                 const int slot = i % kQSlots;
                 if (i >= kQSlots) mbar_wait(empty0 + 8 * slot, (unsigned)((i / kQSlots - 1) & 1));
                 const bool codes = kCodeTma && i >= 1 && i <= K;   // centre planes carry their f-code tile
-                mbar_expect_tx(full0 + 8 * slot, kQPlane * 8 + (codes ? kQX * kQY : 0));
+                const bool dirt = codes && kMasked;                 // ... and their dirty words
+                mbar_expect_tx(full0 + 8 * slot, kQPlane * 8 + (codes ? kQX * kQY : 0) + (dirt ? kQY * 16 : 0));
                 tma_load_3d(pl0 + slot * kQPlaneStride * 8, &tm, (int)xs, (int)(y0 - 1), (int)(zb - 1 + i),
                             full0 + 8 * slot);
                 if (codes)
                     tma_load_3d(cd0 + slot * kQX * kQY, &tmc, (int)x0, (int)y0, (int)(zb - 1 + i), full0 + 8 * slot);
+                if (dirt)
+                    tma_load_3d(smem_u32(&S.dirty[slot][0]), &tmd, (int)((x0 >> 5) & ~int64_t(3)), (int)y0,
+                                (int)(zb - 1 + i), full0 + 8 * slot);
             }
         }
         return;
@@ -202,10 +207,12 @@ __global__ void __launch_bounds__(kQThreads, 3) k_qsweep_tma(Dom d, const __grid
         bool want[kQRowsPerThread];
         if (kCodeTma) {
             const uint8_t* ctl = S.code[(k + 1) % kQSlots];
+            const uint32_t* dtl = S.dirty[(k + 1) % kQSlots] + ((x0 >> 5) & 3);
 #pragma unroll
             for (int r = 0; r < kQRowsPerThread; ++r) {
                 code[r] = ctl[(kQRowsPerThread * ty + r) * kQX + tx];
                 want[r] = live[r] && code[r] != kRobust;
+                if (kMasked) want[r] = want[r] && ((dtl[(kQRowsPerThread * ty + r) * 4] >> tx) & 1u);
             }
         } else {
             const uint32_t cz = cbase + (uint32_t)k * sz32;
@@ -265,6 +272,10 @@ __global__ void __launch_bounds__(kQThreads, 3) k_qsweep_tma(Dom d, const __grid
     op.finish();
 }
 
+// A masked queue sweep stages its dirty words by TMA: bitmap rows must be whole
+// 16-byte groups of words (nx % 128 == 0) and tiles must start on a word.
+inline bool qsweep_masked_ok(const Dom& d) { return d.nx % 128 == 0 && d.lo[0] % 32 == 0; }
+
 inline void qsweep_grid(const Dom& d, dim3& grid, int& zchunk) {
     const int64_t cx = d.hi[0] - d.lo[0], cy = d.hi[1] - d.lo[1], cz = d.hi[2] - d.lo[2];
     const int64_t tiles = ((cx + kQX - 1) / kQX) * ((cy + kQY - 1) / kQY);
@@ -280,32 +291,27 @@ inline void qsweep_grid(const Dom& d, dim3& grid, int& zchunk) {
 
 template <bool kCount, bool kMasked, bool kExtrema>
 inline bool launch_qsweep(const Dom& d, const double* g, const Work& w, cudaStream_t s, const uint32_t* dirty) {
-    CUtensorMap tm, tmc;
+    CUtensorMap tm, tmc, tmd;
     if (!tma_field_map(&tm, g, false, d.nx, d.ny, d.nz, kQPX, kQPY)) return false;
-    // f-code tiles by TMA: 16-byte aligned tile origins and strides
-    const bool code_tma = !kMasked && d.lo[0] % 16 == 0 && tma_u8_map(&tmc, w.code, d.nx, d.ny, d.nz, kQX, kQY);
-    // Without TMA f-code tiles the per-lane code (and dirty-word) loads sit on
-    // the critical path of every plane; the shared-fold cp.async sweep of
+    // f-code tiles by TMA: 16-byte aligned tile origins and strides; masked
+    // sweeps also stage their dirty words (bitmap rows of whole words)
+    bool code_tma = d.lo[0] % 16 == 0 && tma_u8_map(&tmc, w.code, d.nx, d.ny, d.nz, kQX, kQY);
+    if (kMasked) code_tma = code_tma && qsweep_masked_ok(d) && tma_u32_map(&tmd, dirty, d.nx / 32, d.ny, d.nz, 4, kQY);
+    else tmd = tm;
+    // Without TMA tiles the per-lane code (and dirty-word) loads sit on the
+    // critical path of every plane; the shared-fold cp.async sweep of
     // tiles.cuh (which also skips robust centres) is faster there.
-    if (!code_tma && !getenv("PMSZ_QSWEEP_PERLANE")) return false;
-    if (!code_tma) tmc = tm;
+    if (!code_tma) return false;
     using Op = DetectOp<kCount, kMasked, kExtrema>;
     dim3 grid;
     int zchunk;
     qsweep_grid(d, grid, zchunk);
     Op op{w, dirty, 0};
     const dim3 block(kQX, kQConsumers + 1, 1);
-    if (code_tma) {
-        auto kern = k_qsweep_tma<kCount, kMasked, kExtrema, !kMasked>;
-        static bool attr = false;
-        if (!attr) attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kQSmemBytes) == cudaSuccess;
-        kern<<<grid, block, kQSmemBytes, s>>>(d, tm, tmc, op, zchunk);
-    } else {
-        auto kern = k_qsweep_tma<kCount, kMasked, kExtrema, false>;
-        static bool attr = false;
-        if (!attr) attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kQSmemBytes) == cudaSuccess;
-        kern<<<grid, block, kQSmemBytes, s>>>(d, tm, tmc, op, zchunk);
-    }
+    auto kern = k_qsweep_tma<kCount, kMasked, kExtrema, true>;
+    static bool attr = false;
+    if (!attr) attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kQSmemBytes) == cudaSuccess;
+    kern<<<grid, block, kQSmemBytes, s>>>(d, tm, tmc, tmd, op, zchunk);
     return true;
 }
 

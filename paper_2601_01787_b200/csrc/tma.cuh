@@ -70,6 +70,20 @@ inline bool tma_u8_map(CUtensorMap* m, const void* base, int64_t nx, int64_t ny,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Tensor map of a bit field viewed as u32 words (nwx words per row).
+inline bool tma_u32_map(CUtensorMap* m, const void* base, int64_t nwx, int64_t ny, int64_t nz, uint32_t bx, uint32_t by) {
+    if (!tma_strides_ok(nwx, ny, 4) || (reinterpret_cast<uintptr_t>(base) & 15) != 0) return false;
+    auto enc = tma_encoder();
+    if (!enc) return false;
+    const cuuint64_t dims[3] = {(cuuint64_t)nwx, (cuuint64_t)ny, (cuuint64_t)nz};
+    const cuuint64_t strides[2] = {(cuuint64_t)(nwx * 4), (cuuint64_t)(nwx * ny * 4)};
+    const cuuint32_t box[3] = {bx, by, 1};
+    const cuuint32_t es[3] = {1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, const_cast<void*>(base), dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // ---- device ----------------------------------------------------------------
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 
