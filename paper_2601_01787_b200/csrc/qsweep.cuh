@@ -99,8 +99,8 @@ constexpr int kQConsumers = kQY / kQRowsPerThread;   // consumer warps (4 rows x
 constexpr int kQThreads = (kQConsumers + 1) * 32;     // + one producer warp
 struct QSmem {
     double plane[kQSlots][kQPlaneStride];
-    uint8_t code[kQSlots][kQX * kQY];                  // f-code tiles (kCodeTma)
-    uint32_t dirty[kQSlots][kQY * 4];                  // dirty-bitmap tiles (kCodeTma && kMasked): 4 words / row
+    uint8_t code[kQSlots][kQX * kQY];                  // f-code tiles
+    uint32_t dirty[kQSlots][kQY * 4];                  // dirty-bitmap tiles (masked): 4 words / row
     uint32_t queue[kQConsumers][kQRowsPerThread * 32 + 32];   // per-warp queue: tile index | f-code << 16 | plane bit << 24
     unsigned long long full[kQSlots];                  // TMA landed
     unsigned long long empty[kQSlots];                 // every consumer warp is done with the slot
@@ -118,10 +118,10 @@ __device__ __forceinline__ void mbar_arrive(unsigned bar) {
 // plane zb + k it waits for index k + 2, queues its fragile centres in its own
 // shared queue, evaluates them one per lane and releases index k.
 //
-// kCodeTma: the f-code tile of every centre plane comes with the g plane (one
-// more TMA box; needs x0 % 16 == 0 and nx % 16 == 0), else each lane loads
-// its codes (and, masked, dirty words) two planes ahead.
-template <bool kCount, bool kMasked, bool kExtrema, bool kCodeTma>
+// The f-code tile of every centre plane (and, masked, its dirty words) comes
+// with the g plane as one more TMA box (needs x0 % 16 == 0 and nx % 16 == 0;
+// launch_qsweep falls back to tiles.cuh otherwise).
+template <bool kCount, bool kMasked, bool kExtrema>
 __global__ void __launch_bounds__(kQThreads, 3) k_qsweep_tma(Dom d, const __grid_constant__ CUtensorMap tm,
                                                              const __grid_constant__ CUtensorMap tmc,
                                                              const __grid_constant__ CUtensorMap tmd,
@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(kQThreads, 3) k_qsweep_tma(Dom d, const __grid
             for (int i = 0; i <= K + 1; ++i) {
                 const int slot = i % kQSlots;
                 if (i >= kQSlots) mbar_wait(empty0 + 8 * slot, (unsigned)((i / kQSlots - 1) & 1));
-                const bool codes = kCodeTma && i >= 1 && i <= K;   // centre planes carry their f-code tile
+                const bool codes = i >= 1 && i <= K;   // centre planes carry their f-code tile
                 const bool dirt = codes && kMasked;                 // ... and their dirty words
                 mbar_expect_tx(full0 + 8 * slot, kQPlane * 8 + (codes ? kQX * kQY : 0) + (dirt ? kQY * 16 : 0));
                 tma_load_3d(pl0 + slot * kQPlaneStride * 8, &tm, (int)xs, (int)(y0 - 1), (int)(zb - 1 + i),
@@ -180,16 +180,7 @@ __global__ void __launch_bounds__(kQThreads, 3) k_qsweep_tma(Dom d, const __grid
 #pragma unroll
     for (int r = 0; r < kQRowsPerThread; ++r) live[r] = live_x && yr + r < d.hi[1];
     // ids < 2^32 (plan limit): 32-bit index arithmetic
-    const uint32_t cbase = (uint32_t)(x + yr * sy + zb * sz);    // centre of row 0 at plane zb
     const uint32_t ctile = (uint32_t)(x0 + y0 * sy + zb * sz);  // tile cell (0, 0) at plane zb
-    typename Op::Pre p0[kQRowsPerThread], p1[kQRowsPerThread];
-    if (!kCodeTma) {
-#pragma unroll
-        for (int r = 0; r < kQRowsPerThread; ++r) {
-            p0[r] = op.fetch(cbase + r * sy32, live[r]);
-            p1[r] = op.fetch(cbase + r * sy32 + sz32, live[r] && zb + 1 < ze);
-        }
-    }
     uint32_t* q = S.queue[ty];
     const unsigned below = (1u << lane) - 1u;
     // Carry-over: a step evaluates only whole batches of 32 queued centres;
@@ -205,7 +196,7 @@ __global__ void __launch_bounds__(kQThreads, 3) k_qsweep_tma(Dom d, const __grid
         wait_plane(k + 2);
         uint32_t code[kQRowsPerThread];
         bool want[kQRowsPerThread];
-        if (kCodeTma) {
+        {
             const uint8_t* ctl = S.code[(k + 1) % kQSlots];
             const uint32_t* dtl = S.dirty[(k + 1) % kQSlots] + ((x0 >> 5) & 3);
 #pragma unroll
@@ -213,19 +204,6 @@ __global__ void __launch_bounds__(kQThreads, 3) k_qsweep_tma(Dom d, const __grid
                 code[r] = ctl[(kQRowsPerThread * ty + r) * kQX + tx];
                 want[r] = live[r] && code[r] != kRobust;
                 if (kMasked) want[r] = want[r] && ((dtl[(kQRowsPerThread * ty + r) * 4] >> tx) & 1u);
-            }
-        } else {
-            const uint32_t cz = cbase + (uint32_t)k * sz32;
-            typename Op::Pre p2[kQRowsPerThread];
-#pragma unroll
-            for (int r = 0; r < kQRowsPerThread; ++r)
-                p2[r] = op.fetch(cz + r * sy32 + 2 * sz32, live[r] && zb + k + 2 < ze);
-#pragma unroll
-            for (int r = 0; r < kQRowsPerThread; ++r) {
-                code[r] = p0[r].code & 0xffu;
-                want[r] = op.wants(p0[r]);
-                p0[r] = p1[r];
-                p1[r] = p2[r];
             }
         }
         // q[0 .. carry) holds plane k - 1's leftovers; append plane k behind them
@@ -308,7 +286,7 @@ inline bool launch_qsweep(const Dom& d, const double* g, const Work& w, cudaStre
     qsweep_grid(d, grid, zchunk);
     Op op{w, dirty, 0};
     const dim3 block(kQX, kQConsumers + 1, 1);
-    auto kern = k_qsweep_tma<kCount, kMasked, kExtrema, true>;
+    auto kern = k_qsweep_tma<kCount, kMasked, kExtrema>;
     static bool attr = false;
     if (!attr) attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kQSmemBytes) == cudaSuccess;
     kern<<<grid, block, kQSmemBytes, s>>>(d, tm, tmc, tmd, op, zchunk);
