@@ -224,6 +224,10 @@ __global__ void __launch_bounds__(256, sizeof(FT) == 4 ? 3 : 2) k_prep_q(Dom d, 
     unsigned nbound = 0, nfloor = 0, nupper = 0, nnonfin = 0, nfrag = 0, ndet = 0;
     using V = FT;
 
+    // The closed ring of centre (x, y_r, p) is covered by four 2 x 2 boxes:
+    // D = lb of plane p-1, the in-plane part lb + rb of plane p (they share the
+    // centre itself, which is harmless -- a duplicated member can only lower
+    // the screen's gaps, never raise them), and U = rb of plane p+1.
     // Plane p's shared groups for this thread's four centres, streamed row by
     // row: for centre r, emit(r, lb, rb, rp, leaf) with
     //   lb = 2 x 2 box at (x-1, y_r-1)  (D of plane p+1, in-plane of p)
@@ -254,11 +258,10 @@ __global__ void __launch_bounds__(256, sizeof(FT) == 4 ? 3 : 2) k_prep_q(Dom d, 
     wait_plane(1);
     wait_h(0);
     plane_groups(S.plane[0], [&](int r, const T2<V>& lb, const T2<V>&, const P2<V>&, V) { lbprev[r] = lb; });
-    plane_groups(S.plane[1], [&](int r, const T2<V>& lb, const T2<V>&, const P2<V>& rp, V leaf) {
+    plane_groups(S.plane[1], [&](int r, const T2<V>& lb, const T2<V>& rb, const P2<V>&, V) {
         acc[r] = lbprev[r];
         merge2(acc[r], lb);
-        merge2(acc[r], leaf);
-        merge2(acc[r], rp);
+        merge2(acc[r], rb);
         lbprev[r] = lb;
     });
     for (int k = 0; k <= K; ++k) {
@@ -300,8 +303,7 @@ __global__ void __launch_bounds__(256, sizeof(FT) == 4 ? 3 : 2) k_prep_q(Dom d, 
                 // partial ring of the same column at plane zb + k + 1
                 acc[r] = lbprev[r];
                 merge2(acc[r], lb);
-                merge2(acc[r], leaf);
-                merge2(acc[r], rp);
+                merge2(acc[r], rb);
                 lbprev[r] = lb;
             });
             if (a.g != nullptr) {
