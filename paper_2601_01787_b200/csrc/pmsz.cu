@@ -683,8 +683,15 @@ pmsz_status iterate_once(pmsz_plan* p, const void* f, double* g, cudaStream_t s)
             }
             if (nonempty) {
                 ProfScope ps(p, s, PMSZ_K_SWEEP_MASKED);
-                k_gather<false><<<num_sms() * 2, kGWarps * 32, kGatherSmem, s>>>(d, g, p->w, p->w.work,
-                                                                                 &p->ctr->ndefer);
+                // one thread per centre (k_sweep_list, 4 CTAs / SM) beats the
+                // cp.async-pipelined k_gather on the fragile-filtered lists
+                // (0.12 vs 0.25 ms at 512^3); PMSZ_LIST_SWEEP=0 selects k_gather
+                static const int list_per_sm = getenv("PMSZ_LIST_SWEEP") ? atoi(getenv("PMSZ_LIST_SWEEP")) : 4;
+                if (list_per_sm > 0)
+                    k_sweep_list<<<num_sms() * list_per_sm, 256, 0, s>>>(d, g, p->w, p->w.work, &p->ctr->ndefer);
+                else
+                    k_gather<false><<<num_sms() * 2, kGWarps * 32, kGatherSmem, s>>>(d, g, p->w, p->w.work,
+                                                                                     &p->ctr->ndefer);
                 LAUNCHED();
             }
         } else {

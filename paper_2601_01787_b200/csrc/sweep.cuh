@@ -231,6 +231,40 @@ __device__ __forceinline__ void sweep_sparse_range(const Dom& d, const double* _
     }
 }
 
+// Detection + rules over an ascending centre list (a masked iteration's
+// compacted dirty set): one thread per centre, __ldg gathers, proposals by RED
+// into prop / touched (the apply compacts touched afterwards), detection bits
+// set or cleared.  The simple form of k_gather (gather.cuh).
+__global__ void __launch_bounds__(256) k_sweep_list(Dom d, const double* __restrict__ g, Work w,
+                                                    const uint32_t* __restrict__ list,
+                                                    const unsigned long long* __restrict__ count) {
+    const unsigned long long n = *count;
+    unsigned ndet = 0;
+    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (unsigned long long)gridDim.x * blockDim.x) {
+        const int64_t c = list[i];
+        int64_t x, y, z;
+        coords(d, c, x, y, z);
+        if (!(x >= d.lo[0] && x < d.hi[0] && y >= d.lo[1] && y < d.hi[1] && z >= d.lo[2] && z < d.hi[2])) continue;
+        const uint8_t fc = w.code[c];
+        if (fc == kRobust) continue;
+        double nv[14];
+        load_ring(d, g, c, x, y, z, nv, [](const double* q) { return __ldg(q); });
+        const Scan s = fold_scan(__ldg(g + c), nv);
+        const uint32_t bit = 1u << (c & 31);
+        if (code_mismatch(d, scan_code(s), fc)) {
+            ++ndet;
+            atomicOr(w.detbits + (c >> 5), bit);
+            EmitRed emit{w};
+            rules<false>(d, w, s, nv, fc, c, emit);
+        } else if (__ldg(w.detbits + (c >> 5)) & bit) {
+            atomicAnd(w.detbits + (c >> 5), ~bit);
+        }
+    }
+    const unsigned t = __reduce_add_sync(0xffffffffu, ndet);
+    if (t && (threadIdx.x & 31) == 0) atomicAdd(&w.ctr->ndetect, (unsigned long long)t);
+}
+
 __global__ void __launch_bounds__(256) k_sweep_sparse(Dom d, const double* __restrict__ g, Work w, int cur,
                                                      int sorted) {
     sweep_sparse_range(d, g, w, cur, sorted != 0, (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x,
