@@ -263,6 +263,8 @@ inline void qsweep_grid(const Dom& d, dim3& grid, int& zchunk) {
     int64_t chunks = std::max<int64_t>((cz + 63) / 64, std::min<int64_t>(want, cz / 16));
     chunks = std::max<int64_t>(1, std::min<int64_t>(chunks, cz));
     zchunk = (int)std::max<int64_t>(1, (cz + chunks - 1) / chunks);
+    static const int zc_env = getenv("PMSZ_SWEEP_ZCHUNK") ? atoi(getenv("PMSZ_SWEEP_ZCHUNK")) : 0;
+    if (zc_env > 0) zchunk = (int)std::min<int64_t>(zc_env, cz);
     chunks = (cz + zchunk - 1) / zchunk;
     grid = dim3((unsigned)((cx + kQX - 1) / kQX), (unsigned)((cy + kQY - 1) / kQY), (unsigned)chunks);
 }
