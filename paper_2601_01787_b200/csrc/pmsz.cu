@@ -761,6 +761,8 @@ pmsz_status launch_tail(pmsz_plan* p, const void* f, double* g, cudaStream_t s, 
         if (per < 1) return fail(PMSZ_ERR_CUDA, "k_tail cannot be resident");
         static const int cap = getenv("PMSZ_TAIL_PER_SM") ? std::max(1, atoi(getenv("PMSZ_TAIL_PER_SM"))) : 1;
         nb = std::min(per, cap) * num_sms();
+        static const int nb_env = getenv("PMSZ_TAIL_BLOCKS") ? atoi(getenv("PMSZ_TAIL_BLOCKS")) : 0;
+        if (nb_env > 0) nb = std::min(nb, nb_env);
     }
     unsigned long long sort_min = (unsigned long long)p->sort_min;
     unsigned long long dense_min = (unsigned long long)(p->gather_on ? p->dense_min : p->w.act_cap);
