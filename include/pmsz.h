@@ -129,8 +129,12 @@ void pmsz_plan_destroy(pmsz_plan* plan);
 /* Device bytes of scratch owned by the plan. */
 int64_t pmsz_plan_scratch_bytes(const pmsz_plan* plan);
 /* Time every kernel launch of this plan with CUDA events on its stream
- * (enable != 0).  pmsz_profile_read returns the accumulated device time (ms)
- * and launch count per kernel class (arrays of PMSZ_K_COUNT) and optionally resets. */
+ * (enable != 0; enable == PMSZ_PROFILE_FULL_DOMAIN: only the full-domain
+ * classes PREP / SWEEP_FULL / VERIFY, whose events cost nothing measurable --
+ * timing all ~190 launches of a step adds ~0.15 ms at 512^3).
+ * pmsz_profile_read returns the accumulated device time (ms) and launch count
+ * per kernel class (arrays of PMSZ_K_COUNT) and optionally resets. */
+#define PMSZ_PROFILE_FULL_DOMAIN 2
 pmsz_status pmsz_profile(pmsz_plan* plan, int32_t enable);
 pmsz_status pmsz_profile_read(pmsz_plan* plan, double* ms, int64_t* launches, int32_t reset);
 

@@ -442,6 +442,7 @@ struct pmsz_plan {
     int f32 = 0;
     // live kernel timing (pmsz_profile)
     bool prof_on = false;
+    bool prof_light = false;   // only the full-domain classes (PMSZ_PROFILE_FULL_DOMAIN)
     std::vector<cudaEvent_t> prof_ev;   // pairs
     std::vector<int> prof_cls;          // class per recorded pair
     double prof_ms[PMSZ_K_COUNT] = {};
@@ -494,8 +495,9 @@ Dom make_dom(const pmsz_desc& d) {
 }
 
 // ---- live kernel timing: an event pair around every launch of a plan --------
-int prof_begin(pmsz_plan* p, cudaStream_t s) {
+int prof_begin(pmsz_plan* p, cudaStream_t s, int cls) {
     if (!p->prof_on) return -1;
+    if (p->prof_light && cls != PMSZ_K_PREP && cls != PMSZ_K_SWEEP_FULL && cls != PMSZ_K_VERIFY) return -1;
     const size_t k = p->prof_cls.size();
     while (p->prof_ev.size() < 2 * (k + 1)) {
         cudaEvent_t e;
@@ -526,7 +528,7 @@ void prof_flush(pmsz_plan* p) {
 
 struct ProfScope {
     pmsz_plan* p; cudaStream_t s; int tok; int cls;
-    ProfScope(pmsz_plan* p_, cudaStream_t s_, int cls_) : p(p_), s(s_), tok(prof_begin(p_, s_)), cls(cls_) {}
+    ProfScope(pmsz_plan* p_, cudaStream_t s_, int cls_) : p(p_), s(s_), tok(prof_begin(p_, s_, cls_)), cls(cls_) {}
     ~ProfScope() { prof_end(p, s, tok, cls); }
 };
 
@@ -1135,6 +1137,7 @@ void pmsz_plan_destroy(pmsz_plan* p) {
 pmsz_status pmsz_profile(pmsz_plan* p, int32_t enable) {
     if (!p) return fail(PMSZ_ERR_INVALID, "null plan");
     p->prof_on = enable != 0;
+    p->prof_light = enable == PMSZ_PROFILE_FULL_DOMAIN;
     return PMSZ_OK;
 }
 

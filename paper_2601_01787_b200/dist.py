@@ -180,17 +180,29 @@ class PeerTransport:
     def sums_and_pack(self, vals: list[int]) -> list[int]:
         eng = self.engine
         offs, _ = self.layout[self.rank]
+        tr = os.environ.get("PMSZ_DIST_TRACE") == "1"
+        t0 = _tick("-", time.perf_counter()) if tr else 0.0
         for x in self.xs:
             self.buf[offs[x.peer]:offs[x.peer] + x.size].copy_(eng.pack(x))
         k = len(vals)
         self.sums[self.rank][:k].copy_(torch.tensor(vals, dtype=torch.float64))
+        if tr:
+            t0 = _tick(" pack+sums", t0)
         self.h.barrier(channel=0)         # replicas and sums of every rank are in place
+        if tr:
+            t0 = _tick(" barrier1", t0)
         return [int(v) for v in torch.stack([s[:k] for s in self.sums]).sum(0).tolist()]
 
     def merge_packed(self) -> int:
+        tr = os.environ.get("PMSZ_DIST_TRACE") == "1"
+        t0 = _tick("-", time.perf_counter()) if tr else 0.0
         changed = sum(self.engine.merge(x, self.peer_views[x.peer]) for x in self.xs)
         self.sent += sum(x.size * 8 for x in self.xs)
+        if tr:
+            t0 = _tick(" merge_kernels", t0)
         self.h.barrier(channel=0)         # all peers are done reading my buffer (and its sums)
+        if tr:
+            t0 = _tick(" barrier2", t0)
         return changed
 
     def release(self):
@@ -500,7 +512,7 @@ def bench_main(args, metric, unit, ClockSampler, measured_peaks, cpu_sample_inpu
         st = step()
     torch.cuda.synchronize()
     TRACE.clear()
-    eng.plan.profile(True)
+    eng.plan.profile(True, full_domain_only=True)   # the other classes: a second pass below
     eng.plan.profile_read(reset=True)
     launches0 = N.launch_count()
     clocks = ClockSampler(local)
@@ -518,6 +530,14 @@ def bench_main(args, metric, unit, ClockSampler, measured_peaks, cpu_sample_inpu
     ms_local = e0.elapsed_time(e1) / args.steps
     launches = N.launch_count() - launches0
     prof = eng.plan.profile_read(reset=True)
+    eng.plan.profile(True)
+    trace_saved = dict(TRACE)
+    for _ in range(args.steps):
+        step()
+    torch.cuda.synchronize()
+    TRACE.clear()
+    TRACE.update(trace_saved)
+    prof_all = eng.plan.profile_read(reset=True)
     eng.plan.profile(False)
     t = torch.tensor([ms_local], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -540,6 +560,8 @@ def bench_main(args, metric, unit, ClockSampler, measured_peaks, cpu_sample_inpu
         for a in range(3):
             core *= blk.core_stop[a] - blk.core_start[a]
         for name, (kms, cnt) in prof.items():
+            if name not in per_voxel:
+                kms, cnt = prof_all[name]
             if cnt == 0:
                 continue
             entry = {"ms_total_per_step": kms / args.steps, "launches_per_step": cnt / args.steps,

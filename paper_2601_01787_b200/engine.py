@@ -93,8 +93,11 @@ class DomainPlan:
         except Exception:
             pass
 
-    def profile(self, enable: bool = True):
-        N.check(self.lib.pmsz_profile(self.handle, int(bool(enable))), "pmsz_profile")
+    def profile(self, enable: bool = True, full_domain_only: bool = False):
+        """Per-class kernel timing by CUDA events; full_domain_only: only the
+        PREP / SWEEP_FULL / VERIFY launches (cheap enough for a timed region)."""
+        mode = (2 if full_domain_only else 1) if enable else 0
+        N.check(self.lib.pmsz_profile(self.handle, mode), "pmsz_profile")
 
     def profile_read(self, reset: bool = False) -> dict:
         ms = (ctypes.c_double * N.K_COUNT)()
