@@ -145,6 +145,10 @@ class PeerTransport:
         self.h = symm.rendezvous(self.buf, grp)
         self.sums = [self.h.get_buffer(r, (n,), torch.float64)[n - 8:] for r in range(self.world)]
         self.n = n
+        # pinned staging of the round sums: no pageable copy (and its implicit
+        # synchronisation) on the way in, one async copy + stream sync out
+        self._hin = torch.zeros(8, dtype=torch.float64, pin_memory=True)
+        self._hout = torch.zeros(8, dtype=torch.float64, pin_memory=True)
         self.peer_views = {}
         for x in self.xs:
             offs, _ = self.layout[x.peer]
@@ -185,13 +189,17 @@ class PeerTransport:
         for x in self.xs:
             self.buf[offs[x.peer]:offs[x.peer] + x.size].copy_(eng.pack(x))
         k = len(vals)
-        self.sums[self.rank][:k].copy_(torch.tensor(vals, dtype=torch.float64))
+        hin = self._hin.numpy()
+        hin[:k] = vals
+        self.sums[self.rank][:k].copy_(self._hin[:k], non_blocking=True)
         if tr:
             t0 = _tick(" pack+sums", t0)
         self.h.barrier(channel=0)         # replicas and sums of every rank are in place
         if tr:
             t0 = _tick(" barrier1", t0)
-        return [int(v) for v in torch.stack([s[:k] for s in self.sums]).sum(0).tolist()]
+        self._hout[:k].copy_(torch.stack([s[:k] for s in self.sums]).sum(0), non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return [int(v) for v in self._hout.numpy()[:k]]
 
     def merge_packed(self) -> int:
         tr = os.environ.get("PMSZ_DIST_TRACE") == "1"
