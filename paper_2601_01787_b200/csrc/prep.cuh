@@ -221,7 +221,7 @@ __global__ void __launch_bounds__(256, sizeof(FT) == 4 ? 3 : 2) k_prep_q(Dom d, 
     const uint32_t c0 = (uint32_t)(x + yr * (int64_t)sy + zb * (int64_t)sz);   // row-0 centre at plane zb
     const int col = xo + tx;                 // staged column of x - 1
     const int row0 = kQRowsPerThread * ty;   // staged row of y_0 - 1
-    unsigned nbound = 0, nfloor = 0, nupper = 0, nnonfin = 0, nfrag = 0, ndet = 0;
+    unsigned nfrag = 0, ndet = 0;
     using V = FT;
 
     // The closed ring of centre (x, y_r, p) is covered by four 2 x 2 boxes:
@@ -293,14 +293,14 @@ __global__ void __launch_bounds__(256, sizeof(FT) == 4 ? 3 : 2) k_prep_q(Dom d, 
                     // one predicate on the fast path: NaN / Inf fail every
                     // comparison, so `ok` implies all four tests below pass
                     const bool ok = fabs(fv - hv) <= a.xi && hv >= fv - a.xi && hv <= fv + a.xi;
-                    if (!ok) {
-                        nnonfin += (!isfinite(fv) || !isfinite(hv)) ? 1u : 0u;
+                    if (!ok) {   // rare (an invalid pair): count straight into the counters
+                        if (!isfinite(fv) || !isfinite(hv)) atomicAdd(&a.ctr->nonfinite, 1ull);
                         if (fabs(fv - hv) > a.xi) {
-                            ++nbound;
+                            atomicAdd(&a.ctr->bound_viol, 1ull);
                             atomicMin(&a.ctr->bound_first, (unsigned long long)c);
                         }
-                        nfloor += hv < fv - a.xi ? 1u : 0u;
-                        nupper += hv > fv + a.xi ? 1u : 0u;
+                        if (hv < fv - a.xi) atomicAdd(&a.ctr->floor_viol, 1ull);
+                        if (hv > fv + a.xi) atomicAdd(&a.ctr->upper_viol, 1ull);
                     }
                     if (robust) a.code[c] = kRobust;
                 }
@@ -398,18 +398,10 @@ __global__ void __launch_bounds__(256, sizeof(FT) == 4 ? 3 : 2) k_prep_q(Dom d, 
             }
         }
     }
-    const unsigned b = __reduce_add_sync(0xffffffffu, nbound);
-    const unsigned fl = __reduce_add_sync(0xffffffffu, nfloor);
-    const unsigned up = __reduce_add_sync(0xffffffffu, nupper);
-    const unsigned nf = __reduce_add_sync(0xffffffffu, nnonfin);
     const unsigned nfr = __reduce_add_sync(0xffffffffu, nfrag);
     const unsigned nd = __reduce_add_sync(0xffffffffu, ndet);
     if (lane == 0) {
         if (nd) atomicAdd(&a.ctr->ndetect, (unsigned long long)nd);
-        if (b) atomicAdd(&a.ctr->bound_viol, (unsigned long long)b);
-        if (fl) atomicAdd(&a.ctr->floor_viol, (unsigned long long)fl);
-        if (up) atomicAdd(&a.ctr->upper_viol, (unsigned long long)up);
-        if (nf) atomicAdd(&a.ctr->nonfinite, (unsigned long long)nf);
         if (nfr) atomicAdd(&a.ctr->nfragile, (unsigned long long)nfr);
     }
 }
