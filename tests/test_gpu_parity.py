@@ -248,6 +248,29 @@ def test_device_tail_equals_host_loop(n, rel):
     assert (a.full_sweeps, a.masked_sweeps, a.sparse_sweeps) == (b.full_sweeps, b.masked_sweeps, b.sparse_sweeps)
 
 
+def test_profile_full_domain_only_times_only_the_full_domain_kernels():
+    """pmsz_profile(plan, PMSZ_PROFILE_FULL_DOMAIN) (the bench's timed region):
+    events only around K0 / K1 / K4, same results as the fully timed run."""
+    from paper_2601_01787_b200.engine import DomainPlan, DomainSpec
+    dims = (96, 96, 96)
+    f32 = gen.perlin_device(gen.NoiseSpec(dims, 5), f32=True)
+    xi = gen.relative_to_absolute_device(f32, 1e-4)
+    fh = gen.quantize_device(f32, xi)
+    cfg = pm.CorrectionConfig(xi_abs=xi)
+    plan = DomainPlan(DomainSpec.whole(dims), xi, cfg.tau, cfg.max_outer_iterations, f32_original=True)
+    outs = []
+    for light in (True, False):
+        plan.profile(True, full_domain_only=light)
+        plan.profile_read(reset=True)
+        outs.append((pm.run_correction_device(f32, fh, dims, cfg, plan=plan), plan.profile_read(reset=True)))
+    plan.profile(False)
+    (a, pa), (b, pb) = outs
+    assert pa["prep"][1] == pb["prep"][1] == 1
+    assert all(pa[k][1] == 0 for k in pa if k not in ("prep", "sweep_full", "verify"))
+    assert sum(pb[k][1] for k in pb if k not in ("prep", "sweep_full", "verify")) > 0
+    assert torch.equal(a.corrected, b.corrected) and a.edits_per_iteration == b.edits_per_iteration
+
+
 def test_plan_is_reusable_and_restores_invariants():
     dims = (64, 64, 64)
     f32 = gen.perlin_device(gen.NoiseSpec(dims, 2), f32=True)
