@@ -22,6 +22,10 @@
 #pragma once
 #include "qsweep.cuh"
 
+#ifndef PMSZ_PREP_MINB
+#define PMSZ_PREP_MINB 3   // resident K0 CTAs per SM for f32 fields (smem allows 3)
+#endif
+
 namespace pmsz {
 
 template <typename V> __device__ __forceinline__ V vmx(V a, V b);
@@ -173,7 +177,7 @@ struct PrepArgs {
 };
 
 template <typename FT, bool kScreen, bool kDetect>
-__global__ void __launch_bounds__(256, sizeof(FT) == 4 ? 3 : 2) k_prep_q(Dom d, const __grid_constant__ CUtensorMap tf,
+__global__ void __launch_bounds__(256, sizeof(FT) == 4 ? PMSZ_PREP_MINB : 2) k_prep_q(Dom d, const __grid_constant__ CUtensorMap tf,
                                                    const __grid_constant__ CUtensorMap th, PrepArgs a, int zchunk) {
     using G = PrepGeo<FT>;
     extern __shared__ __align__(1024) unsigned char praw[];
