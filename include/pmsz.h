@@ -233,7 +233,9 @@ pmsz_status pmsz_box_unpack_copy(int64_t nx, int64_t ny, int64_t nz, double* dst
                                  unsigned long long* changed_dev, void* stream);
 /* Ghost merge of a received replica box (_merge_min, parallel.py:122-140):
  * g[box] = min(g[box], buf) and every vertex that changed dirties its 1-ring
- * for the next incremental sweep of the plan.  *changed_out = changed vertices. */
+ * for the next incremental sweep of the plan.  *changed_out = changed vertices;
+ * changed_out == NULL: no host synchronisation -- the plan reads the marking
+ * counters at its next iteration (pmsz_iterate / pmsz_block_round). */
 pmsz_status pmsz_box_merge_min(pmsz_plan* plan, double* g_dev, const int64_t lo[3], const int64_t hi[3],
                                const double* buf_dev, int64_t* changed_out, void* stream);
 /* Detections left at the latest evaluation of every core centre (the

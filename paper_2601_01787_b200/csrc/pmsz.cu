@@ -456,6 +456,7 @@ struct pmsz_plan {
     int tail_blocks[2] = {0, 0};          // cooperative grid per FT (f64, f32)
     int64_t sort_min = 262144;            // longer dirty lists are kept in actbits only and rebuilt sorted
     int64_t dense_min = 0;                // dirty lists above this take the pipelined gather (kMaskedList)
+    bool mark_deferred = false;           // a merge marked rings without reading the counters back
     bool bits_only = false;               // the pending dirty set is in actbits only (no list)
     int64_t full_div = 8;                 // a full sweep follows when 15 x edits > ncore / full_div
     const uint32_t* offsets_of = nullptr; // bitmap whose block offsets block_counts holds
@@ -853,6 +854,7 @@ void tail_result(pmsz_plan* p, pmsz_result* r, int64_t k) {
 
 pmsz_status reset_run_state(pmsz_plan* p, cudaStream_t s) {
     p->edits_cached = -1;
+    p->mark_deferred = false;
     CUDA_TRY(cudaMemsetAsync(p->ctr, 0, sizeof(DevCounters), s));
     CUDA_TRY(cudaMemsetAsync(&p->ctr->bound_first, 0xff, sizeof(unsigned long long), s));
     CUDA_TRY(cudaMemsetAsync(p->w.editbits, 0, p->nwords * 4, s));
@@ -1168,10 +1170,16 @@ pmsz_status pmsz_prepare(pmsz_plan* p, const void* f, const double* fh, double* 
     return PMSZ_OK;
 }
 
+static pmsz_status flush_deferred_marks(pmsz_plan* p, cudaStream_t s);
+
 pmsz_status pmsz_iterate(pmsz_plan* p, const void* f, double* g, uint8_t* edited_mask, pmsz_result* r,
                          void* stream) {
     if (!p || !p->prepared) return fail(PMSZ_ERR_INVALID, "plan not prepared");
     cudaStream_t s = S(stream);
+    {
+        const pmsz_status st0 = flush_deferred_marks(p, s);
+        if (st0) return st0;
+    }
     p->w.edited_mask = edited_mask;
     if (edited_mask) CUDA_TRY(cudaMemsetAsync(edited_mask, 0, p->n, s));
     pmsz_status st = iterate_once(p, f, g, s);
@@ -1200,6 +1208,10 @@ pmsz_status pmsz_iterate(pmsz_plan* p, const void* f, double* g, uint8_t* edited
 pmsz_status pmsz_block_round(pmsz_plan* p, const void* f, double* g, int32_t lockstep, int64_t* round_edits,
                              pmsz_result* r, void* stream) {
     if (!p || !p->prepared) return fail(PMSZ_ERR_INVALID, "plan not prepared");
+    {
+        const pmsz_status st0 = flush_deferred_marks(p, S(stream));
+        if (st0) return st0;
+    }
     int64_t total = 0;
     bool dirty = false;
     for (int64_t it = 0; it < p->desc.max_iterations; ++it) {
@@ -1244,6 +1256,7 @@ pmsz_status pmsz_mark_all_dirty(pmsz_plan* p, void* stream) {
 // After marking outside an iteration: refresh the pending list length, or
 // fall back to a full sweep when the list overflowed.
 static pmsz_status after_mark(pmsz_plan* p, cudaStream_t s) {
+    p->mark_deferred = false;
     CUDA_TRY(cudaGetLastError());
     pmsz_status st = sync_counters(p, s);
     if (st) return st;
@@ -1291,6 +1304,10 @@ pmsz_status pmsz_box_mark_changed(pmsz_plan* p, const int64_t lo[3], const int64
 
 static bool make_box(int64_t nx, int64_t ny, int64_t nz, const int64_t lo[3], const int64_t hi[3], Box& b);
 
+static pmsz_status flush_deferred_marks(pmsz_plan* p, cudaStream_t s) {
+    return p->mark_deferred ? after_mark(p, s) : PMSZ_OK;
+}
+
 pmsz_status pmsz_box_merge_min(pmsz_plan* p, double* g, const int64_t lo[3], const int64_t hi[3], const double* buf,
                                int64_t* changed_out, void* stream) {
     if (!p || !g || !buf) return fail(PMSZ_ERR_INVALID, "null argument");
@@ -1308,9 +1325,14 @@ pmsz_status pmsz_box_merge_min(pmsz_plan* p, double* g, const int64_t lo[3], con
         k_box_merge<<<grid_for(n, 256), 256, 0, s>>>(p->dom, p->w, b, g, buf, p->cur, mode, &p->ctr->changed);
         LAUNCHED();
     }
+    if (!changed_out) {   // the counters are read at the next iteration
+        CUDA_TRY(cudaGetLastError());
+        p->mark_deferred = true;
+        return PMSZ_OK;
+    }
     pmsz_status st = after_mark(p, s);
     if (st) return st;
-    if (changed_out) *changed_out = (int64_t)p->hctr->changed;
+    *changed_out = (int64_t)p->hctr->changed;
     return PMSZ_OK;
 }
 

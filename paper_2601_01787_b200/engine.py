@@ -166,11 +166,14 @@ class DomainPlan:
                                                 N.stream_handle(stream)), "pmsz_bounds_violations")
         return int(out.value)
 
-    def merge_min(self, g, lo, hi, buf, stream=None) -> int:
-        """Ghost merge of a received replica box; changed vertices dirty their ring."""
-        out = ctypes.c_int64()
+    def merge_min(self, g, lo, hi, buf, stream=None, count: bool = True) -> int:
+        """Ghost merge of a received replica box; changed vertices dirty their ring.
+        count=False: no host synchronisation (returns -1; the plan reads its
+        marking counters at the next iteration)."""
+        out = ctypes.c_int64(-1)
         N.check(self.lib.pmsz_box_merge_min(self.handle, N.ptr(g), N.ivec(lo), N.ivec(hi), N.ptr(buf),
-                                            ctypes.byref(out), N.stream_handle(stream)), "pmsz_box_merge_min")
+                                            ctypes.byref(out) if count else None, N.stream_handle(stream)),
+                "pmsz_box_merge_min")
         return int(out.value)
 
     def residual(self, stream=None) -> int:
