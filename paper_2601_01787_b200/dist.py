@@ -303,7 +303,10 @@ def run_local(engines, blocks, grid, lockstep: bool, cap: int) -> DistStats:
             for x in xs[r]:
                 buf = packed[(x.peer, r)]          # the peer's replica of the same overlap
                 sent += buf.numel() * buf.element_size()
-                changed += engines[r].merge(x, buf)
+                if lockstep:
+                    changed += engines[r].merge(x, buf)
+                else:   # as run_distributed: relaxed merges defer their counter read
+                    engines[r].merge(x, buf, count=False)
         syncs += 1
         if lockstep and round_edits == 0 and changed == 0:
             break
