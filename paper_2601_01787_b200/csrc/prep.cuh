@@ -184,17 +184,18 @@ __global__ void __launch_bounds__(256, sizeof(FT) == 4 ? PMSZ_PREP_MINB : 2) k_p
     PrepSmem<FT>& S = *reinterpret_cast<PrepSmem<FT>*>(praw);
     const int tx = threadIdx.x, ty = threadIdx.y;
     const int tid = ty * kQX + tx, lane = tid & 31;
-    const int64_t x0 = (int64_t)blockIdx.x * kQX, y0 = (int64_t)blockIdx.y * kQY;
-    const int64_t zb = (int64_t)blockIdx.z * zchunk;
-    const int64_t ze = min(zb + (int64_t)zchunk, d.nz);
-    const int K = (int)(ze - zb);
+    // 32-bit coordinates (extents < 2^31, ids < 2^32: plan limits): fewer
+    // registers than int64 in this register-bound kernel
+    const int x0 = (int)blockIdx.x * kQX, y0 = (int)blockIdx.y * kQY;
+    const int zb = (int)blockIdx.z * zchunk;
+    const int K = (int)(min((int64_t)zb + zchunk, d.nz) - zb);
     const uint32_t sy = (uint32_t)d.sy, sz = (uint32_t)d.sz;
-    const int64_t xs = (x0 - 1) & ~int64_t(G::kAlign - 1);
+    const int xs = (x0 - 1) & ~(G::kAlign - 1);
     const int xo = (int)(x0 - 1 - xs);   // column of x0 - 1 in a staged row
     const unsigned bar0 = smem_u32(&S.bar[0]), hbar0 = smem_u32(&S.hbar[0]);
     const unsigned pl0 = smem_u32(&S.plane[0][0]), fh0 = smem_u32(&S.fh[0][0]);
     // plane index i = p - (zb - 1), i in [0, K + 1], for f and fhat alike
-    const int64_t xh = (x0 - 1) & ~int64_t(1);   // fhat boxes (f64): even origin
+    const int xh = (x0 - 1) & ~1;   // fhat boxes (f64): even origin
     const int xho = (int)(x0 - 1 - xh);
     auto issue = [&](int i) {
         const int s = i % G::kSlots;
@@ -217,12 +218,12 @@ __global__ void __launch_bounds__(256, sizeof(FT) == 4 ? PMSZ_PREP_MINB : 2) k_p
         for (int i = 0; i <= 2 && i <= K + 1; ++i) issue(i);
         for (int j = 0; j <= 1 && j <= K + 1; ++j) issue_h(j);
     }
-    const int64_t x = x0 + tx, yr = y0 + kQRowsPerThread * ty;
+    const int x = x0 + tx, yr = y0 + kQRowsPerThread * ty;
     const bool live_x = x < d.nx;
     bool live[kQRowsPerThread];
 #pragma unroll
     for (int r = 0; r < kQRowsPerThread; ++r) live[r] = live_x && yr + r < d.ny;
-    const uint32_t c0 = (uint32_t)(x + yr * (int64_t)sy + zb * (int64_t)sz);   // row-0 centre at plane zb
+    const uint32_t c0 = (uint32_t)x + (uint32_t)yr * sy + (uint32_t)zb * sz;   // row-0 centre at plane zb
     const int col = xo + tx;                 // staged column of x - 1
     const int row0 = kQRowsPerThread * ty;   // staged row of y_0 - 1
     unsigned nfrag = 0, ndet = 0;
@@ -359,14 +360,14 @@ __global__ void __launch_bounds__(256, sizeof(FT) == 4 ? PMSZ_PREP_MINB : 2) k_p
         }
         if (k >= 1) {
             // exact f-codes of the fragile centres of plane zc = zb + k - 1
-            const int64_t zc = zb + k - 1;
+            const int zc = zb + k - 1;
             const unsigned n = S.cnt[(k - 1) % 3];
             const uint16_t* q = S.queue[(k - 1) & 1];
             const V* dn = S.plane[(k - 1) % G::kSlots];
             const V* ct = S.plane[k % G::kSlots];
             const V* up = S.plane[(k + 1) % G::kSlots];
             const bool edge = x0 == 0 || x0 + kQX >= d.nx || y0 == 0 || y0 + kQY >= d.ny || zc == 0 || zc + 1 >= d.nz;
-            const uint32_t cpl = c0 - (uint32_t)(tx + kQRowsPerThread * ty * (int64_t)sy) + (uint32_t)(k - 1) * sz;
+            const uint32_t cpl = c0 - (uint32_t)tx - (uint32_t)(kQRowsPerThread * ty) * sy + (uint32_t)(k - 1) * sz;
             for (unsigned e = tid; e < n; e += 256) {
                 const int idx = q[e];
                 const int ly = idx >> 5, lx = idx & 31;
@@ -382,7 +383,7 @@ __global__ void __launch_bounds__(256, sizeof(FT) == 4 ? PMSZ_PREP_MINB : 2) k_p
                 a.code[c] = fc;
                 if (kDetect) {
                     // the first detection sweep (g = fhat) of this centre
-                    const int64_t gx = x0 + lx, gy = y0 + ly;
+                    const int gx = x0 + lx, gy = y0 + ly;
                     if (gx >= a.core_lo[0] && gx < a.core_hi[0] && gy >= a.core_lo[1] && gy < a.core_hi[1] &&
                         zc >= a.core_lo[2] && zc < a.core_hi[2]) {
                         double hv[14], hc;
