@@ -241,7 +241,7 @@ __global__ void __launch_bounds__(256, sizeof(FT) == 4 ? PMSZ_PREP_MINB : 2) k_p
     auto plane_groups = [&](const V* P, auto&& emit) {
         const V* row = P + row0 * G::kPX + col;
         V l = row[0], m = row[1], rr = row[2];
-        P2<V> pl = p2(l, m), pr = p2(m, rr), pl1, pr1;
+        P2<V> pl = p2(l, m), pr = p2(m, rr), pl1;
         V leaf_prev = rr;
 #pragma unroll
         for (int j = 1; j < kQRowsPerThread + 2; ++j) {
