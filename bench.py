@@ -336,8 +336,11 @@ def run_ours_single(args):
                        "parallelism": "single GPU"},
             "roofline": roofline, "clocks": clk, "gpu_launches": launches, "result": check}
 
+    # bit-exact pin against the reference's own 512^3 result (tests/golden/
+    # make_golden_large.py): corrected field, edit record, schedule
+    line["result"].update(reference_pin(args, wl, f32, fh, res))
     if not args.no_e2e:
-        line["e2e"] = e2e_host(args, plan, f32, fh, dims, nvox)
+        line["e2e"] = e2e_host(args, plan, f32, fh, dims, nvox, res)
     if not args.no_cpu_baseline:
         f, fhs, xic, sdims = cpu_sample_inputs(args.workload, dims, args.cpu_sample_z, args.rel, args.seed,
                                                xi=xi, origin=lo, norm=wl.get("norm"))
@@ -351,10 +354,43 @@ def run_ours_single(args):
     return 0
 
 
-def e2e_host(args, plan, f32, fh, dims, nvox) -> dict:
+def _sha(t) -> str:
+    import hashlib
+    import torch
+    a = t.detach().cpu() if isinstance(t, torch.Tensor) else t
+    return hashlib.sha256(np.ascontiguousarray(a.numpy() if hasattr(a, "numpy") else a).tobytes()).hexdigest()
+
+
+def reference_pin(args, wl, f32, fh, res) -> dict:
+    """Digests of this run against the reference's result on the same inputs
+    (tests/golden/golden_large.json, generated by the reference itself)."""
+    p = ROOT / "tests" / "golden" / "golden_large.json"
+    key = {256: "c256", 512: "c512"}.get(args.size)
+    out = {"corrected_sha256": _sha(res.corrected), "ids_sha256": _sha(res.edit_ids),
+           "vals_sha256": _sha(res.edit_values)}
+    if not p.exists() or key is None or args.workload != "perlin" or args.seed != 0 or args.rel != 1e-4:
+        out["reference_pin"] = "no reference digest for this workload"
+        return out
+    ref = json.loads(p.read_text()).get(key)
+    if ref is None or "serial" not in ref:
+        out["reference_pin"] = "no reference digest for this workload"
+        return out
+    s = ref["serial"]
+    inputs_ok = _sha(f32) == ref["f32_sha256"] and _sha(fh) == ref["fhat_sha256"]
+    match = (inputs_ok and out["corrected_sha256"] == s["corrected_sha256"] and out["ids_sha256"] == s["ids_sha256"]
+             and out["vals_sha256"] == s["vals_sha256"] and list(res.edits_per_iteration) == s["edits_per_iteration"]
+             and res.max_vertex_edits == s["max_vertex_edits"])
+    out["reference_pin"] = {"source": f"tests/golden/golden_large.json[{key}] (reference run_correction, "
+                                      f"{s.get('seconds', '?')} s on the build host)",
+                            "inputs_match": inputs_ok, "bit_exact": bool(match)}
+    return out
+
+
+def e2e_host(args, plan, f32, fh, dims, nvox, dev_res) -> dict:
     """Same metric through the C ABI with HOST buffers: pinned f32 original and
-    f64 decompressed in, edit record (ids + values) out, copies inside the
-    timed region (pmsz_run_correction_host)."""
+    f64 decompressed in, corrected field + edit record (ids + values) out,
+    copies inside the timed region (pmsz_run_correction_host).  The outputs of
+    the last timed call are checked against the device-resident run."""
     import ctypes
     import torch
     from paper_2601_01787_b200 import _native as N
@@ -366,12 +402,13 @@ def e2e_host(args, plan, f32, fh, dims, nvox) -> dict:
     cap = nvox // 8
     ids = torch.empty(cap, dtype=torch.int64, pin_memory=True)
     vals = torch.empty(cap, dtype=torch.float64, pin_memory=True)
+    g_host = torch.empty(nvox, dtype=torch.float64, pin_memory=True)
     hist = (ctypes.c_int64 * plan.max_iterations)()
     res = N.PmszResult()
     stream = torch.cuda.current_stream()
 
     def call():
-        st = L.pmsz_run_correction_host(plan.handle, N.ptr(f_host), N.ptr(fh_host), None, N.ptr(ids), N.ptr(vals),
+        st = L.pmsz_run_correction_host(plan.handle, N.ptr(f_host), N.ptr(fh_host), N.ptr(g_host), N.ptr(ids), N.ptr(vals),
                                         cap, hist, plan.max_iterations, ctypes.byref(res),
                                         N.stream_handle(stream))
         N.check(st, "pmsz_run_correction_host")
@@ -385,9 +422,19 @@ def e2e_host(args, plan, f32, fh, dims, nvox) -> dict:
     torch.cuda.synchronize()
     dt = (time.perf_counter() - t0) / args.steps
     edits = int(res.edit_count)
+    m = min(edits, cap)
+    check = {"edit_count": edits, "matches_device": bool(
+        edits == int(dev_res.edit_ids.numel()) and edits <= cap
+        and _sha(ids[:m]) == _sha(dev_res.edit_ids) and _sha(vals[:m]) == _sha(dev_res.edit_values)
+        and _sha(g_host) == _sha(dev_res.corrected)
+        and list(hist[:int(res.iterations)]) == list(dev_res.edits_per_iteration))}
+    if not check["matches_device"]:
+        raise SystemExit("e2e host path differs from the device-resident run")
     return {"value": nvox / dt, "unit": UNIT, "h2d_bytes_per_step": nvox * (4 + 8),
-            "d2h_bytes_per_step": edits * 16 + 8 * int(res.iterations), "ms_per_step": dt * 1e3,
-            "path": "pmsz_run_correction_host (pinned host f32 f + f64 fhat in, edit ids+values out)"}
+            "d2h_bytes_per_step": nvox * 8 + edits * 16 + 8 * int(res.iterations), "ms_per_step": dt * 1e3,
+            "path": "pmsz_run_correction_host (pinned host f32 f + f64 fhat in; corrected f64 field + edit "
+                    "ids/values out; input copied in z-slabs overlapped with K0)",
+            "check": check}
 
 
 def main():

@@ -52,8 +52,13 @@ enum {
     PMSZ_FLAG_INCREMENTAL = 1,   /* dirty-ring sweeps after the first (exact) */
     PMSZ_FLAG_EXTREMA_ONLY = 2,  /* drop the two order kinds (BASELINE config 5) */
     PMSZ_FLAG_F32_ORIGINAL = 4,  /* f is passed as float32 (exact promotion) */
-    PMSZ_FLAG_HOST_LOOP = 8      /* no device-resident tail: every iteration is launched
+    PMSZ_FLAG_HOST_LOOP = 8,     /* no device-resident tail: every iteration is launched
                                     and synchronised from the host (A/B and tests) */
+    PMSZ_FLAG_NO_ROBUST = 16,    /* evaluate every centre: required when g may leave
+                                    [f - xi, f + xi] (local_converge on arbitrary inputs) */
+    PMSZ_FLAG_LOWER = 32         /* pmsz_iterate / pmsz_block_round receive the f64 lower
+                                    bound L itself in place of f (local_converge's lower_ext,
+                                    parallel.py:150-172): the apply clamps to L, not f - xi */
 };
 
 /* Distortion kinds, in the reference declaration order (correction.py:133-139). */
@@ -153,10 +158,15 @@ pmsz_status pmsz_run_correction(pmsz_plan* plan, const void* f_dev, const double
 /*
  * The same call with HOST buffers (the end-to-end drop-in): copies f and fhat
  * in, runs, and writes the corrected field and the edit set back to the host.
- * g_host may be NULL (edit set only); ids_host/vals_host receive up to
- * edits_cap edits (EditSet.diff, correction.py:363-369).  The device staging
+ * g_host may be NULL (edit set only); ids_host/vals_host receive the first
+ * min(edits_cap, edit_count) edits (EditSet.diff, correction.py:363-369) --
+ * result->edit_count is always the full count, so a caller detects a
+ * truncated record by edit_count > edits_cap.  history_host receives up to
+ * history_cap entries (pmsz_history has all of them).  The device staging
  * (12 or 16 bytes per voxel plus the edit record) is owned by the plan,
- * allocated on the first call and reused.
+ * allocated on the first call and reused.  The host-to-device copy runs in
+ * z-slabs on a second stream and K0 starts on each slab as soon as it (and
+ * its upper neighbour plane) has landed.
  */
 pmsz_status pmsz_run_correction_host(pmsz_plan* plan, const void* f_host, const double* fhat_host,
                                      double* g_host, int64_t* ids_host, double* vals_host,
@@ -186,6 +196,14 @@ pmsz_status pmsz_mark_all_dirty(pmsz_plan* plan, void* stream);
 pmsz_status pmsz_mark_dirty_ids(pmsz_plan* plan, const uint32_t* ids_dev, int64_t count, void* stream);
 /* Final full detection sweep; per-kind residuals into result->residual (correction.py:424-426). */
 pmsz_status pmsz_verify(pmsz_plan* plan, const double* g_dev, pmsz_result* result, void* stream);
+/* Vertices with g < lower (f64, e.g. local_converge's lower_ext): the reference's
+ * monotonicity assertion fires at the first iteration with a detection when this is
+ * non-zero (correction.py:239-241).  The count is recorded in the plan (PMSZ_FLAG_LOWER). */
+pmsz_status pmsz_floor_violations(pmsz_plan* plan, const double* lower_dev, const double* g_dev,
+                                  int64_t* count_out, void* stream);
+/* Full per-iteration edit history of the plan's last run (edits_per_iteration,
+ * correction.py:411-416); *count receives its length, out up to cap entries. */
+pmsz_status pmsz_history(const pmsz_plan* plan, int64_t* out, int64_t cap, int64_t* count);
 /* Dense bounds check L <= g <= U (BoundsField.admits, correction.py:124-125); count out. */
 pmsz_status pmsz_bounds_violations(pmsz_plan* plan, const void* f_dev, const double* g_dev,
                                    int64_t* count_out, void* stream);
@@ -252,6 +270,10 @@ pmsz_status pmsz_box_mark_changed(pmsz_plan* plan, const int64_t lo[3], const in
 pmsz_status pmsz_perlin(const int64_t gdims[3], const int64_t lo[3], const int64_t ext[3],
                         const int32_t* perm512_host, double frequency, int32_t octaves,
                         double* out_f64_dev, float* out_f32_dev, void* stream);
+/* out = (float)v; *inexact (host) = values that do not survive the round trip
+ * (f32 fields promoted to f64 survive it exactly, codec.py:86-87; the drop-in
+ * then runs the f32 K0). */
+pmsz_status pmsz_narrow_f32(const double* v_dev, int64_t n, float* out_dev, int64_t* inexact, void* stream);
 /* min / max of n values (f32 or f64); result on the host. */
 pmsz_status pmsz_minmax(const void* values_dev, int32_t is_f32, int64_t n, double* mn, double* mx,
                         void* stream);

@@ -14,7 +14,7 @@ from .correction import (BoundsField, CorrectionConfig, CorrectionResult, Device
                          apply_edit, compute_bounds, iterate_array, run_correction,
                          run_correction_device, validate_error_bound)
 from .parallel import (Block, BlockDecomposition, ParallelStats, SyncStrategy, block_domain, decompose,
-                       run_parallel)
+                       local_converge, run_parallel, sync_ghosts)
 from .codec import (FormatError, decode_edits, decode_edits_meta, encode_edits, read_field, read_labels,
                     write_field, write_labels)
 from .inputs import NoiseSpec, PeakSpec

@@ -37,6 +37,8 @@ FLAG_INCREMENTAL = 1
 FLAG_EXTREMA_ONLY = 2
 FLAG_F32_ORIGINAL = 4
 FLAG_HOST_LOOP = 8
+FLAG_NO_ROBUST = 16
+FLAG_LOWER = 32
 
 i64 = ctypes.c_int64
 i32 = ctypes.c_int32
@@ -89,6 +91,8 @@ SIGNATURES = {
     "pmsz_mark_dirty_ids": (i32, [vp, vp, i64, vp]),
     "pmsz_verify": (i32, [vp, vp, ctypes.POINTER(PmszResult), vp]),
     "pmsz_bounds_violations": (i32, [vp, vp, vp, i64p, vp]),
+    "pmsz_floor_violations": (i32, [vp, vp, vp, i64p, vp]),
+    "pmsz_history": (i32, [vp, i64p, i64, i64p]),
     "pmsz_scan_neighbors": (i32, [i64, i64, i64, vp, vp, vp, vp, vp, vp]),
     "pmsz_scan_codes": (i32, [i64, i64, i64, vp, vp, vp]),
     "pmsz_box_pack": (i32, [i64, i64, i64, vp, i64p, i64p, vp, vp]),
@@ -99,6 +103,7 @@ SIGNATURES = {
     "pmsz_residual": (i32, [vp, i64p, vp]),
     "pmsz_perlin": (i32, [i64p, i64p, i64p, ctypes.POINTER(i32), ctypes.c_double, i32, vp, vp, vp]),
     "pmsz_minmax": (i32, [vp, i32, i64, dp, dp, vp]),
+    "pmsz_narrow_f32": (i32, [vp, i64, vp, i64p, vp]),
     "pmsz_quantize": (i32, [vp, i32, i64, ctypes.c_double, ctypes.c_double, vp, i64p, vp]),
     "pmsz_bounded_noise": (i32, [vp, i32, i64, i64, i64, i64p, i64p, ctypes.c_double, u64, vp, vp]),
     "pmsz_box_extract": (i32, [i64p, vp, i32, i64p, i64p, vp, vp]),

@@ -27,7 +27,7 @@ import torch
 
 from . import _native as N
 from .engine import (BoundViolationError, ConvergenceError, DomainPlan, DomainSpec,
-                     as_device_f64, raise_for)
+                     as_device_f64, narrow_if_exact, raise_for)
 from .grid import ScalarField
 from .topology import DistortionReport
 
@@ -247,11 +247,16 @@ def run_correction(original: ScalarField, decompressed: ScalarField, config: Cor
     dev = torch.device("cuda", torch.cuda.current_device())
     f = as_device_f64(original.values, dev)
     fh = as_device_f64(decompressed.values, dev)
-    g = torch.empty_like(fh)
+    # ScalarField always holds f64 (grid.py:57); an f32-exact field (every
+    # field read from an f32 file, codec.py:86-87) runs the f32 K0
+    f32 = narrow_if_exact(f)
+    if f32 is not None:
+        f = f32
     plan = _plan_for(original.dims, config, incremental=incremental, extrema_only=False,
-                     f32_original=False)
-    st, res, hist = plan.run(f, fh, g)
+                     f32_original=f32 is not None)
+    st, res, hist = plan.run(f, fh, fh)   # in place: fh is this call's own device copy
     raise_for(st, res, original.values, decompressed.values, config.xi_abs)
+    g = fh
     ids, vals = plan.export_edits(g)
     corrected = ScalarField(original.dims, g.cpu().numpy())
     edits = EditSet(ids=ids.cpu().numpy(), values=vals.cpu().numpy(),

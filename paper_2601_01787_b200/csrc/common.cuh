@@ -45,6 +45,7 @@ struct Dom {
     int64_t lo[3], hi[3]; // core (centre) box
     int32_t shl[3], shh[3]; // shared band widths (block mode)
     double xi, tau;
+    double lxi;           // subtracted from the apply's f operand: xi, or 0 when the caller passes L itself
     int extrema_only;
     // exact 32-bit division by the strides (ids < 2^32): q = umulhi64(m, c)
     // with m = ceil(2^64 / stride) (Lemire-Kaser-Kurz); 0 encodes stride 1

@@ -107,6 +107,34 @@ __global__ void __launch_bounds__(256) k_bounds(int64_t n, const FT* __restrict_
     if ((threadIdx.x & 31) == 0 && mine) atomicAdd(count, mine);
 }
 
+// g < lower (local_converge with an explicit lower bound): the reference's
+// dense apply would raise such a vertex (correction.py:239-241)
+__global__ void __launch_bounds__(256) k_below(int64_t n, const double* __restrict__ lower,
+                                               const double* __restrict__ g, unsigned long long* count) {
+    unsigned mine = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        if (g[i] < lower[i]) ++mine;
+    mine = __reduce_add_sync(0xffffffffu, mine);
+    if ((threadIdx.x & 31) == 0 && mine) atomicAdd(count, (unsigned long long)mine);
+}
+
+// f64 -> f32 with an exactness count (the drop-in's f32 fast path: fields read
+// from f32 files are promoted exactly, codec.py:86-87)
+__global__ void __launch_bounds__(256) k_narrow(int64_t n, const double* __restrict__ v, float* __restrict__ out,
+                                                unsigned long long* inexact) {
+    unsigned mine = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double x = v[i];
+        const float y = (float)x;
+        out[i] = y;
+        if (!((double)y == x)) ++mine;   // NaN counts as inexact: the f64 path reports it
+    }
+    mine = __reduce_add_sync(0xffffffffu, mine);
+    if ((threadIdx.x & 31) == 0 && mine) atomicAdd(inexact, (unsigned long long)mine);
+}
+
 // ---- bitmap compaction (ascending id lists) ----------------------------------
 // The bitmap is cut into at most kMaxChunks contiguous chunks of whole warps'
 // words (one chunk per CTA).  k_chunk_count sums each chunk; k_chunk_scan
@@ -469,6 +497,8 @@ struct pmsz_plan {
     bool qmask_ok = false;                // dense masked iterations can use the TMA queue sweep (kMaskedQ)
     bool k0_detected = false;             // detbits / ndetect of the first iteration come from K0
     uint32_t* frag = nullptr;             // fragile-centre bitmap written by K0
+    int64_t hist_chunk = 0;               // thist / hthist entries: iterations per tail launch
+    std::vector<int64_t> hist_all;        // edits_per_iteration of the last pmsz_run_correction
     // host-buffer entry point staging (pmsz_run_correction_host)
     uint32_t* frag_out() const { return robust_on ? frag : nullptr; }
     void* stage_f = nullptr;
@@ -476,6 +506,10 @@ struct pmsz_plan {
     int64_t* stage_ids = nullptr;
     double* stage_vals = nullptr;
     int64_t stage_cap = 0;
+    cudaStream_t copy_stream = nullptr;   // host-to-device slabs of pmsz_run_correction_host
+    std::vector<cudaEvent_t> stage_ev;    // [0]: staging free; [1 + c]: slab c landed
+    std::vector<int64_t> stage_z;         // slab boundaries in z (nslabs + 1)
+    bool stage_pending = false;           // the next K0 waits for the slabs, one launch per slab
 };
 
 namespace {
@@ -489,6 +523,7 @@ Dom make_dom(const pmsz_desc& d) {
         o.shl[a] = d.shared_lo[a]; o.shh[a] = d.shared_hi[a];
     }
     o.xi = d.xi; o.tau = d.tau;
+    o.lxi = (d.flags & PMSZ_FLAG_LOWER) ? 0.0 : d.xi;
     o.extrema_only = (d.flags & PMSZ_FLAG_EXTREMA_ONLY) ? 1 : 0;
     o.msy = div_magic((uint64_t)o.sy);
     o.msz = div_magic((uint64_t)o.sz);
@@ -858,7 +893,7 @@ pmsz_status reset_run_state(pmsz_plan* p, cudaStream_t s) {
     CUDA_TRY(cudaMemsetAsync(p->ctr, 0, sizeof(DevCounters), s));
     CUDA_TRY(cudaMemsetAsync(&p->ctr->bound_first, 0xff, sizeof(unsigned long long), s));
     CUDA_TRY(cudaMemsetAsync(p->w.editbits, 0, p->nwords * 4, s));
-    CUDA_TRY(cudaMemsetAsync(p->w.counts, 0, p->n * sizeof(uint16_t), s));
+    CUDA_TRY(cudaMemsetAsync(p->w.counts, 0, p->n * (p->w.counts32 ? 4 : 2), s));
     if (p->w.incremental) {
         CUDA_TRY(cudaMemsetAsync(p->w.actbits, 0, p->nwords * 4, s));
         CUDA_TRY(cudaMemsetAsync(p->w.iteredit, 0, p->nwords * 4, s));
@@ -893,9 +928,25 @@ pmsz_status prep(pmsz_plan* p, const void* f, const double* fh, double* g, cudaS
         uint32_t* det = p->fuse_on ? p->w.detbits : nullptr;
         if (det) CUDA_TRY(cudaMemsetAsync(det, 0, p->nwords * 4, s));
         bool queued = false;
-        if (p->qprep_on)
+        const size_t nsl = p->stage_pending ? p->stage_z.size() - 1 : 0;
+        if (p->qprep_on && nsl > 0) {
+            // input still arriving in z-slabs: K0 over slab c once slab c and
+            // the first plane of slab c + 1 (its upper halo) have landed
+            for (size_t c = 0; c < nsl; ++c) {
+                CUDA_TRY(cudaStreamWaitEvent(s, p->stage_ev[1 + std::min(c + 1, nsl - 1)], 0));
+                queued = p->f32 ? launch_prep_q<float>(p->dom, (const float*)f, fh, g, p->w.code, p->frag_out(), p->ctr,
+                                                       det, s, p->stage_z[c], p->stage_z[c + 1])
+                                : launch_prep_q<double>(p->dom, (const double*)f, fh, g, p->w.code, p->frag_out(),
+                                                        p->ctr, det, s, p->stage_z[c], p->stage_z[c + 1]);
+                if (!queued) break;   // no tensor map for this field: nothing was launched
+                if (c + 1 < nsl) LAUNCHED();
+            }
+        } else if (p->qprep_on) {
             queued = p->f32 ? launch_prep_q<float>(p->dom, (const float*)f, fh, g, p->w.code, p->frag_out(), p->ctr, det, s)
                             : launch_prep_q<double>(p->dom, (const double*)f, fh, g, p->w.code, p->frag_out(), p->ctr, det, s);
+        }
+        if (nsl > 0) CUDA_TRY(cudaStreamWaitEvent(s, p->stage_ev[nsl], 0));   // every slab is in
+        p->stage_pending = false;
         p->k0_detected = queued && det != nullptr;
         if (!queued) {
             if (p->f32)
@@ -1046,6 +1097,9 @@ pmsz_status pmsz_plan_create(const pmsz_desc* desc, pmsz_plan** out) {
     p->nwords = (n + 31) / 32;
     p->f32 = (d.flags & PMSZ_FLAG_F32_ORIGINAL) ? 1 : 0;
     p->w.incremental = (d.flags & PMSZ_FLAG_INCREMENTAL) ? 1 : 0;
+    // a vertex is edited at most once per iteration: u16 counts hold any run of <= 65535 iterations
+    p->w.counts32 = d.max_iterations > 65535 ? 1 : 0;
+    if (d.flags & PMSZ_FLAG_LOWER) p->f32 = 0;   // the iteration operand is the f64 lower bound
     const int64_t ncore = (d.core_hi[0] - d.core_lo[0]) * (d.core_hi[1] - d.core_lo[1]) *
                           (d.core_hi[2] - d.core_lo[2]);
     p->w.act_cap = (unsigned long long)std::max<int64_t>(ncore / 4, 4096);
@@ -1068,7 +1122,7 @@ pmsz_status pmsz_plan_create(const pmsz_desc* desc, pmsz_plan** out) {
         return true;
     };
     bool ok = alloc((void**)&p->w.prop, n * 8) && alloc((void**)&p->w.work, n * 4) &&
-              alloc((void**)&p->w.editbits, p->nwords * 4) && alloc((void**)&p->w.counts, n * 2) &&
+              alloc((void**)&p->w.editbits, p->nwords * 4) && alloc((void**)&p->w.counts, n * (p->w.counts32 ? 4 : 2)) &&
               alloc((void**)&p->w.touched, p->nwords * 4) && alloc((void**)&p->w.detbits, p->nwords * 4) &&
               alloc((void**)&p->w.code, n) && alloc((void**)&p->frag, p->nwords * 4) &&
               alloc((void**)&p->ctr, sizeof(DevCounters)) &&
@@ -1077,7 +1131,10 @@ pmsz_status pmsz_plan_create(const pmsz_desc* desc, pmsz_plan** out) {
         ok = alloc((void**)&p->w.actbits, p->nwords * 4) && alloc((void**)&p->w.act[0], p->w.act_cap * 4) &&
              alloc((void**)&p->w.act[1], p->w.act_cap * 4) && alloc((void**)&p->w.iteredit, p->nwords * 4) &&
              alloc((void**)&p->w.elist, p->w.mark_limit * 4);
-    const int64_t hist_n = std::max<int64_t>(d.max_iterations, 1);
+    // per-launch history of the device tail: a fixed chunk (the tail hands back
+    // to the host after at most this many iterations), not the iteration cap
+    const int64_t hist_n = std::min<int64_t>(std::max<int64_t>(d.max_iterations, 1), 4096);
+    p->hist_chunk = hist_n;
     if (ok) ok = alloc((void**)&p->tail, sizeof(TailState)) && alloc((void**)&p->thist, hist_n * 8);
     if (ok) ok = cudaMallocHost((void**)&p->hctr, sizeof(DevCounters)) == cudaSuccess &&
                  cudaMallocHost((void**)&p->htail, sizeof(TailState)) == cudaSuccess &&
@@ -1089,6 +1146,7 @@ pmsz_status pmsz_plan_create(const pmsz_desc* desc, pmsz_plan** out) {
     if (const char* e = getenv("PMSZ_FULL_DIV")) p->full_div = std::max<int64_t>(1, atoll(e));
     if (const char* e = getenv("PMSZ_SWEEP")) p->gather_on = strcmp(e, "tiled") != 0;
     if (const char* e = getenv("PMSZ_ROBUST")) p->robust_on = atoi(e) != 0;
+    if (d.flags & PMSZ_FLAG_NO_ROBUST) p->robust_on = false;
     if (const char* e = getenv("PMSZ_QSWEEP")) p->qsweep_on = atoi(e) != 0;
     if (const char* e = getenv("PMSZ_QPREP")) p->qprep_on = atoi(e) != 0;
     if (const char* e = getenv("PMSZ_FUSE")) p->fuse_on = atoi(e) != 0;
@@ -1132,6 +1190,8 @@ void pmsz_plan_destroy(pmsz_plan* p) {
     if (p->htail) cudaFreeHost(p->htail);
     if (p->hthist) cudaFreeHost(p->hthist);
     cudaFree(p->stage_f); cudaFree(p->stage_g); cudaFree(p->stage_ids); cudaFree(p->stage_vals);
+    for (cudaEvent_t e : p->stage_ev) cudaEventDestroy(e);
+    if (p->copy_stream) cudaStreamDestroy(p->copy_stream);
     for (cudaEvent_t e : p->prof_ev) cudaEventDestroy(e);
     delete p;
 }
@@ -1218,7 +1278,7 @@ pmsz_status pmsz_block_round(pmsz_plan* p, const void* f, double* g, int32_t loc
         if (!lockstep && tail_ok(p)) {
             int64_t k = 0;
             bool sh = false;
-            pmsz_status st = tail_step(p, f, g, S(stream), p->desc.max_iterations - it, &k, &sh);
+            pmsz_status st = tail_step(p, f, g, S(stream), std::min(p->desc.max_iterations - it, p->hist_chunk), &k, &sh);
             if (st) { restore_prop(p, S(stream)); return st; }
             tail_result(p, r, k);
             for (int64_t i = 0; i < k; ++i) total += (int64_t)p->hthist[i];
@@ -1353,6 +1413,27 @@ pmsz_status pmsz_verify(pmsz_plan* p, const double* g, pmsz_result* r, void* str
     return PMSZ_OK;
 }
 
+pmsz_status pmsz_floor_violations(pmsz_plan* p, const double* lower, const double* g, int64_t* out, void* stream) {
+    if (!p || !lower || !g || !out) return fail(PMSZ_ERR_INVALID, "null argument");
+    cudaStream_t s = S(stream);
+    CUDA_TRY(cudaMemsetAsync(&p->ctr->scratch[1], 0, sizeof(unsigned long long), s));
+    k_below<<<grid_for(p->n, 256), 256, 0, s>>>(p->n, lower, g, &p->ctr->scratch[1]);
+    LAUNCHED();
+    CUDA_TRY(cudaGetLastError());
+    pmsz_status st = sync_counters(p, s);
+    if (st) return st;
+    *out = (int64_t)p->hctr->scratch[1];
+    p->floor_viol = *out;   // arms the monotonicity check of pmsz_iterate (correction.py:240-241)
+    return PMSZ_OK;
+}
+
+pmsz_status pmsz_history(const pmsz_plan* p, int64_t* out, int64_t cap, int64_t* count) {
+    if (!p || !count) return fail(PMSZ_ERR_INVALID, "null argument");
+    *count = (int64_t)p->hist_all.size();
+    for (int64_t i = 0; out && i < cap && i < *count; ++i) out[i] = p->hist_all[i];
+    return PMSZ_OK;
+}
+
 pmsz_status pmsz_bounds_violations(pmsz_plan* p, const void* f, const double* g, int64_t* out, void* stream) {
     if (!p || !out) return fail(PMSZ_ERR_INVALID, "null argument");
     return count_bounds(p, f, g, S(stream), out);
@@ -1365,6 +1446,7 @@ pmsz_status pmsz_run_correction(pmsz_plan* p, const void* f, const double* fh, d
     pmsz_result local{};
     if (!r) r = &local;
     memset(r, 0, sizeof(*r));
+    p->hist_all.clear();
     // Out of place, K0's validation is read together with the first
     // iteration's counters (g is an output buffer, so running one iteration
     // on invalid input has no visible effect beyond the error).  In place
@@ -1385,6 +1467,7 @@ pmsz_status pmsz_run_correction(pmsz_plan* p, const void* f, const double* fh, d
             return fail(PMSZ_ERR_MONOTONE, "edit raised a value; monotonicity broken");
         }
         const int64_t e = (int64_t)p->hctr->nedits;
+        p->hist_all.push_back(e);
         if (history && history_cap > 0) history[0] = e;
         it = 1;
         if (e == 0) converged = true;
@@ -1393,11 +1476,13 @@ pmsz_status pmsz_run_correction(pmsz_plan* p, const void* f, const double* fh, d
         if (tail_ok(p)) {
             int64_t k = 0;
             bool sh = false;
-            st = tail_step(p, f, g, s, p->desc.max_iterations - it, &k, &sh);
+            st = tail_step(p, f, g, s, std::min(p->desc.max_iterations - it, p->hist_chunk), &k, &sh);
             if (st) { restore_prop(p, s); return st; }
             tail_result(p, r, k);
-            for (int64_t i = 0; i < k; ++i)
+            for (int64_t i = 0; i < k; ++i) {
+                p->hist_all.push_back((int64_t)p->hthist[i]);
                 if (history && it + i < history_cap) history[it + i] = (int64_t)p->hthist[i];
+            }
             it += k;
             if (p->htail->last_edits == 0) { converged = true; break; }
             --it;   // the loop increment
@@ -1406,6 +1491,7 @@ pmsz_status pmsz_run_correction(pmsz_plan* p, const void* f, const double* fh, d
         st = pmsz_iterate(p, f, g, nullptr, r, stream);
         if (st) return st;
         const int64_t e = (int64_t)p->hctr->nedits;
+        p->hist_all.push_back(e);
         if (history && it < history_cap) history[it] = e;
         if (e == 0) { converged = true; ++it; break; }
     }
@@ -1483,9 +1569,32 @@ pmsz_status pmsz_run_correction_host(pmsz_plan* p, const void* f_host, const dou
     void* f = p->stage_f;
     double* g = p->stage_g;
     pmsz_status st = PMSZ_OK;
-    CUDA_TRY(cudaMemcpyAsync(f, f_host, fbytes, cudaMemcpyHostToDevice, s));
-    CUDA_TRY(cudaMemcpyAsync(g, fh_host, gbytes, cudaMemcpyHostToDevice, s));
+    // Input copy in z-slabs on a second stream; K0 runs slab by slab as the
+    // data lands (prep), so only the last slab's K0 is exposed.
+    const int64_t nz = p->dom.nz, plane = p->dom.nx * p->dom.ny;
+    const int64_t nsl = (p->n >= (int64_t)1 << 22) ? std::min<int64_t>(nz, 16) : 1;
+    if (!p->copy_stream) CUDA_TRY(cudaStreamCreateWithFlags(&p->copy_stream, cudaStreamNonBlocking));
+    while ((int64_t)p->stage_ev.size() < nsl + 1) {
+        cudaEvent_t e;
+        CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        p->stage_ev.push_back(e);
+    }
+    p->stage_z.assign(nsl + 1, 0);
+    for (int64_t c = 0; c <= nsl; ++c) p->stage_z[c] = nz * c / nsl;
+    CUDA_TRY(cudaEventRecord(p->stage_ev[0], s));   // earlier work on the staging buffers is done
+    CUDA_TRY(cudaStreamWaitEvent(p->copy_stream, p->stage_ev[0], 0));
+    const size_t fel = p->f32 ? 4 : 8;
+    for (int64_t c = 0; c < nsl; ++c) {
+        const int64_t o = p->stage_z[c] * plane, m = (p->stage_z[c + 1] - p->stage_z[c]) * plane;
+        CUDA_TRY(cudaMemcpyAsync((char*)f + o * fel, (const char*)f_host + o * fel, m * fel, cudaMemcpyHostToDevice,
+                                 p->copy_stream));
+        CUDA_TRY(cudaMemcpyAsync(g + o, fh_host + o, m * 8, cudaMemcpyHostToDevice, p->copy_stream));
+        CUDA_TRY(cudaEventRecord(p->stage_ev[1 + c], p->copy_stream));
+    }
+    p->stage_pending = true;
     st = pmsz_run_correction(p, f, g, g, history, history_cap, r, stream);
+    p->stage_pending = false;
+    CUDA_TRY(cudaStreamWaitEvent(s, p->stage_ev[nsl], 0));   // (already waited by K0 unless it failed early)
     if (st == PMSZ_OK) {
         if (g_host) CUDA_TRY(cudaMemcpyAsync(g_host, g, gbytes, cudaMemcpyDeviceToHost, s));
         if (ids_host && vals_host && edits_cap > 0 && r && r->edit_count > 0) {
@@ -1624,6 +1733,24 @@ pmsz_status pmsz_perlin(const int64_t gdims[3], const int64_t lo[3], const int64
     cudaFreeAsync(perm, s);
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaStreamSynchronize(s));   // perm512 is a host buffer owned by the caller
+    return PMSZ_OK;
+}
+
+pmsz_status pmsz_narrow_f32(const double* v, int64_t n, float* out, int64_t* inexact, void* stream) {
+    if (!v || !out || n < 0 || !inexact) return fail(PMSZ_ERR_INVALID, "bad arguments");
+    cudaStream_t s = S(stream);
+    unsigned long long* k = nullptr;
+    CUDA_TRY(cudaMallocAsync((void**)&k, 8, s));
+    CUDA_TRY(cudaMemsetAsync(k, 0, 8, s));
+    if (n > 0) {
+        k_narrow<<<grid_for(n, 256, 16), 256, 0, s>>>(n, v, out, k);
+        LAUNCHED();
+    }
+    unsigned long long h = 0;
+    CUDA_TRY(cudaMemcpyAsync(&h, k, 8, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    cudaFreeAsync(k, s);
+    *inexact = (int64_t)h;
     return PMSZ_OK;
 }
 

@@ -174,6 +174,7 @@ struct PrepArgs {
     uint32_t* det;
     int extrema_only;
     int64_t core_lo[3], core_hi[3];
+    int z0, z1;         // centre planes of this launch (z-slab launches overlap the input copy)
 };
 
 template <typename FT, bool kScreen, bool kDetect>
@@ -187,8 +188,8 @@ __global__ void __launch_bounds__(256, sizeof(FT) == 4 ? PMSZ_PREP_MINB : 2) k_p
     // 32-bit coordinates (extents < 2^31, ids < 2^32: plan limits): fewer
     // registers than int64 in this register-bound kernel
     const int x0 = (int)blockIdx.x * kQX, y0 = (int)blockIdx.y * kQY;
-    const int zb = (int)blockIdx.z * zchunk;
-    const int K = (int)(min((int64_t)zb + zchunk, d.nz) - zb);
+    const int zb = a.z0 + (int)blockIdx.z * zchunk;
+    const int K = min(zb + zchunk, a.z1) - zb;
     const uint32_t sy = (uint32_t)d.sy, sz = (uint32_t)d.sz;
     const int xs = (x0 - 1) & ~(G::kAlign - 1);
     const int xo = (int)(x0 - 1 - xs);   // column of x0 - 1 in a staged row
@@ -417,7 +418,8 @@ __global__ void __launch_bounds__(256, sizeof(FT) == 4 ? PMSZ_PREP_MINB : 2) k_p
 // the shared-fold K0 of tiles.cuh).
 template <typename FT>
 inline bool launch_prep_q(const Dom& d, const FT* f, const double* fh, double* g, uint8_t* code, uint32_t* frag,
-                          DevCounters* ctr, uint32_t* det, cudaStream_t s) {
+                          DevCounters* ctr, uint32_t* det, cudaStream_t s, int64_t z0 = 0, int64_t z1 = -1) {
+    if (z1 < 0) z1 = d.nz;
     using G = PrepGeo<FT>;
     CUtensorMap tf, th;
     if (!tma_field_map(&tf, f, sizeof(FT) == 4, d.nx, d.ny, d.nz, G::kPX, G::kPY)) return false;
@@ -440,6 +442,9 @@ inline bool launch_prep_q(const Dom& d, const FT* f, const double* fh, double* g
     a.det = det;
     a.extrema_only = d.extrema_only;
     for (int ax = 0; ax < 3; ++ax) { a.core_lo[ax] = d.lo[ax]; a.core_hi[ax] = d.hi[ax]; }
+    a.z0 = (int)z0;
+    a.z1 = (int)z1;
+    const int64_t nzr = z1 - z0;
     Dom all = d;
     for (int ax = 0; ax < 3; ++ax) all.lo[ax] = 0;
     all.hi[0] = d.nx; all.hi[1] = d.ny; all.hi[2] = d.nz;
@@ -447,12 +452,12 @@ inline bool launch_prep_q(const Dom& d, const FT* f, const double* fh, double* g
     const int64_t want = (148 * 2 * 6 + tiles - 1) / tiles;
     // z chunks of at most 24 planes: the ~+8 % halo re-reads cost less than
     // the tail of fewer, longer CTAs (512^3: 1.33 ms at 64 planes, 1.27 at 20-26)
-    int64_t chunks = std::max<int64_t>((d.nz + 23) / 24, std::min<int64_t>(want, d.nz / 16));
-    chunks = std::max<int64_t>(1, std::min<int64_t>(chunks, d.nz));
-    int zchunk = (int)std::max<int64_t>(1, (d.nz + chunks - 1) / chunks);
+    int64_t chunks = std::max<int64_t>((nzr + 23) / 24, std::min<int64_t>(want, nzr / 16));
+    chunks = std::max<int64_t>(1, std::min<int64_t>(chunks, nzr));
+    int zchunk = (int)std::max<int64_t>(1, (nzr + chunks - 1) / chunks);
     static const int zc_env = getenv("PMSZ_PREP_ZCHUNK") ? atoi(getenv("PMSZ_PREP_ZCHUNK")) : 0;
-    if (zc_env > 0) zchunk = (int)std::min<int64_t>(zc_env, d.nz);
-    chunks = (d.nz + zchunk - 1) / zchunk;
+    if (zc_env > 0) zchunk = (int)std::min<int64_t>(zc_env, nzr);
+    chunks = (nzr + zchunk - 1) / zchunk;
     const dim3 grid((unsigned)((d.nx + kQX - 1) / kQX), (unsigned)((d.ny + kQY - 1) / kQY), (unsigned)chunks);
     const dim3 block(kQX, kQY / kQRowsPerThread, 1);
     const size_t smem = sizeof(PrepSmem<FT>);

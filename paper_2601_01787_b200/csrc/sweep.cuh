@@ -51,7 +51,8 @@ struct Work {
     uint32_t* detbits;          // n bits: centre had a detection at its latest evaluation
     uint32_t* iteredit;         // n bits: edited in this iteration (bitmap-mode marking)
     uint32_t* elist;            // edits of a list-mode iteration (ring marking input)
-    uint16_t* counts;           // per-vertex edit counts
+    void* counts;               // per-vertex edit counts: u16, or u32 when counts32
+    int counts32;               // the iteration cap exceeds 65535 (a vertex is edited at most once per iteration)
     uint8_t* code;              // packed f-code
     const uint32_t* frag;       // n bits: fragile centres (K0); null = every centre is evaluated
     uint8_t* edited_mask;       // optional per-iteration mask
@@ -323,7 +324,9 @@ struct TargetOps {
 template <typename FT>
 __device__ __forceinline__ TargetOps load_target(const FT* __restrict__ f, const double* __restrict__ g,
                                                  const Work& w, int64_t t) {
-    return TargetOps{__ldcg(w.prop + t), __ldcg(g + t), (double)f[t], (unsigned int)__ldcg(w.counts + t)};
+    const unsigned int cnt = w.counts32 ? __ldcg((const unsigned int*)w.counts + t)
+                                        : (unsigned int)__ldcg((const uint16_t*)w.counts + t);
+    return TargetOps{__ldcg(w.prop + t), __ldcg(g + t), (double)f[t], cnt};
 }
 
 template <typename FT>
@@ -333,14 +336,15 @@ __device__ __forceinline__ void apply_target(const Dom& d, const FT* __restrict_
     const double p = okey_inv(op.key);
     w.prop[t] = kNoProposal;
     const double gt = op.gt;
-    const double lower = op.fv - d.xi;                   // BoundsField.lower (correction.py:122)
+    const double lower = op.fv - d.lxi;                  // BoundsField.lower (correction.py:122)
     const double m = (p < gt) ? p : gt;                  // np.minimum(g, prop)
     const double nv = (m < lower) ? lower : m;           // np.maximum(., lower)
     if (nv != gt) {
         g[t] = nv;
         ++acc.edits;
         const unsigned int cnt = op.cnt + 1u;
-        w.counts[t] = (uint16_t)min(cnt, 65535u);
+        if (w.counts32) ((unsigned int*)w.counts)[t] = cnt;
+        else ((uint16_t*)w.counts)[t] = (uint16_t)cnt;   // cnt <= iterations <= 65535 (plan_create)
         acc.maxc = max(acc.maxc, cnt);
         atomicOr(w.editbits + (t >> 5), 1u << (t & 31));
         if (w.edited_mask) w.edited_mask[t] = 1;

@@ -125,7 +125,11 @@ class PeerTransport:
     reading."""
 
     def __init__(self, engine, blocks, rank: int, group=None):
+        """Local part only (layout + symmetric allocation); connect() is the
+        collective rendezvous.  make_transport runs the two with an agreement
+        step in between, so a rank that fails never leaves the others waiting."""
         import torch.distributed._symmetric_memory as symm
+        self.group = group
         self.engine = engine
         self.rank = rank
         self.world = len(blocks)
@@ -141,7 +145,12 @@ class PeerTransport:
             self.layout.append((offs, o))
         n = max(o for _, o in self.layout) + 8
         self.buf = symm.empty(n, dtype=torch.float64, device=engine.device)
-        grp = (group or dist.group.WORLD).group_name
+        self.n = n
+
+    def connect(self):
+        import torch.distributed._symmetric_memory as symm
+        n = self.n
+        grp = (self.group or dist.group.WORLD).group_name
         self.h = symm.rendezvous(self.buf, grp)
         self.sums = [self.h.get_buffer(r, (n,), torch.float64)[n - 8:] for r in range(self.world)]
         self.n = n
@@ -220,13 +229,36 @@ class PeerTransport:
         self.h.barrier(channel=0)         # the loop ended without a merge: same protection
 
 
+def _agree(ok: bool, device, group=None) -> bool:
+    """True on every rank iff it is True on every rank (MIN allreduce)."""
+    t = torch.tensor([1 if ok else 0], dtype=torch.int64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+    return bool(t.item())
+
+
 def make_transport(engine, blocks, rank: int, group=None):
-    """Peer-memory transport on CUDA devices (PMSZ_P2P=0 forces the collectives)."""
-    if engine.device.type == "cuda" and os.environ.get("PMSZ_P2P", "1") != "0" and len(blocks) > 1:
+    """Peer-memory transport on CUDA devices (PMSZ_P2P=0 forces the collectives).
+    Every rank takes the same decision: the symmetric allocation and the
+    rendezvous are each followed by a MIN-allreduce of the success flags, and
+    all ranks fall back to the collectives together if any rank failed."""
+    if engine.device.type != "cuda" or len(blocks) <= 1:
+        return CollectiveTransport(engine, blocks, rank, group)
+    tp = None
+    if os.environ.get("PMSZ_P2P", "1") != "0":
         try:
-            return PeerTransport(engine, blocks, rank, group)
-        except Exception:   # no P2P / symmetric memory on this system
-            pass
+            tp = PeerTransport(engine, blocks, rank, group)
+        except Exception as e:   # no symmetric memory on this system / allocation failed
+            print(f"[pmsz rank {rank}] peer-memory transport unavailable: {e!r}", flush=True)
+    if _agree(tp is not None, engine.device, group):
+        ok = True
+        try:
+            tp.connect()
+        except Exception as e:
+            ok = False
+            print(f"[pmsz rank {rank}] symmetric-memory rendezvous failed: {e!r}", flush=True)
+        if _agree(ok, engine.device, group):
+            return tp
+    del tp   # release the symmetric buffer on every rank
     return CollectiveTransport(engine, blocks, rank, group)
 
 

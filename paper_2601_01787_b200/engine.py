@@ -57,7 +57,8 @@ class DomainPlan:
 
     def __init__(self, spec: DomainSpec, xi: float, tau: float, max_iterations: int,
                  *, incremental: bool = True, extrema_only: bool = False,
-                 f32_original: bool = False, host_loop: bool = False):
+                 f32_original: bool = False, host_loop: bool = False, no_robust: bool = False,
+                 explicit_lower: bool = False):
         self.lib = N.lib()
         self.spec = spec
         self.xi, self.tau, self.max_iterations = float(xi), float(tau), int(max_iterations)
@@ -73,7 +74,9 @@ class DomainPlan:
         d.flags = ((N.FLAG_INCREMENTAL if incremental else 0)
                    | (N.FLAG_EXTREMA_ONLY if extrema_only else 0)
                    | (N.FLAG_F32_ORIGINAL if f32_original else 0)
-                   | (N.FLAG_HOST_LOOP if host_loop else 0))
+                   | (N.FLAG_HOST_LOOP if host_loop else 0)
+                   | (N.FLAG_NO_ROBUST if no_robust else 0)
+                   | (N.FLAG_LOWER if explicit_lower else 0))
         h = ctypes.c_void_p()
         st = self.lib.pmsz_plan_create(ctypes.byref(d), ctypes.byref(h))
         if st == N.PMSZ_ERR_INVALID:
@@ -110,15 +113,29 @@ class DomainPlan:
         return int(self.lib.pmsz_plan_scratch_bytes(self.handle))
 
     # -- whole run -----------------------------------------------------------
+    HIST_BUF = 4096
+
     def run(self, f: torch.Tensor, fhat: torch.Tensor, g: torch.Tensor, stream=None):
-        """pmsz_run_correction; returns (status, PmszResult, history list)."""
-        cap = self.max_iterations
+        """pmsz_run_correction; returns (status, PmszResult, history list).  The
+        history buffer is a fixed chunk; longer runs read the plan's full
+        history afterwards (pmsz_history), so a huge iteration cap costs nothing."""
+        cap = min(self.max_iterations, self.HIST_BUF)
         hist = (ctypes.c_int64 * cap)()
         res = N.PmszResult()
         st = self.lib.pmsz_run_correction(self.handle, N.ptr(f), N.ptr(fhat), N.ptr(g), hist, cap,
                                           ctypes.byref(res), N.stream_handle(stream))
-        n_hist = min(int(res.iterations), cap)
-        return st, res, [int(hist[i]) for i in range(n_hist)]
+        n_hist = int(res.iterations)
+        if n_hist <= cap:
+            return st, res, [int(hist[i]) for i in range(n_hist)]
+        return st, res, self.history()
+
+    def history(self) -> list[int]:
+        """edits_per_iteration of the plan's last run (pmsz_history)."""
+        cnt = ctypes.c_int64()
+        N.check(self.lib.pmsz_history(self.handle, None, 0, ctypes.byref(cnt)), "pmsz_history")
+        buf = (ctypes.c_int64 * max(1, cnt.value))()
+        N.check(self.lib.pmsz_history(self.handle, buf, cnt.value, ctypes.byref(cnt)), "pmsz_history")
+        return [int(buf[i]) for i in range(cnt.value)]
 
     def export_edits(self, g: torch.Tensor, stream=None) -> tuple[torch.Tensor, torch.Tensor]:
         cnt = ctypes.c_int64()
@@ -159,6 +176,13 @@ class DomainPlan:
         st = self.lib.pmsz_verify(self.handle, N.ptr(g), ctypes.byref(res), N.stream_handle(stream))
         N.check(st, "pmsz_verify")
         return [int(res.residual[k]) for k in range(6)]
+
+    def floor_violations(self, lower, g, stream=None) -> int:
+        """Vertices with g < lower (explicit-lower plans); arms the monotonicity check."""
+        out = ctypes.c_int64()
+        N.check(self.lib.pmsz_floor_violations(self.handle, N.ptr(lower), N.ptr(g), ctypes.byref(out),
+                                               N.stream_handle(stream)), "pmsz_floor_violations")
+        return int(out.value)
 
     def bounds_violations(self, f, g, stream=None) -> int:
         out = ctypes.c_int64()
@@ -214,6 +238,16 @@ def raise_for(status: int, res: N.PmszResult, f_host_values=None, fhat_host_valu
 
 def default_cap(xi: float, tau: float) -> int:
     return 10 * math.ceil(2.0 * xi / tau)
+
+
+def narrow_if_exact(f64: torch.Tensor) -> torch.Tensor | None:
+    """The f32 copy of a device f64 field when every value survives the round
+    trip (fields read from f32 files, codec.py:86-87), else None."""
+    out = torch.empty(f64.numel(), dtype=torch.float32, device=f64.device)
+    bad = ctypes.c_int64()
+    N.check(N.lib().pmsz_narrow_f32(N.ptr(f64), f64.numel(), N.ptr(out), ctypes.byref(bad), N.stream_handle()),
+            "pmsz_narrow_f32")
+    return out if bad.value == 0 else None
 
 
 def as_device_f64(values: np.ndarray, device) -> torch.Tensor:

@@ -25,7 +25,7 @@ import torch
 
 from . import _native as N
 from .correction import CorrectionConfig, CorrectionResult, EditSet
-from .engine import (BoundViolationError, ConvergenceError, DomainPlan, DomainSpec, as_device_f64,
+from .engine import (BoundViolationError, ConvergenceError, DomainPlan, DomainSpec, as_device_f64, narrow_if_exact,
                      raise_for)
 from .grid import ScalarField
 from .topology import DistortionReport
@@ -150,13 +150,15 @@ class _DevBlock:
         self.spec = block_domain(block, dims)
         ed = self.spec.dims
         n = ed[0] * ed[1] * ed[2]
-        self.f = torch.empty(n, dtype=torch.float64, device=f.device)
+        f32 = f.dtype == torch.float32   # an f32-exact original (narrow_if_exact)
+        self.f = torch.empty(n, dtype=f.dtype, device=f.device)
         self.fh = torch.empty(n, dtype=torch.float64, device=f.device)
-        for src, dst in ((f, self.f), (fh, self.fh)):
-            N.check(N.lib().pmsz_box_extract(N.ivec(dims), N.ptr(src), 0, N.ivec(block.ext_start),
+        for src, dst, is32 in ((f, self.f, int(f32)), (fh, self.fh, 0)):
+            N.check(N.lib().pmsz_box_extract(N.ivec(dims), N.ptr(src), is32, N.ivec(block.ext_start),
                                              N.ivec(ed), N.ptr(dst), N.stream_handle()), "pmsz_box_extract")
         self.g = torch.empty_like(self.fh)
-        self.plan = DomainPlan(self.spec, cfg.xi_abs, cfg.tau, cfg.max_outer_iterations, incremental=True)
+        self.plan = DomainPlan(self.spec, cfg.xi_abs, cfg.tau, cfg.max_outer_iterations, incremental=True,
+                               f32_original=f32)
         st, res = self.plan.prepare(self.f, self.fh, self.g)
         if st not in (N.PMSZ_OK,):
             raise_for(st, res, None, None, cfg.xi_abs, f_dev=self.f, fhat_dev=self.fh)
@@ -176,6 +178,113 @@ class _DevBlock:
         self.max_count = int(res.max_vertex_edits)
         self.shared_dirty = self.shared_dirty or bool(res.shared_dirty)
         return e
+
+
+def _merge_min_arrays(blocks, dims, arrays: list[torch.Tensor], acc: torch.Tensor) -> bool:
+    """All replicas <- min over replicas for raw per-block ext arrays (device
+    f64 tensors, updated in place); returns whether anything changed
+    (parallel.py:122-140)."""
+    L = N.lib()
+    s = N.stream_handle()
+    acc.fill_(float("inf"))
+    zero = (0, 0, 0)
+    for b, g in zip(blocks, arrays):
+        hi = tuple(b.ext_start[a] + b.ext_dims[a] for a in range(3))
+        N.check(L.pmsz_box_unpack_min(dims[0], dims[1], dims[2], N.ptr(acc), N.ivec(b.ext_start), N.ivec(hi),
+                                      N.ptr(g), None, s), "pmsz_box_unpack_min")
+    changed = torch.zeros(1, dtype=torch.int64, device=acc.device)
+    for b, g in zip(blocks, arrays):
+        ed = b.ext_dims
+        hi = tuple(b.ext_start[a] + ed[a] for a in range(3))
+        merged = torch.empty_like(g)
+        N.check(L.pmsz_box_pack(dims[0], dims[1], dims[2], N.ptr(acc), N.ivec(b.ext_start), N.ivec(hi),
+                                N.ptr(merged), s), "pmsz_box_pack")
+        N.check(L.pmsz_box_unpack_copy(ed[0], ed[1], ed[2], N.ptr(g), N.ivec(zero), N.ivec(ed), N.ptr(merged),
+                                       N.ptr(changed), s), "pmsz_box_unpack_copy")
+    return bool(changed.item() > 0)
+
+
+def sync_ghosts(decomposition: BlockDecomposition, g_exts) -> bool:
+    """Public one-shot ghost exchange over raw per-block arrays
+    (parallel.py:143-147): every replicated vertex <- the minimum over its
+    replicas, in place; returns whether anything changed.  Host numpy arrays
+    are merged on the device and written back into the same arrays; CUDA
+    float64 tensors are merged in place."""
+    if len(g_exts) != len(decomposition.blocks):
+        raise ValueError("one array per block required")
+    dims = decomposition.dims
+    dev = torch.device("cuda", torch.cuda.current_device())
+    arrays = []
+    for b, a in zip(decomposition.blocks, g_exts):
+        n = b.ext_dims[0] * b.ext_dims[1] * b.ext_dims[2]
+        if isinstance(a, torch.Tensor) and a.is_cuda and a.dtype == torch.float64 and a.is_contiguous():
+            t = a.view(-1)
+        else:
+            t = as_device_f64(np.asarray(a).reshape(-1), dev)
+        if t.numel() != n:
+            raise ValueError(f"block {b.index}: array has {t.numel()} values, ext extent has {n}")
+        arrays.append(t)
+    acc = torch.empty(dims[0] * dims[1] * dims[2], dtype=torch.float64, device=dev)
+    changed = _merge_min_arrays(decomposition.blocks, dims, arrays, acc)
+    for a, t in zip(g_exts, arrays):
+        if not (isinstance(a, torch.Tensor) and a.is_cuda):
+            np.asarray(a).reshape(-1)[:] = t.cpu().numpy()
+    return changed
+
+
+def local_converge(block: Block, f_ext, g_ext, lower_ext, config: CorrectionConfig
+                   ) -> tuple[np.ndarray, int, int]:
+    """Iterate one block to its local fixpoint, ghosts held fixed apart from
+    the block's own edits (parallel.py:150-172): centres are the block's core,
+    every ext vertex may be edited.  Returns (new g_ext, iterations counting
+    the final zero-edit pass, total edits); g_ext itself is not modified.
+
+    When ``lower_ext`` is exactly ``f_ext - xi`` and g_ext satisfies the error
+    bound (the reference's own use) this is one device plan with the usual
+    robust-centre skipping; otherwise the plan evaluates every centre and
+    clamps to the given lower bound (PMSZ_FLAG_NO_ROBUST | PMSZ_FLAG_LOWER), so
+    arbitrary inputs behave as in the reference, including its monotonicity
+    AssertionError when g starts below the lower bound."""
+    ed = tuple(int(v) for v in block.ext_dims)
+    n = ed[0] * ed[1] * ed[2]
+    dev = torch.device("cuda", torch.cuda.current_device())
+    f = as_device_f64(np.asarray(f_ext).reshape(-1), dev)
+    g0 = as_device_f64(np.asarray(g_ext).reshape(-1), dev)
+    lower = as_device_f64(np.asarray(lower_ext).reshape(-1), dev)
+    if not (f.numel() == g0.numel() == lower.numel() == n):
+        raise ValueError(f"block {block.index}: arrays must hold the {n} values of the ext extent")
+    lo = tuple(block.core_start[a] - block.ext_start[a] for a in range(3))
+    hi = tuple(block.core_stop[a] - block.ext_start[a] for a in range(3))
+    spec = DomainSpec(ed, lo, hi)
+    cap = config.max_outer_iterations
+    g = torch.empty_like(g0)
+    exact = bool(torch.equal(lower, f - config.xi_abs))   # the IEEE subtraction numpy performs
+    plan = None
+    if exact:
+        plan = DomainPlan(spec, config.xi_abs, config.tau, cap, incremental=True)
+        st, res = plan.prepare(f, g0, g)
+        if st == N.PMSZ_ERR_BOUND:   # g outside [f - xi, f + xi]: robust skipping is not valid
+            plan.close()
+            plan = None
+        elif st != N.PMSZ_OK:
+            raise_for(st, res, None, None, config.xi_abs, f_dev=f, fhat_dev=g0)
+    operand = f
+    if plan is None:
+        plan = DomainPlan(spec, config.xi_abs, config.tau, cap, incremental=True, no_robust=True,
+                          explicit_lower=True)
+        st, res = plan.prepare(f, g0, g)
+        if st not in (N.PMSZ_OK, N.PMSZ_ERR_BOUND):
+            raise_for(st, res, None, None, config.xi_abs, f_dev=f, fhat_dev=g0)
+        plan.floor_violations(lower, g)
+        operand = lower
+    try:
+        st, _, res = plan.block_round(operand, g, lockstep=False)
+        if st == N.PMSZ_ERR_CONVERGENCE:
+            raise ConvergenceError(f"block {block.index} found no zero-edit iteration within {cap}")
+        raise_for(st, res)
+        return g.cpu().numpy(), int(res.iterations), int(res.edit_count)
+    finally:
+        plan.close()
 
 
 def _merge_min(blocks: list[_DevBlock], dims, acc: torch.Tensor) -> bool:
@@ -224,7 +333,8 @@ def run_parallel(original: ScalarField, decompressed: ScalarField, config: Corre
     st, res = gplan.prepare(f, fh, scratch)
     raise_for(st, res, original.values, decompressed.values, config.xi_abs)
     decomp = decompose(dims, block_grid)
-    blocks = [_DevBlock(b, dims, config, f, fh) for b in decomp.blocks]
+    f32 = narrow_if_exact(f)   # f32-exact originals run the f32 K0 in every block
+    blocks = [_DevBlock(b, dims, config, f if f32 is None else f32, fh) for b in decomp.blocks]
     lockstep = strategy is SyncStrategy.LOCKSTEP
     rounds = syncs = 0
     totals: list[int] = []

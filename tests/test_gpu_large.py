@@ -1,0 +1,185 @@
+"""Parity at the BENCHMARK sizes.
+
+* 256^3 and 512^3 (BASELINE config 2): inputs regenerated on the device and
+  checked against the digests of the reference's own inputs, then the
+  corrected field, the edit record and the schedule compared with the
+  reference's own run_correction / run_parallel results
+  (tests/golden/golden_large.json, made by tests/golden/make_golden_large.py
+  in the build container -- the reference took ~48 min for 512^3).
+* 1024^3 (config 4) and the 2048 x 2048 x 256 peak stack (config 5), where the
+  CPU reference does not fit: multi-block LOCKSTEP on one GPU
+  (dist.run_local, the engine of the multi-GPU path) must equal the
+  single-domain run bit for bit (test_parallel.py:207-216 is the reference's
+  lockstep == serial contract), and the corrected field must pass an
+  independent full detection sweep (K4, pmsz_verify) and the GPU
+  compare_plmss -- not just the incremental detection bookkeeping.
+"""
+
+import hashlib
+import json
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import GOLDEN
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+
+def sha(t) -> str:
+    a = t.detach().cpu().numpy() if isinstance(t, torch.Tensor) else t
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+@pytest.fixture(scope="module")
+def large():
+    p = GOLDEN / "golden_large.json"
+    return json.loads(p.read_text())
+
+
+def _inputs(n, seed, rel):
+    from paper_2601_01787_b200 import inputs as gen
+    dims = (n, n, n)
+    f32 = gen.perlin_device(gen.NoiseSpec(dims, seed), f32=True)
+    lo, hi = gen.minmax_device(f32)
+    xi = gen.relative_to_absolute_range(lo, hi, rel)
+    fh = gen.quantize_device(f32, xi, lo, hi)
+    return dims, f32, fh, xi
+
+
+def _independent_checks(f32, g, dims, xi, extrema_only=False):
+    """Full K4 count sweep + dense bound check + GPU compare_plmss on the final field."""
+    import paper_2601_01787_b200 as pm
+    from paper_2601_01787_b200.engine import DomainPlan, DomainSpec
+    plan = DomainPlan(DomainSpec.whole(dims), xi, xi / 1024.0, 1, incremental=False, f32_original=True,
+                      extrema_only=extrema_only, no_robust=True)
+    scratch = torch.empty_like(g)
+    st, _ = plan.prepare(f32, g, scratch)   # exact f-code at every centre (no robust skipping)
+    assert st == 0
+    kinds = plan.verify(g)
+    assert kinds == [0] * 6, kinds
+    assert plan.bounds_violations(f32, g) == 0
+    plan.close()
+    del scratch
+    if not extrema_only:
+        rep = pm.topology.compare_plmss_device(f32, g, dims, with_sets=False)
+        assert rep.is_clean, rep.counts()
+
+
+@pytest.mark.parametrize("key", ["c256", "c512"])
+def test_serial_matches_reference_digest(large, key):
+    import paper_2601_01787_b200 as pm
+    if key not in large:
+        pytest.skip(f"{key} digests not generated (make_golden_large.py)")
+    ref = large[key]
+    dims, f32, fh, xi = _inputs(ref["dims"][0], ref["seed"], ref["rel"])
+    assert xi == ref["xi"]
+    assert sha(f32) == ref["f32_sha256"] and sha(fh) == ref["fhat_sha256"]
+    cfg = pm.CorrectionConfig(xi_abs=xi)
+    s = ref["serial"]
+    for incremental in (True, False):
+        res = pm.run_correction_device(f32, fh, dims, cfg, incremental=incremental)
+        assert list(res.edits_per_iteration) == s["edits_per_iteration"]
+        assert res.max_vertex_edits == s["max_vertex_edits"]
+        assert sha(res.corrected) == s["corrected_sha256"]
+        assert sha(res.edit_ids) == s["ids_sha256"] and sha(res.edit_values) == s["vals_sha256"]
+    _independent_checks(f32, res.corrected, dims, xi)
+
+
+def test_run_parallel_matches_reference_digest_256(large):
+    """The drop-in run_parallel at 256^3 against the reference's own
+    run_parallel (relaxed on three grids, lockstep on (2,2,2)): stats, schedule,
+    corrected field."""
+    import paper_2601_01787_b200 as pm
+    if "c256" not in large:
+        pytest.skip("c256 digests not generated")
+    ref = large["c256"]
+    dims, f32, fh, xi = _inputs(256, ref["seed"], ref["rel"])
+    f = pm.ScalarField(dims, f32.double().cpu().numpy())
+    fhat = pm.ScalarField(dims, fh.cpu().numpy())
+    cfg = pm.CorrectionConfig(xi_abs=xi)
+    for case in ref["parallel"]:
+        res, st = pm.run_parallel(f, fhat, cfg, tuple(case["grid"]), pm.SyncStrategy(case["strategy"]))
+        d = st.to_dict()
+        d.pop("timings")
+        assert d == case["stats"], case["grid"]
+        assert list(res.edits_per_iteration) == case["edits_per_iteration"]
+        assert res.iterations == case["iterations"] and res.max_vertex_edits == case["max_vertex_edits"]
+        assert sha(res.corrected.values) == case["corrected_sha256"], (case["grid"], case["strategy"])
+        assert sha(res.edits.ids) == case["ids_sha256"]
+
+
+def _lockstep_local(f32, fh, dims, cfg, grid, extrema_only=False):
+    """dist.run_local with one DeviceEngine per block on this GPU; returns the
+    assembled corrected field (cores) and the round totals."""
+    from paper_2601_01787_b200 import _native as N
+    from paper_2601_01787_b200.dist import DeviceEngine, run_local
+    from paper_2601_01787_b200.parallel import decompose
+    blocks = decompose(dims, grid).blocks
+    engines = []
+    L = N.lib()
+    for b in blocks:
+        ed = b.ext_dims
+        n = ed[0] * ed[1] * ed[2]
+        fe = torch.empty(n, dtype=torch.float32, device=f32.device)
+        he = torch.empty(n, dtype=torch.float64, device=f32.device)
+        N.check(L.pmsz_box_extract(N.ivec(dims), N.ptr(f32), 1, N.ivec(b.ext_start), N.ivec(ed), N.ptr(fe),
+                                   N.stream_handle()), "extract")
+        N.check(L.pmsz_box_extract(N.ivec(dims), N.ptr(fh), 0, N.ivec(b.ext_start), N.ivec(ed), N.ptr(he),
+                                   N.stream_handle()), "extract")
+        e = DeviceEngine(b, dims, fe, he, cfg, extrema_only=extrema_only)
+        e.prepare()
+        engines.append(e)
+    st = run_local(engines, blocks, grid, lockstep=True, cap=cfg.max_outer_iterations)
+    out = torch.empty_like(fh)
+    for b, e in zip(blocks, engines):
+        ed = e.spec.dims
+        lo = tuple(b.core_start[a] - b.ext_start[a] for a in range(3))
+        hi = tuple(b.core_stop[a] - b.ext_start[a] for a in range(3))
+        cd = tuple(hi[a] - lo[a] for a in range(3))
+        buf = torch.empty(cd[0] * cd[1] * cd[2], dtype=torch.float64, device=fh.device)
+        N.check(L.pmsz_box_pack(ed[0], ed[1], ed[2], N.ptr(e.g), N.ivec(lo), N.ivec(hi), N.ptr(buf),
+                                N.stream_handle()), "pack")
+        N.check(L.pmsz_box_unpack_copy(dims[0], dims[1], dims[2], N.ptr(out), N.ivec(b.core_start),
+                                       N.ivec(b.core_stop), N.ptr(buf), None, N.stream_handle()), "unpack")
+        e.plan.close()
+    return out, st
+
+
+@pytest.mark.parametrize("workload", ["perlin1024", "hedm"])
+def test_lockstep_blocks_equal_single_domain_at_size(workload):
+    """SURVEY H9 for the configs the CPU reference cannot hold: lockstep over
+    blocks == one domain, bit for bit, and an independent final verification."""
+    import paper_2601_01787_b200 as pm
+    from paper_2601_01787_b200 import inputs as gen
+    free, _ = torch.cuda.mem_get_info()
+    if free < 120e9:
+        pytest.skip("needs a 180 GB B200")
+    if workload == "hedm":
+        dims, eo = (2048, 2048, 256), True
+        f32 = gen.gaussian_peaks_device(gen.PeakSpec(dims, 0), f32=True)
+        grids = [(1, 2, 1), (2, 2, 2)]
+    else:
+        dims, eo = (1024, 1024, 1024), False
+        f32 = gen.perlin_device(gen.NoiseSpec(dims, 0), f32=True)
+        grids = [(1, 1, 2), (2, 2, 2)]
+    lo, hi = gen.minmax_device(f32)
+    xi = gen.relative_to_absolute_range(lo, hi, 1e-4)
+    fh = gen.quantize_device(f32, xi, lo, hi)
+    cfg = pm.CorrectionConfig(xi_abs=xi)
+    single = pm.run_correction_device(f32, fh, dims, cfg, extrema_only=eo, export_edits=False)
+    ref_sha = sha(single.corrected)
+    hist = list(single.edits_per_iteration)
+    _independent_checks(f32, single.corrected, dims, xi, extrema_only=eo)
+    del single
+    pm.correction._PLAN_CACHE.clear()
+    torch.cuda.empty_cache()
+    for grid in grids:
+        out, st = _lockstep_local(f32, fh, dims, cfg, grid, extrema_only=eo)
+        assert sha(out) == ref_sha, grid
+        # a lockstep round is one serial iteration (its edit total counts
+        # replicated vertices once per block, so only the length compares)
+        assert st.rounds == len(hist), grid
+        del out
+        torch.cuda.empty_cache()

@@ -471,31 +471,18 @@ def test_robust_skipping_changes_nothing(monkeypatch):
 
 def test_floor_violation_raises_like_the_reference():
     """Hazard H6: fhat below fl(f - xi) although the rounded |f - fhat| <= xi
-    check passes.  The reference raises its monotonicity AssertionError in the first
-    iteration with a detection (correction.py:239-241); the GPU path (robust
+    check passes.  The reference itself raised its monotonicity AssertionError
+    on this input (tests/golden/make_golden_api.py, outcome pinned in
+    golden_api.json; correction.py:239-241); the oracle and the GPU path (robust
     classification and K0-fused first sweep included) must do the same."""
-    from fractions import Fraction
-    dims = (48, 40, 32)
-    f = orc.perlin(dims, 5)
-    xi = orc.relative_to_absolute(f, 1e-3)
-    fh = orc.quantize(f, xi).copy()
-    hit = 0
-    for i in range(0, f.size, 7):
-        lower = f[i] - xi
-        if Fraction(lower) > Fraction(f[i]) - Fraction(xi):          # f - xi rounded up
-            cand = np.nextafter(lower, -np.inf)
-            if abs(f[i] - cand) <= xi:           # passes the rounded check of correction.py:52-60
-                fh[i] = cand
-                hit += 1
-                if hit == 3:
-                    break
-    assert hit > 0
-    ref = orc.run_correction(dims, f, fh, xi)
-    cfg = pm.CorrectionConfig(xi_abs=xi)
-    if ref.status == orc.ORC_MONOTONE:
-        with pytest.raises(AssertionError):
-            pm.run_correction(pm.ScalarField(dims, f), pm.ScalarField(dims, fh), cfg)
-    else:
-        assert ref.status == orc.ORC_OK
-        res = pm.run_correction(pm.ScalarField(dims, f), pm.ScalarField(dims, fh), cfg)
-        assert np.array_equal(res.corrected.values, ref.corrected)
+    import json
+    from conftest import GOLDEN
+    meta = json.loads((GOLDEN / "golden_api.json").read_text())["h6"]
+    fh = np.load(GOLDEN / "golden_api.npz")["h6_fhat"]
+    dims = tuple(meta["dims"])
+    f = orc.perlin(dims, meta["seed"])
+    xi = meta["xi"]
+    assert meta["outcome"] == "AssertionError" and len(meta["indices"]) > 0
+    assert orc.run_correction(dims, f, fh, xi).status == orc.ORC_MONOTONE
+    with pytest.raises(AssertionError):
+        pm.run_correction(pm.ScalarField(dims, f), pm.ScalarField(dims, fh), pm.CorrectionConfig(xi_abs=xi))
