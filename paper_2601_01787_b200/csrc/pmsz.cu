@@ -30,6 +30,7 @@
 #include "gather.cuh"
 #include "qsweep.cuh"
 #include "prep.cuh"
+#include "prep2.cuh"
 #include "segment.cuh"
 
 using namespace pmsz;
@@ -477,6 +478,7 @@ struct pmsz_plan {
     long long prof_n[PMSZ_K_COUNT] = {};
     // device-resident tail (k_tail)
     bool tail_on = true;
+    bool tail1_on = true;                 // small dirty sets in the one-CTA shared-memory tail (k_tail1)
     TailState* tail = nullptr;
     TailState* htail = nullptr;          // pinned mirror
     unsigned long long* thist = nullptr;  // per-iteration edits of one tail launch
@@ -496,6 +498,8 @@ struct pmsz_plan {
     bool fuse_on = true;                  // K0 also runs the first detection sweep (prep.cuh)
     bool qmask_ok = false;                // dense masked iterations can use the TMA queue sweep (kMaskedQ)
     bool k0_detected = false;             // detbits / ndetect of the first iteration come from K0
+    bool k0_rules = false;                // ... and its proposals are already in prop / touched (prep2.cuh)
+    bool prep2_on = true;                 // K0 = the fused producer / consumer kernel of prep2.cuh
     uint32_t* frag = nullptr;             // fragile-centre bitmap written by K0
     int64_t hist_chunk = 0;               // thist / hthist entries: iterations per tail launch
     std::vector<int64_t> hist_all;        // edits_per_iteration of the last pmsz_run_correction
@@ -685,6 +689,10 @@ pmsz_status iterate_once(pmsz_plan* p, const void* f, double* g, cudaStream_t s)
     // other per-iteration counter is still zero from reset_run_state)
     const bool predetected = mode == kFull && p->k0_detected;
     p->k0_detected = false;
+    // the rules of this iteration's mismatches already ran: inside K0 (prep2.cuh)
+    // or inside the TMA queue sweep below; otherwise k_defer runs them
+    bool ruled = predetected && p->k0_rules;
+    p->k0_rules = false;
     pmsz_status st = predetected ? PMSZ_OK : reset_iter(p, s, nxt);
     if (st) return st;
     const int64_t cx = d.hi[0] - d.lo[0], cy = d.hi[1] - d.lo[1], cz = d.hi[2] - d.lo[2];
@@ -698,7 +706,9 @@ pmsz_status iterate_once(pmsz_plan* p, const void* f, double* g, cudaStream_t s)
         p->w.track = 0;
         if (nonempty && !predetected) {
             ProfScope ps(p, s, PMSZ_K_SWEEP_FULL);
-            if (!(p->qsweep_on && launch_sweep_q<false>(d, g, p->w, s))) launch_sweep_full<false>(d, g, p->w, s);
+            // the TMA queue sweep runs the rules of its mismatches itself
+            ruled = p->qsweep_on && launch_sweep_q<false>(d, g, p->w, s);
+            if (!ruled) launch_sweep_full<false>(d, g, p->w, s);
             LAUNCHED();
         }
     } else if (mode == kMasked || mode == kMaskedList || mode == kMaskedQ) {
@@ -735,14 +745,14 @@ pmsz_status iterate_once(pmsz_plan* p, const void* f, double* g, cudaStream_t s)
         } else {
             if (nonempty) {
                 ProfScope ps(p, s, PMSZ_K_SWEEP_MASKED);
-                if (!(p->qsweep_on && launch_sweep_q<false>(d, g, p->w, s, p->w.actbits)))
-                    launch_sweep_full<false>(d, g, p->w, s, p->w.actbits);
+                ruled = p->qsweep_on && launch_sweep_q<false>(d, g, p->w, s, p->w.actbits);
+                if (!ruled) launch_sweep_full<false>(d, g, p->w, s, p->w.actbits);
                 LAUNCHED();
             }
             CUDA_TRY(cudaMemsetAsync(p->w.actbits, 0, p->nwords * 4, s));
         }
     }
-    if (mode != kList && nonempty && !gather) {
+    if (mode != kList && nonempty && !gather && !ruled) {
         // centres with a detection (bitmap set by the tiled sweep) -> list -> rules
         {
             ProfScope ps(p, s, PMSZ_K_COMPACT);
@@ -821,7 +831,10 @@ pmsz_status launch_tail(pmsz_plan* p, const void* f, double* g, cudaStream_t s, 
         tr = trace_buf;
         CUDA_TRY(cudaMemsetAsync(tr, 0, 2 * 8 * 4096, s));
     }
-    void* args[] = {&d, &fp, &g, &w, &cur, &sorted, &sort_min, &dense_min, &cc, &budget, &h, &t, &tr};
+    static const int64_t t1max = getenv("PMSZ_TAIL1_MAX") ? atoll(getenv("PMSZ_TAIL1_MAX")) : kT1Handover;
+    unsigned long long small_max =
+        p->tail1_on ? (unsigned long long)std::min<int64_t>(std::min<int64_t>(t1max, kT1Dirty), (int64_t)p->w.act_cap) : 0ull;
+    void* args[] = {&d, &fp, &g, &w, &cur, &sorted, &sort_min, &dense_min, &cc, &budget, &h, &t, &tr, &small_max};
     CUDA_TRY(cudaLaunchCooperativeKernel((const void*)k_tail<FT>, dim3(nb), dim3(256), args, 0, s));
     LAUNCHED();
     if (trace) {
@@ -842,6 +855,45 @@ pmsz_status launch_tail(pmsz_plan* p, const void* f, double* g, cudaStream_t s, 
     return PMSZ_OK;
 }
 
+// Small dirty sets: the one-CTA shared-memory tail (k_tail1, tail.cuh).
+template <typename FT>
+pmsz_status launch_tail1(pmsz_plan* p, const void* f, double* g, cudaStream_t s, long long budget, int chained) {
+    static bool attr = false;
+    if (!attr) {
+        CUDA_TRY(cudaFuncSetAttribute(k_tail1<FT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kT1SmemBytes));
+        attr = true;
+    }
+    static const bool trace = getenv("PMSZ_TAIL_TRACE") != nullptr;
+    static unsigned long long* trace_buf = nullptr;
+    unsigned long long* tr = nullptr;
+    if (trace) {
+        if (!trace_buf) CUDA_TRY(cudaMalloc(&trace_buf, 2 * 8 * 4096));
+        tr = trace_buf;
+        CUDA_TRY(cudaMemsetAsync(tr, 0, 2 * 8 * 4096, s));
+    }
+    static const int var = getenv("PMSZ_T1V") ? atoi(getenv("PMSZ_T1V")) : 0;
+    k_tail1<FT><<<1, kT1Threads, kT1SmemBytes, s>>>(p->dom, (const FT*)f, g, p->w, p->cur, budget, p->thist, p->tail, tr,
+                                                     chained, var);
+    LAUNCHED();
+    if (trace) {
+        std::vector<unsigned long long> h2(2 * 4096);
+        cudaMemcpyAsync(h2.data(), tr, h2.size() * 8, cudaMemcpyDeviceToHost, s);
+        cudaStreamSynchronize(s);
+        fprintf(stderr, "tail1 cur=%d pending=%lld:", p->cur, (long long)p->pending);
+        for (int i = 0; i < 4000 && h2[2 * i]; ++i)
+            fprintf(stderr, " %.1fus/%llu", (h2[2 * i] - (i ? h2[2 * i - 2] : h2[8190])) / 1e3, h2[2 * i + 1]);
+        fprintf(stderr, "\n  cycles pre/S/A/post (edits):");
+        for (int i = 0; i < 90 && h2[2 * i]; ++i) {
+            const long long pre = i ? (long long)(h2[7000 + i] - h2[7100 + i - 1]) : 0;
+            fprintf(stderr, " [%lld %lld %lld %lld (%llu)]", pre, (long long)(h2[8000 + 2 * i] - h2[7000 + i]),
+                    (long long)(h2[8001 + 2 * i] - h2[8000 + 2 * i]), (long long)(h2[7100 + i] - h2[8001 + 2 * i]),
+                    h2[7200 + i]);
+        }
+        fprintf(stderr, "\n");
+    }
+    return PMSZ_OK;
+}
+
 // Run up to `budget` list-mode iterations in one k_tail launch and bring the
 // plan state to where iterate_once would have left it.  Per-iteration edit
 // counts land in p->hthist[0 .. *k).
@@ -850,10 +902,20 @@ pmsz_status tail_step(pmsz_plan* p, const void* f, double* g, cudaStream_t s, lo
     p->edits_cached = -1;
     pmsz_status st = reset_iter(p, s, p->cur ^ 1);
     if (st) return st;
-    const int sorted = sort_pending(p, s);
+    static const int64_t t1max = getenv("PMSZ_TAIL1_MAX") ? atoll(getenv("PMSZ_TAIL1_MAX")) : kT1Handover;
+    const bool micro = p->tail1_on && !p->bits_only && p->pending > 0 &&
+                       p->pending <= std::min<int64_t>(std::min<int64_t>(t1max, kT1Dirty), (int64_t)p->w.act_cap);
+    const int sorted = micro ? 0 : sort_pending(p, s);
     {
         ProfScope ps(p, s, PMSZ_K_TAIL);
-        st = p->f32 ? launch_tail<float>(p, f, g, s, budget, sorted) : launch_tail<double>(p, f, g, s, budget, sorted);
+        if (micro) {
+            st = p->f32 ? launch_tail1<float>(p, f, g, s, budget, 0) : launch_tail1<double>(p, f, g, s, budget, 0);
+        } else {
+            st = p->f32 ? launch_tail<float>(p, f, g, s, budget, sorted) : launch_tail<double>(p, f, g, s, budget, sorted);
+            // the grid tail hands a small dirty list straight to k_tail1 (kTailSmall)
+            if (!st && p->tail1_on)
+                st = p->f32 ? launch_tail1<float>(p, f, g, s, budget, 1) : launch_tail1<double>(p, f, g, s, budget, 1);
+        }
         if (st) return st;
     }
     CUDA_TRY(cudaMemcpyAsync(p->htail, p->tail, sizeof(TailState), cudaMemcpyDeviceToHost, s));
@@ -927,9 +989,26 @@ pmsz_status prep(pmsz_plan* p, const void* f, const double* fh, double* g, cudaS
         // K0 also runs the first detection sweep (g = fhat) unless told otherwise
         uint32_t* det = p->fuse_on ? p->w.detbits : nullptr;
         if (det) CUDA_TRY(cudaMemsetAsync(det, 0, p->nwords * 4, s));
-        bool queued = false;
+        bool queued = false, fused = false;
         const size_t nsl = p->stage_pending ? p->stage_z.size() - 1 : 0;
-        if (p->qprep_on && nsl > 0) {
+        const bool try2 = p->prep2_on && p->qprep_on && det != nullptr && p->frag_out() != nullptr;
+        if (try2) {
+            // fused K0 (prep2.cuh): the first iteration's detection and rules included
+            const size_t n2 = nsl > 0 ? nsl : 1;
+            for (size_t c = 0; c < n2; ++c) {
+                const int64_t za = nsl > 0 ? p->stage_z[c] : 0, zb2 = nsl > 0 ? p->stage_z[c + 1] : p->dom.nz;
+                if (nsl > 0) CUDA_TRY(cudaStreamWaitEvent(s, p->stage_ev[1 + std::min(c + 1, nsl - 1)], 0));
+                fused = p->f32 ? launch_prep2<float>(p->dom, (const float*)f, fh, g, p->w.code, p->frag_out(), p->ctr,
+                                                     det, p->w, s, za, zb2)
+                               : launch_prep2<double>(p->dom, (const double*)f, fh, g, p->w.code, p->frag_out(),
+                                                      p->ctr, det, p->w, s, za, zb2);
+                if (!fused) break;   // nothing was launched
+                if (c + 1 < n2) LAUNCHED();
+            }
+            queued = fused;
+        }
+        if (queued) {
+        } else if (p->qprep_on && nsl > 0) {
             // input still arriving in z-slabs: K0 over slab c once slab c and
             // the first plane of slab c + 1 (its upper halo) have landed
             for (size_t c = 0; c < nsl; ++c) {
@@ -948,6 +1027,7 @@ pmsz_status prep(pmsz_plan* p, const void* f, const double* fh, double* g, cudaS
         if (nsl > 0) CUDA_TRY(cudaStreamWaitEvent(s, p->stage_ev[nsl], 0));   // every slab is in
         p->stage_pending = false;
         p->k0_detected = queued && det != nullptr;
+        p->k0_rules = fused;
         if (!queued) {
             if (p->f32)
                 launch_prep<float>(p->dom, (const float*)f, fh, g, p->w.code, p->frag_out(), p->ctr, s);
@@ -1150,6 +1230,8 @@ pmsz_status pmsz_plan_create(const pmsz_desc* desc, pmsz_plan** out) {
     if (const char* e = getenv("PMSZ_QSWEEP")) p->qsweep_on = atoi(e) != 0;
     if (const char* e = getenv("PMSZ_QPREP")) p->qprep_on = atoi(e) != 0;
     if (const char* e = getenv("PMSZ_FUSE")) p->fuse_on = atoi(e) != 0;
+    if (const char* e = getenv("PMSZ_TAIL1")) p->tail1_on = atoi(e) != 0;
+    if (const char* e = getenv("PMSZ_PREP2")) p->prep2_on = atoi(e) != 0;
     // measured: the dense masked queue sweep (0.45 ms) plus the dilation (0.08 ms)
     // do not beat the plain queue sweep (0.49 ms) at 512^3, so it is opt-in
     p->qmask_ok = p->qsweep_on && p->gather_on && qsweep_masked_ok(p->dom) && getenv("PMSZ_QMASK") &&
@@ -1305,10 +1387,17 @@ pmsz_status pmsz_block_round(pmsz_plan* p, const void* f, double* g, int32_t loc
     return fail(PMSZ_ERR_CONVERGENCE, "block found no zero-edit iteration within the cap");
 }
 
+// Something may change g before the first iteration: K0's detections (and,
+// with prep2.cuh, its proposals) are stale.
+static void drop_k0(pmsz_plan* p, cudaStream_t s) {
+    if (p->k0_rules) restore_prop(p, s);
+    p->k0_rules = false;
+    p->k0_detected = false;
+}
+
 pmsz_status pmsz_mark_all_dirty(pmsz_plan* p, void* stream) {
-    (void)stream;
     if (!p) return fail(PMSZ_ERR_INVALID, "null plan");
-    p->k0_detected = false;   // g may change before the first iteration: K0's detections are stale
+    drop_k0(p, S(stream));   // g may change before the first iteration: K0's detections are stale
     p->next_mode = kFull;
     return PMSZ_OK;
 }
@@ -1336,7 +1425,7 @@ static pmsz_status after_mark(pmsz_plan* p, cudaStream_t s) {
 
 pmsz_status pmsz_mark_dirty_ids(pmsz_plan* p, const uint32_t* ids, int64_t count, void* stream) {
     if (!p) return fail(PMSZ_ERR_INVALID, "null plan");
-    p->k0_detected = false;   // g may change before the first iteration: K0's detections are stale
+    drop_k0(p, S(stream));   // g may change before the first iteration: K0's detections are stale
     if (!p->w.incremental || p->next_mode == kFull || count <= 0) return PMSZ_OK;
     cudaStream_t s = S(stream);
     k_mark_ids<<<grid_for(count, 256), 256, 0, s>>>(p->dom, p->w, ids, count, p->cur,
@@ -1348,7 +1437,7 @@ pmsz_status pmsz_mark_dirty_ids(pmsz_plan* p, const uint32_t* ids, int64_t count
 pmsz_status pmsz_box_mark_changed(pmsz_plan* p, const int64_t lo[3], const int64_t hi[3], const double* before,
                                   const double* g, void* stream) {
     if (!p) return fail(PMSZ_ERR_INVALID, "null plan");
-    p->k0_detected = false;   // g may change before the first iteration: K0's detections are stale
+    drop_k0(p, S(stream));   // g may change before the first iteration: K0's detections are stale
     if (!p->w.incremental || p->next_mode == kFull) return PMSZ_OK;
     cudaStream_t s = S(stream);
     Box b{p->dom.nx, p->dom.ny, {lo[0], lo[1], lo[2]}, {hi[0] - lo[0], hi[1] - lo[1], hi[2] - lo[2]}, 0, 0};
@@ -1371,7 +1460,7 @@ static pmsz_status flush_deferred_marks(pmsz_plan* p, cudaStream_t s) {
 pmsz_status pmsz_box_merge_min(pmsz_plan* p, double* g, const int64_t lo[3], const int64_t hi[3], const double* buf,
                                int64_t* changed_out, void* stream) {
     if (!p || !g || !buf) return fail(PMSZ_ERR_INVALID, "null argument");
-    p->k0_detected = false;   // g may change before the first iteration: K0's detections are stale
+    drop_k0(p, S(stream));   // g may change before the first iteration: K0's detections are stale
     cudaStream_t s = S(stream);
     Box b;
     if (!make_box(p->dom.nx, p->dom.ny, p->dom.nz, lo, hi, b)) return fail(PMSZ_ERR_INVALID, "box outside the domain");

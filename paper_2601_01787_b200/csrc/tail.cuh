@@ -35,7 +35,8 @@
 
 namespace pmsz {
 
-enum : unsigned long long { kTailConverged = 1, kTailBits = 2, kTailOverflow = 3, kTailBudget = 4, kTailSort = 5 };
+enum : unsigned long long { kTailConverged = 1, kTailBits = 2, kTailOverflow = 3, kTailBudget = 4, kTailSort = 5,
+                            kTailSmall = 6 /* the dirty list fits k_tail1, which runs next on the stream */ };
 
 struct TailState {
     unsigned long long iterations;   // iterations run by this launch
@@ -129,7 +130,7 @@ __global__ void __launch_bounds__(256) k_tail(Dom d, const FT* __restrict__ f, d
                                               int sorted, unsigned long long sort_min, unsigned long long dense_min,
                                               unsigned long long* __restrict__ chunk_counts, long long budget,
                                               unsigned long long* __restrict__ hist, TailState* ts,
-                                              unsigned long long* __restrict__ trace) {
+                                              unsigned long long* __restrict__ trace, unsigned long long small_max) {
     cg::grid_group grid = cg::this_grid();
     __shared__ unsigned warp_cnt[kTailWarps];
     const unsigned long long tid = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -196,6 +197,7 @@ __global__ void __launch_bounds__(256) k_tail(Dom d, const FT* __restrict__ f, d
         else if (mark != kMarkList) exit = kTailBits;
         else if (nact > w.act_cap) exit = kTailOverflow;
         else if (it + 1 >= budget) exit = kTailBudget;
+        else if (append && nact <= small_max) exit = kTailSmall;   // k_tail1 takes over on the device
         else if (!append || nact > sort_min) {
             // a long dirty set: rebuild the list sorted from actbits here, or
             // hand it to the host's gather path when it is longer still
@@ -236,6 +238,320 @@ __global__ void __launch_bounds__(256) k_tail(Dom d, const FT* __restrict__ f, d
             return;
         }
         cur = nxt;
+    }
+}
+
+}  // namespace pmsz
+
+namespace pmsz {
+
+// ---------------------------------------------------------------------------
+// k_tail1: the small-dirty-set iterations in ONE CTA.
+//
+// Late in the loop an iteration sweeps a few hundred centres and applies a
+// few dozen edits; the grid-wide tail above then pays its three grid
+// barriers and ~20 dependent L2 round trips per iteration (~15 us at 512^3).
+// Here one 1024-thread CTA keeps the dirty set, the proposal targets and the
+// iteration's edits in shared memory, and an iteration is two phases with
+// one L2 round trip each (plus the wait for the proposals' reductions):
+//
+//   S  ring gather + detection + rules of every dirty centre; proposals go to
+//      prop[] by RED.MIN as everywhere else, the target ids into a shared
+//      hash set (first insert wins, no global work list)
+//   A  per target: the apply operands AND the fragile bits of its closed
+//      1-ring are loaded together; the apply (K2 arithmetic), and for an edit
+//      the ring's core, fragile members go straight into a second shared
+//      hash set -> the next dirty list (the M phase of k_tail, fused)
+//
+// Same device functions as the list-mode iteration (load_ring, fold_scan,
+// rules, the apply arithmetic of apply_target), so results are bit-identical.
+// The entry list's actbits are cleared on entry; on a hand-back the pending
+// list is written to act[cur ^ 1] with its actbits set, exactly the state a
+// list-mode iteration leaves.  Overflow of any shared structure falls back to
+// the global structures (work list + touched bits for targets, mark_ring for
+// the next dirty set) and hands back to the host.
+constexpr int kT1Threads = 1024;
+constexpr int kT1Dirty = 4096;      // dirty-list capacity (ping-pong)
+constexpr int kT1Set = 8192;        // hash sets (targets / next dirty); power of two
+constexpr int kT1SetBits = 13;
+constexpr uint32_t kT1Empty = 0xffffffffu;
+// hand-over threshold of the grid tail: the one-CTA iteration beats the grid
+// barriers below about a thousand dirty centres (PMSZ_TAIL1_MAX overrides)
+constexpr int kT1Handover = 1024;
+
+struct T1Smem {
+    uint32_t dirty[2][kT1Dirty];
+    uint32_t tset[kT1Set];
+    uint32_t dset[kT1Set];
+    uint32_t edits[kT1Set];
+    unsigned nd[2];
+    unsigned nedit, ndet, shared, maxc, ovf_tgt, ovf_edit, ovf_mark;
+};
+constexpr size_t kT1SmemBytes = sizeof(T1Smem);
+
+// 1 = inserted, 0 = present, 2 = no free slot within the probe limit
+__device__ __forceinline__ int t1_insert(uint32_t* set, uint32_t u) {
+    const uint32_t h = (u * 2654435761u) >> (32 - kT1SetBits);
+#pragma unroll 1
+    for (int k = 0; k < 64; ++k) {
+        const uint32_t slot = (h + (uint32_t)k) & (uint32_t)(kT1Set - 1);
+        const uint32_t old = atomicCAS(set + slot, kT1Empty, u);
+        if (old == kT1Empty) return 1;
+        if (old == u) return 0;
+    }
+    return 2;
+}
+
+struct EmitT1 {
+    const Work& w;
+    T1Smem& S;
+    bool issued = false;
+    __device__ __forceinline__ void operator()(int64_t t, double val) {
+        atomicMin(w.prop + t, okey(val));
+        issued = true;
+        if (t1_insert(S.tset, (uint32_t)t) == 2) {
+            // set full: the global target list, deduplicated by the touched bit
+            S.ovf_tgt = 1;
+            const uint32_t bit = 1u << (t & 31);
+            if (!(atomicOr(w.touched + (t >> 5), bit) & bit)) w.work[agg_append(&w.ctr->nwork)] = (uint32_t)t;
+        }
+    }
+};
+
+// Apply target t (apply_target's arithmetic) and, for an edit, put the core,
+// fragile members of its closed 1-ring into the next dirty set.  The fragile
+// words of the ring are loaded with the apply operands (one round trip).
+template <typename FT>
+__device__ __forceinline__ void t1_apply_mark(const Dom& d, const FT* __restrict__ f, double* __restrict__ g,
+                                              const Work& w, T1Smem& S, int b, unsigned dcap, int64_t t,
+                                              ApplyAcc& acc) {
+    int64_t x, y, z;
+    coords(d, t, x, y, z);
+    uint32_t fw[15];
+#pragma unroll
+    for (int r = -1; r < 14; ++r) {
+        const int64_t px = x + (r < 0 ? 0 : rank_dx(r)), py = y + (r < 0 ? 0 : rank_dy(r)),
+                      pz = z + (r < 0 ? 0 : rank_dz(r));
+        const int64_t u = px + py * d.sy + pz * d.sz;
+        fw[r + 1] = !in_core(d, px, py, pz) ? 0u : (w.frag ? __ldg(w.frag + (u >> 5)) : ~0u);
+    }
+    const TargetOps op = load_target(f, g, w, t);
+    const double p = okey_inv(op.key);
+    w.prop[t] = kNoProposal;
+    const double gt = op.gt;
+    const double lower = op.fv - d.lxi;                  // BoundsField.lower (correction.py:122)
+    const double m = (p < gt) ? p : gt;                  // np.minimum(g, prop)
+    const double nv = (m < lower) ? lower : m;           // np.maximum(., lower)
+    if (nv == gt) return;
+    g[t] = nv;
+    ++acc.edits;
+    const unsigned int cnt = op.cnt + 1u;
+    if (w.counts32) ((unsigned int*)w.counts)[t] = cnt;
+    else ((uint16_t*)w.counts)[t] = (uint16_t)cnt;
+    acc.maxc = max(acc.maxc, cnt);
+    atomicOr(w.editbits + (t >> 5), 1u << (t & 31));
+    acc.shared |= in_shared(d, x, y, z);
+    const unsigned k = atomicAdd(&S.nedit, 1u);
+    if (k < (unsigned)kT1Set) {
+        S.edits[k] = (uint32_t)t;
+    } else {   // edit list full: the global one (marked globally at the hand-back)
+        S.ovf_edit = 1;
+        w.elist[agg_append(&w.ctr->nelist)] = (uint32_t)t;
+    }
+#pragma unroll
+    for (int r = -1; r < 14; ++r) {
+        const int64_t u = t + (r < 0 ? 0 : rank_off(d, r));
+        if (!((fw[r + 1] >> (u & 31)) & 1u)) continue;   // outside the core, or robust (never evaluated)
+        const int ins = t1_insert(S.dset, (uint32_t)u);
+        if (ins == 1) {
+            const unsigned q = atomicAdd(&S.nd[b ^ 1], 1u);
+            if (q < dcap) S.dirty[b ^ 1][q] = (uint32_t)u;
+            else S.ovf_mark = 1;
+        } else if (ins == 2) {
+            S.ovf_mark = 1;
+        }
+    }
+}
+
+// chained != 0: launched right behind k_tail on the stream; runs only if that
+// launch handed over (exit kTailSmall), continuing its iteration count,
+// history and flags, so the hand-over costs no host round trip.
+template <typename FT>
+__global__ void __launch_bounds__(kT1Threads, 1) k_tail1(Dom d, const FT* __restrict__ f, double* g, Work w, int cur,
+                                                         long long budget, unsigned long long* __restrict__ hist,
+                                                         TailState* ts, unsigned long long* __restrict__ trace,
+                                                         int chained, int var) {
+    extern __shared__ __align__(16) unsigned char t1raw[];
+    T1Smem& S = *reinterpret_cast<T1Smem*>(t1raw);
+    const int tid = threadIdx.x;
+    DevCounters* c = w.ctr;
+    long long it0 = 0;
+    unsigned long long shared_or = 0, detections = 0;
+    if (chained) {
+        if (ts->exit != kTailSmall) return;
+        cur = (int)ts->cur;
+        it0 = (long long)ts->iterations;
+        shared_or = ts->shared_or;
+        detections = ts->detections;
+        hist += it0;
+        budget -= it0;
+    }
+    const int xl = cur ^ 1;   // global list a hand-back leaves the pending dirty set in
+    // dirty-list capacity: the shared list, and the global list a hand-back fills
+    const unsigned dcap = (unsigned)min((unsigned long long)kT1Dirty, w.act_cap);
+    const unsigned n0 = (unsigned)min(__ldcg(&c->nact[cur]), (unsigned long long)dcap);
+    for (unsigned i = tid; i < n0; i += kT1Threads) {
+        const uint32_t u = __ldcg(w.act[cur] + i);
+        S.dirty[0][i] = u;
+        atomicAnd(w.actbits + (u >> 5), ~(1u << (u & 31)));
+    }
+    for (int i = tid; i < kT1Set; i += kT1Threads) S.tset[i] = kT1Empty;
+    if (tid == 0) {
+        S.nd[0] = n0;
+        S.nd[1] = 0;
+        S.ovf_tgt = S.ovf_edit = S.ovf_mark = 0;
+        S.nedit = S.ndet = S.shared = S.maxc = 0;
+        c->nact[xl] = 0;
+        c->nwork = 0;
+        c->nelist = 0;
+        if (trace) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            trace[8190] = t;
+        }
+    }
+    int b = 0;
+    for (long long it = 0;; ++it) {
+        for (int i = tid; i < kT1Set; i += kT1Threads) S.dset[i] = kT1Empty;   // filled by A
+        __syncthreads();
+        if (trace && tid == 0 && it < 90) trace[7000 + it] = clock64();
+        // ---- S: detection + rules of the dirty list ----------------------------
+        const unsigned nd = S.nd[b];
+        unsigned mydet = 0;
+        bool issued = false;
+        for (unsigned i = tid; i < nd; i += kT1Threads) {
+            const int64_t cc = S.dirty[b][i];
+            int64_t x, y, z;
+            coords(d, cc, x, y, z);
+            double nv[14];
+            load_ring(d, g, cc, x, y, z, nv, [](const double* q) { return __ldcg(q); });
+            const double vc = __ldcg(g + cc);
+            const uint8_t fc = __ldg(w.code + cc);
+            const Scan s = fold_scan(vc, nv);
+            const uint32_t bit = 1u << (cc & 31);
+            if (code_mismatch(d, scan_code(s), fc)) {
+                atomicOr(w.detbits + (cc >> 5), bit);
+                ++mydet;
+                EmitT1 emit{w, S};
+                rules<false>(d, w, s, nv, fc, cc, emit);
+                issued = issued || emit.issued;
+            } else {
+                atomicAnd(w.detbits + (cc >> 5), ~bit);   // (a reduction: no round trip)
+            }
+        }
+        mydet = __reduce_add_sync(0xffffffffu, mydet);
+        if ((tid & 31) == 0 && mydet) atomicAdd(&S.ndet, mydet);
+        if (issued) {   // this thread's RED.MINs are performed before anyone reads prop
+            if (var & 1) {
+            } else if (var & 2) {
+                asm volatile("fence.acq_rel.gpu;" ::: "memory");
+            } else {
+                __threadfence();
+            }
+        }
+        __syncthreads();
+        if (trace && tid == 0 && it < 90 && !(var & 4)) trace[8000 + 2 * it] = clock64();
+        // ---- A: apply every target, mark the rings of the edits -------------------
+        ApplyAcc acc;
+        for (int slot = tid; slot < kT1Set; slot += kT1Threads) {
+            const uint32_t t = S.tset[slot];
+            if (t == kT1Empty) continue;
+            S.tset[slot] = kT1Empty;   // empty again for the next S
+            t1_apply_mark(d, f, g, w, S, b, dcap, (int64_t)t, acc);
+        }
+        if (S.ovf_tgt) {
+            const unsigned long long n = __ldcg(&c->nwork);
+            for (unsigned long long i = tid; i < n; i += kT1Threads) {
+                const int64_t t = __ldcg(w.work + i);
+                const uint32_t bit = 1u << (t & 31);
+                if (atomicAnd(w.touched + (t >> 5), ~bit) & bit) t1_apply_mark(d, f, g, w, S, b, dcap, t, acc);
+            }
+        }
+        {
+            const unsigned wm = __reduce_max_sync(0xffffffffu, acc.maxc);
+            const unsigned wsh = __reduce_or_sync(0xffffffffu, acc.shared ? 1u : 0u);
+            if ((tid & 31) == 0) {
+                if (wm) atomicMax(&S.maxc, wm);
+                if (wsh) S.shared = 1;
+            }
+        }
+        __syncthreads();
+        if (trace && tid == 0 && it < 90 && !(var & 4)) trace[8001 + 2 * it] = clock64();
+        const unsigned nedit = S.nedit, ndet = S.ndet;
+        const bool ovf_edit = S.ovf_edit != 0;
+        const bool ovf = ovf_edit || S.ovf_mark != 0;
+        const unsigned ne = min(nedit, (unsigned)kT1Set);
+        shared_or |= S.shared;
+        detections += ndet;
+        if (tid == 0) {
+            hist[it] = nedit;
+            if (trace) {
+                unsigned long long t;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+                trace[2 * it] = t;
+                trace[2 * it + 1] = S.nd[b ^ 1];
+                trace[7100 + it] = clock64();
+                trace[7200 + it] = nedit;
+            }
+        }
+        unsigned long long exit = 0, pending = 0;
+        if (nedit == 0) {
+            exit = kTailConverged;
+        } else if (ovf) {
+            // a shared structure overflowed: the 1-rings of every edit go through
+            // the global marking of the list-mode iteration (actbits + act[xl])
+            for (unsigned i = tid; i < ne; i += kT1Threads) mark_ring(d, w, S.edits[i], xl);
+            if (ovf_edit) {
+                const unsigned long long n = __ldcg(&c->nelist);
+                for (unsigned long long i = tid; i < n; i += kT1Threads) mark_ring(d, w, __ldcg(w.elist + i), xl);
+            }
+            __threadfence();
+            __syncthreads();
+            pending = __ldcg(&c->nact[xl]);
+            exit = pending > w.act_cap ? kTailOverflow : kTailBudget;
+        } else if (it + 1 >= budget) {
+            const unsigned n1 = S.nd[b ^ 1];
+            for (unsigned i = tid; i < n1; i += kT1Threads) {
+                const uint32_t u = S.dirty[b ^ 1][i];
+                w.act[xl][i] = u;
+                atomicOr(w.actbits + (u >> 5), 1u << (u & 31));
+            }
+            pending = n1;
+            exit = kTailBudget;
+            if (tid == 0) c->nact[xl] = n1;
+        }
+        if (exit) {
+            if (tid == 0) {
+                if (S.maxc) atomicMax(&c->maxcount, (unsigned long long)S.maxc);
+                ts->iterations = (unsigned long long)(it0 + it + 1);
+                ts->exit = exit;
+                ts->cur = (unsigned long long)xl;
+                ts->pending = pending;
+                ts->last_edits = nedit;
+                ts->last_detect = ndet;
+                ts->shared_or = shared_or;
+                ts->detections = detections;
+                ts->appended = 1ull;
+                c->ndetect = ndet;   // the host reads the last iteration's counters
+            }
+            return;
+        }
+        __syncthreads();   // every thread has read nedit / ndet / the flags above
+        if (tid == 0) {    // the new dirty list is dirty[b ^ 1]
+            S.nd[b] = 0;
+            S.nedit = S.ndet = S.shared = 0;
+        }
+        b ^= 1;
     }
 }
 

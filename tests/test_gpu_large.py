@@ -56,7 +56,9 @@ def _independent_checks(f32, g, dims, xi, extrema_only=False):
                       extrema_only=extrema_only, no_robust=True)
     scratch = torch.empty_like(g)
     st, _ = plan.prepare(f32, g, scratch)   # exact f-code at every centre (no robust skipping)
-    assert st == 0
+    # (the prepare's |f - g| <= xi check may flag g = fl(f - xi) by one rounding;
+    # the reference's post-check is BoundsField.admits, counted below)
+    assert st in (0, 2)
     kinds = plan.verify(g)
     assert kinds == [0] * 6, kinds
     assert plan.bounds_violations(f32, g) == 0

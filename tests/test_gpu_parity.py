@@ -469,6 +469,36 @@ def test_robust_skipping_changes_nothing(monkeypatch):
     assert torch.equal(a.edit_ids, b.edit_ids) and torch.equal(a.edit_values, b.edit_values)
 
 
+@pytest.mark.parametrize("dims,rel", [((160, 144, 128), 1e-4), ((96, 96, 96), 1e-3), ((64, 64), 1e-2)])
+def test_loop_forms_agree(monkeypatch, dims, rel):
+    """Every form of an iteration is exact: the one-CTA shared-memory tail
+    (default), the grid-wide tail (PMSZ_TAIL1=0) and host-launched iterations
+    (PMSZ_FLAG_HOST_LOOP) give identical trajectories, fields, edit records and
+    max_vertex_edits -- and all equal the oracle."""
+    from paper_2601_01787_b200.engine import DomainPlan, DomainSpec
+    d3 = dims if len(dims) == 3 else (*dims, 1)
+    f32 = gen.perlin_device(gen.NoiseSpec(d3, 9), f32=True)
+    xi = gen.relative_to_absolute_device(f32, rel)
+    fh = gen.quantize_device(f32, xi)
+    cfg = pm.CorrectionConfig(xi_abs=xi)
+    outs = []
+    for env, host_loop in (({}, False), ({"PMSZ_TAIL1": "0"}, False), ({}, True)):
+        monkeypatch.delenv("PMSZ_TAIL1", raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        plan = DomainPlan(DomainSpec.whole(d3), xi, cfg.tau, cfg.max_outer_iterations, f32_original=True,
+                          host_loop=host_loop)
+        outs.append(pm.run_correction_device(f32, fh, d3, cfg, plan=plan))
+        plan.close()
+    ref = orc.run_correction(d3, f32.double().cpu().numpy(), fh.cpu().numpy(), xi)
+    assert ref.status == orc.ORC_OK
+    for o in outs:
+        assert list(o.edits_per_iteration) == list(ref.edits_per_iteration)
+        assert o.max_vertex_edits == ref.max_vertex_edits
+        assert np.array_equal(o.corrected.cpu().numpy(), ref.corrected)
+        assert torch.equal(o.edit_ids, outs[0].edit_ids) and torch.equal(o.edit_values, outs[0].edit_values)
+
+
 def test_floor_violation_raises_like_the_reference():
     """Hazard H6: fhat below fl(f - xi) although the rounded |f - fhat| <= xi
     check passes.  The reference itself raised its monotonicity AssertionError
