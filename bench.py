@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--rel", type=float, default=1e-4)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-dropin", action="store_true", help="skip the drop-in run_correction(ScalarField) timing")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-z", type=int, default=64, help="z-planes of the CPU baseline sample")
     ap.add_argument("--full-sweeps", action="store_true", help="disable incremental dirty-ring sweeps")
@@ -341,6 +342,8 @@ def run_ours_single(args):
     line["result"].update(reference_pin(args, wl, f32, fh, res))
     if not args.no_e2e:
         line["e2e"] = e2e_host(args, plan, f32, fh, dims, nvox, res)
+    if not args.no_dropin and not wl["extrema_only"]:
+        line["dropin"] = dropin_api(args, f32, fh, dims, cfg, res)
     if not args.no_cpu_baseline:
         f, fhs, xic, sdims = cpu_sample_inputs(args.workload, dims, args.cpu_sample_z, args.rel, args.seed,
                                                xi=xi, origin=lo, norm=wl.get("norm"))
@@ -384,6 +387,33 @@ def reference_pin(args, wl, f32, fh, res) -> dict:
                                       f"{s.get('seconds', '?')} s on the build host)",
                             "inputs_match": inputs_ok, "bit_exact": bool(match)}
     return out
+
+
+def dropin_api(args, f32, fh, dims, cfg, dev_res) -> dict:
+    """The reference-facing Python API on host data: run_correction(ScalarField,
+    ScalarField, CorrectionConfig) -> CorrectionResult (correction.py:391-436),
+    i.e. what a topocorrect user calls.  Timed per call (wall clock: host f64
+    arrays in, host corrected ScalarField + EditSet out), with the device path
+    plus the copies it implies beside it for comparison."""
+    import torch
+    import paper_2601_01787_b200 as pm
+    f = pm.ScalarField(dims, f32.double().cpu().numpy())
+    fhat = pm.ScalarField(dims, fh.cpu().numpy())
+    steps = max(2, min(args.steps, 3))
+    pm.run_correction(f, fhat, cfg)   # warm-up (plan creation)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        r = pm.run_correction(f, fhat, cfg)
+    dt = (time.perf_counter() - t0) / steps
+    ok = (list(r.edits_per_iteration) == list(dev_res.edits_per_iteration) and r.edits.count == dev_res.edit_ids.numel()
+          and _sha(r.corrected.values) == _sha(dev_res.corrected))
+    if not ok:
+        raise SystemExit("drop-in run_correction differs from the device-resident run")
+    n = dims[0] * dims[1] * dims[2]
+    return {"ms_per_call": dt * 1e3, "voxels_per_s": n / dt, "calls": steps, "matches_device": ok,
+            "path": "paper_2601_01787_b200.run_correction(ScalarField f64 x2, CorrectionConfig) -> CorrectionResult "
+                    "(pageable host f64 in, corrected ScalarField + EditSet out; f32-exact original detected on device)"}
 
 
 def e2e_host(args, plan, f32, fh, dims, nvox, dev_res) -> dict:

@@ -30,7 +30,6 @@
 #include "gather.cuh"
 #include "qsweep.cuh"
 #include "prep.cuh"
-#include "prep2.cuh"
 #include "segment.cuh"
 
 using namespace pmsz;
@@ -498,8 +497,6 @@ struct pmsz_plan {
     bool fuse_on = true;                  // K0 also runs the first detection sweep (prep.cuh)
     bool qmask_ok = false;                // dense masked iterations can use the TMA queue sweep (kMaskedQ)
     bool k0_detected = false;             // detbits / ndetect of the first iteration come from K0
-    bool k0_rules = false;                // ... and its proposals are already in prop / touched (prep2.cuh)
-    bool prep2_on = true;                 // K0 = the fused producer / consumer kernel of prep2.cuh
     uint32_t* frag = nullptr;             // fragile-centre bitmap written by K0
     int64_t hist_chunk = 0;               // thist / hthist entries: iterations per tail launch
     std::vector<int64_t> hist_all;        // edits_per_iteration of the last pmsz_run_correction
@@ -689,10 +686,6 @@ pmsz_status iterate_once(pmsz_plan* p, const void* f, double* g, cudaStream_t s)
     // other per-iteration counter is still zero from reset_run_state)
     const bool predetected = mode == kFull && p->k0_detected;
     p->k0_detected = false;
-    // the rules of this iteration's mismatches already ran: inside K0 (prep2.cuh)
-    // or inside the TMA queue sweep below; otherwise k_defer runs them
-    bool ruled = predetected && p->k0_rules;
-    p->k0_rules = false;
     pmsz_status st = predetected ? PMSZ_OK : reset_iter(p, s, nxt);
     if (st) return st;
     const int64_t cx = d.hi[0] - d.lo[0], cy = d.hi[1] - d.lo[1], cz = d.hi[2] - d.lo[2];
@@ -707,8 +700,7 @@ pmsz_status iterate_once(pmsz_plan* p, const void* f, double* g, cudaStream_t s)
         if (nonempty && !predetected) {
             ProfScope ps(p, s, PMSZ_K_SWEEP_FULL);
             // the TMA queue sweep runs the rules of its mismatches itself
-            ruled = p->qsweep_on && launch_sweep_q<false>(d, g, p->w, s);
-            if (!ruled) launch_sweep_full<false>(d, g, p->w, s);
+            if (!(p->qsweep_on && launch_sweep_q<false>(d, g, p->w, s))) launch_sweep_full<false>(d, g, p->w, s);
             LAUNCHED();
         }
     } else if (mode == kMasked || mode == kMaskedList || mode == kMaskedQ) {
@@ -745,14 +737,14 @@ pmsz_status iterate_once(pmsz_plan* p, const void* f, double* g, cudaStream_t s)
         } else {
             if (nonempty) {
                 ProfScope ps(p, s, PMSZ_K_SWEEP_MASKED);
-                ruled = p->qsweep_on && launch_sweep_q<false>(d, g, p->w, s, p->w.actbits);
-                if (!ruled) launch_sweep_full<false>(d, g, p->w, s, p->w.actbits);
+                if (!(p->qsweep_on && launch_sweep_q<false>(d, g, p->w, s, p->w.actbits)))
+                    launch_sweep_full<false>(d, g, p->w, s, p->w.actbits);
                 LAUNCHED();
             }
             CUDA_TRY(cudaMemsetAsync(p->w.actbits, 0, p->nwords * 4, s));
         }
     }
-    if (mode != kList && nonempty && !gather && !ruled) {
+    if (mode != kList && nonempty && !gather) {
         // centres with a detection (bitmap set by the tiled sweep) -> list -> rules
         {
             ProfScope ps(p, s, PMSZ_K_COMPACT);
@@ -871,9 +863,8 @@ pmsz_status launch_tail1(pmsz_plan* p, const void* f, double* g, cudaStream_t s,
         tr = trace_buf;
         CUDA_TRY(cudaMemsetAsync(tr, 0, 2 * 8 * 4096, s));
     }
-    static const int var = getenv("PMSZ_T1V") ? atoi(getenv("PMSZ_T1V")) : 0;
     k_tail1<FT><<<1, kT1Threads, kT1SmemBytes, s>>>(p->dom, (const FT*)f, g, p->w, p->cur, budget, p->thist, p->tail, tr,
-                                                     chained, var);
+                                                     chained);
     LAUNCHED();
     if (trace) {
         std::vector<unsigned long long> h2(2 * 4096);
@@ -882,13 +873,6 @@ pmsz_status launch_tail1(pmsz_plan* p, const void* f, double* g, cudaStream_t s,
         fprintf(stderr, "tail1 cur=%d pending=%lld:", p->cur, (long long)p->pending);
         for (int i = 0; i < 4000 && h2[2 * i]; ++i)
             fprintf(stderr, " %.1fus/%llu", (h2[2 * i] - (i ? h2[2 * i - 2] : h2[8190])) / 1e3, h2[2 * i + 1]);
-        fprintf(stderr, "\n  cycles pre/S/A/post (edits):");
-        for (int i = 0; i < 90 && h2[2 * i]; ++i) {
-            const long long pre = i ? (long long)(h2[7000 + i] - h2[7100 + i - 1]) : 0;
-            fprintf(stderr, " [%lld %lld %lld %lld (%llu)]", pre, (long long)(h2[8000 + 2 * i] - h2[7000 + i]),
-                    (long long)(h2[8001 + 2 * i] - h2[8000 + 2 * i]), (long long)(h2[7100 + i] - h2[8001 + 2 * i]),
-                    h2[7200 + i]);
-        }
         fprintf(stderr, "\n");
     }
     return PMSZ_OK;
@@ -989,26 +973,9 @@ pmsz_status prep(pmsz_plan* p, const void* f, const double* fh, double* g, cudaS
         // K0 also runs the first detection sweep (g = fhat) unless told otherwise
         uint32_t* det = p->fuse_on ? p->w.detbits : nullptr;
         if (det) CUDA_TRY(cudaMemsetAsync(det, 0, p->nwords * 4, s));
-        bool queued = false, fused = false;
+        bool queued = false;
         const size_t nsl = p->stage_pending ? p->stage_z.size() - 1 : 0;
-        const bool try2 = p->prep2_on && p->qprep_on && det != nullptr && p->frag_out() != nullptr;
-        if (try2) {
-            // fused K0 (prep2.cuh): the first iteration's detection and rules included
-            const size_t n2 = nsl > 0 ? nsl : 1;
-            for (size_t c = 0; c < n2; ++c) {
-                const int64_t za = nsl > 0 ? p->stage_z[c] : 0, zb2 = nsl > 0 ? p->stage_z[c + 1] : p->dom.nz;
-                if (nsl > 0) CUDA_TRY(cudaStreamWaitEvent(s, p->stage_ev[1 + std::min(c + 1, nsl - 1)], 0));
-                fused = p->f32 ? launch_prep2<float>(p->dom, (const float*)f, fh, g, p->w.code, p->frag_out(), p->ctr,
-                                                     det, p->w, s, za, zb2)
-                               : launch_prep2<double>(p->dom, (const double*)f, fh, g, p->w.code, p->frag_out(),
-                                                      p->ctr, det, p->w, s, za, zb2);
-                if (!fused) break;   // nothing was launched
-                if (c + 1 < n2) LAUNCHED();
-            }
-            queued = fused;
-        }
-        if (queued) {
-        } else if (p->qprep_on && nsl > 0) {
+        if (p->qprep_on && nsl > 0) {
             // input still arriving in z-slabs: K0 over slab c once slab c and
             // the first plane of slab c + 1 (its upper halo) have landed
             for (size_t c = 0; c < nsl; ++c) {
@@ -1027,7 +994,6 @@ pmsz_status prep(pmsz_plan* p, const void* f, const double* fh, double* g, cudaS
         if (nsl > 0) CUDA_TRY(cudaStreamWaitEvent(s, p->stage_ev[nsl], 0));   // every slab is in
         p->stage_pending = false;
         p->k0_detected = queued && det != nullptr;
-        p->k0_rules = fused;
         if (!queued) {
             if (p->f32)
                 launch_prep<float>(p->dom, (const float*)f, fh, g, p->w.code, p->frag_out(), p->ctr, s);
@@ -1231,7 +1197,6 @@ pmsz_status pmsz_plan_create(const pmsz_desc* desc, pmsz_plan** out) {
     if (const char* e = getenv("PMSZ_QPREP")) p->qprep_on = atoi(e) != 0;
     if (const char* e = getenv("PMSZ_FUSE")) p->fuse_on = atoi(e) != 0;
     if (const char* e = getenv("PMSZ_TAIL1")) p->tail1_on = atoi(e) != 0;
-    if (const char* e = getenv("PMSZ_PREP2")) p->prep2_on = atoi(e) != 0;
     // measured: the dense masked queue sweep (0.45 ms) plus the dilation (0.08 ms)
     // do not beat the plain queue sweep (0.49 ms) at 512^3, so it is opt-in
     p->qmask_ok = p->qsweep_on && p->gather_on && qsweep_masked_ok(p->dom) && getenv("PMSZ_QMASK") &&
@@ -1387,13 +1352,8 @@ pmsz_status pmsz_block_round(pmsz_plan* p, const void* f, double* g, int32_t loc
     return fail(PMSZ_ERR_CONVERGENCE, "block found no zero-edit iteration within the cap");
 }
 
-// Something may change g before the first iteration: K0's detections (and,
-// with prep2.cuh, its proposals) are stale.
-static void drop_k0(pmsz_plan* p, cudaStream_t s) {
-    if (p->k0_rules) restore_prop(p, s);
-    p->k0_rules = false;
-    p->k0_detected = false;
-}
+// Something may change g before the first iteration: K0's detections are stale.
+static void drop_k0(pmsz_plan* p, cudaStream_t) { p->k0_detected = false; }
 
 pmsz_status pmsz_mark_all_dirty(pmsz_plan* p, void* stream) {
     if (!p) return fail(PMSZ_ERR_INVALID, "null plan");

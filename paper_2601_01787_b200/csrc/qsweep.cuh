@@ -233,8 +233,8 @@ __global__ void __launch_bounds__(kQThreads, 3) k_qsweep_tma(Dom d, const __grid
                            nv, vc);
             const bool interior = cur ? int_cur : int_prev;
             const Scan s = interior ? tree_scan(vc, nv) : fold_scan(vc, nv);   // NaN = outside the field
-            op.evaluate_ring(d, (int64_t)(cpl - (cur ? 0u : sz32) + (uint32_t)r * sy32 + (uint32_t)lx), s, nv,
-                             (uint8_t)(ent >> 16));
+            op.evaluate(d, (int64_t)(cpl - (cur ? 0u : sz32) + (uint32_t)r * sy32 + (uint32_t)lx), s,
+                        (uint8_t)(ent >> 16));
         }
         __syncwarp();
         // leftovers of plane k move to the front, marked as carried

@@ -380,7 +380,7 @@ template <typename FT>
 __global__ void __launch_bounds__(kT1Threads, 1) k_tail1(Dom d, const FT* __restrict__ f, double* g, Work w, int cur,
                                                          long long budget, unsigned long long* __restrict__ hist,
                                                          TailState* ts, unsigned long long* __restrict__ trace,
-                                                         int chained, int var) {
+                                                         int chained) {
     extern __shared__ __align__(16) unsigned char t1raw[];
     T1Smem& S = *reinterpret_cast<T1Smem*>(t1raw);
     const int tid = threadIdx.x;
@@ -424,7 +424,6 @@ __global__ void __launch_bounds__(kT1Threads, 1) k_tail1(Dom d, const FT* __rest
     for (long long it = 0;; ++it) {
         for (int i = tid; i < kT1Set; i += kT1Threads) S.dset[i] = kT1Empty;   // filled by A
         __syncthreads();
-        if (trace && tid == 0 && it < 90) trace[7000 + it] = clock64();
         // ---- S: detection + rules of the dirty list ----------------------------
         const unsigned nd = S.nd[b];
         unsigned mydet = 0;
@@ -451,16 +450,8 @@ __global__ void __launch_bounds__(kT1Threads, 1) k_tail1(Dom d, const FT* __rest
         }
         mydet = __reduce_add_sync(0xffffffffu, mydet);
         if ((tid & 31) == 0 && mydet) atomicAdd(&S.ndet, mydet);
-        if (issued) {   // this thread's RED.MINs are performed before anyone reads prop
-            if (var & 1) {
-            } else if (var & 2) {
-                asm volatile("fence.acq_rel.gpu;" ::: "memory");
-            } else {
-                __threadfence();
-            }
-        }
+        if (issued) __threadfence();   // this thread's RED.MINs are performed before anyone reads prop
         __syncthreads();
-        if (trace && tid == 0 && it < 90 && !(var & 4)) trace[8000 + 2 * it] = clock64();
         // ---- A: apply every target, mark the rings of the edits -------------------
         ApplyAcc acc;
         for (int slot = tid; slot < kT1Set; slot += kT1Threads) {
@@ -486,7 +477,6 @@ __global__ void __launch_bounds__(kT1Threads, 1) k_tail1(Dom d, const FT* __rest
             }
         }
         __syncthreads();
-        if (trace && tid == 0 && it < 90 && !(var & 4)) trace[8001 + 2 * it] = clock64();
         const unsigned nedit = S.nedit, ndet = S.ndet;
         const bool ovf_edit = S.ovf_edit != 0;
         const bool ovf = ovf_edit || S.ovf_mark != 0;
@@ -500,8 +490,6 @@ __global__ void __launch_bounds__(kT1Threads, 1) k_tail1(Dom d, const FT* __rest
                 asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
                 trace[2 * it] = t;
                 trace[2 * it + 1] = S.nd[b ^ 1];
-                trace[7100 + it] = clock64();
-                trace[7200 + it] = nedit;
             }
         }
         unsigned long long exit = 0, pending = 0;

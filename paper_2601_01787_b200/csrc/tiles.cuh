@@ -264,25 +264,6 @@ struct DetectOp {
         if (kCount) count_kinds(d, w, s, fc);
         else atomicOr(w.detbits + (c >> 5), 1u << (c & 31));   // RED; k_defer picks it up
     }
-    // The same with the ring values at hand (TMA queue sweep): a mismatching
-    // centre's rules run right here (correction.py:169-229; proposals by
-    // RED.MIN, exactly as k_defer would), so no deferred rule pass is needed.
-    __device__ __forceinline__ void evaluate_ring(const Dom& d, int64_t c, const Scan& s, const double (&nv)[14],
-                                                  uint8_t fc) {
-        const uint8_t gc = scan_code(s);
-        const bool mismatch = kExtrema ? (((gc & 15) == kExtremum) != ((fc & 15) == kExtremum) ||
-                                          ((gc >> 4) == kExtremum) != ((fc >> 4) == kExtremum))
-                                       : gc != fc;
-        if (!mismatch) return;
-        ++ndet;
-        if (kCount) {
-            count_kinds(d, w, s, fc);
-        } else {
-            atomicOr(w.detbits + (c >> 5), 1u << (c & 31));
-            EmitRed emit{w};
-            rules<false>(d, w, s, nv, fc, c, emit);
-        }
-    }
     __device__ __forceinline__ void finish() {
         if (!kCount) {
             const unsigned t = __reduce_add_sync(0xffffffffu, ndet);
