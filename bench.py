@@ -55,9 +55,10 @@ def parse():
     ap.add_argument("--workload", default="perlin", choices=["perlin", "strong", "hedm"],
                     help="perlin: configs 2/3 (default); strong: config 4; hedm: config 5 (extrema-only)")
     ap.add_argument("--decomp", default="slab", choices=["slab", "block"], help="strong scaling layout")
-    ap.add_argument("--weak-layout", default="mirror", choices=["mirror", "continuous"],
-                    help="weak scaling: every GPU's cube is the 1-GPU field or its z-mirror (mirror), or the "
-                         "next stretch of the Perlin function (continuous)")
+    ap.add_argument("--weak-layout", default="tile", choices=["tile", "mirror", "continuous"],
+                    help="weak scaling: every GPU's core is the 1-GPU cube (tile, default), the cube or its "
+                         "z-mirror (mirror: duplicates the interface planes), or the next stretch of the Perlin "
+                         "function (continuous)")
     return ap.parse_args()
 
 

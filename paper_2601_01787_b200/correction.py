@@ -27,7 +27,7 @@ import torch
 
 from . import _native as N
 from .engine import (BoundViolationError, ConvergenceError, DomainPlan, DomainSpec,
-                     as_device_f64, narrow_if_exact, raise_for)
+                     as_device_f64, narrow_if_exact, raise_for, to_host_f64)
 from .grid import ScalarField
 from .topology import DistortionReport
 
@@ -258,7 +258,7 @@ def run_correction(original: ScalarField, decompressed: ScalarField, config: Cor
     raise_for(st, res, original.values, decompressed.values, config.xi_abs)
     g = fh
     ids, vals = plan.export_edits(g)
-    corrected = ScalarField(original.dims, g.cpu().numpy())
+    corrected = ScalarField._owned(original.dims, to_host_f64(g))
     edits = EditSet(ids=ids.cpu().numpy(), values=vals.cpu().numpy(),
                     vertex_count=original.vertex_count)
     return CorrectionResult(corrected=corrected, edits=edits, iterations=int(res.iterations),

@@ -26,6 +26,7 @@ import torch
 from . import _native as N
 from .correction import CorrectionConfig, CorrectionResult, EditSet
 from .engine import (BoundViolationError, ConvergenceError, DomainPlan, DomainSpec, as_device_f64, narrow_if_exact,
+                     to_host_f64,
                      raise_for)
 from .grid import ScalarField
 from .topology import DistortionReport
@@ -387,8 +388,7 @@ def run_parallel(original: ScalarField, decompressed: ScalarField, config: Corre
         raise ConvergenceError("corrected field escaped the error bound")
     if any(gplan.verify(out)):
         raise ConvergenceError("distortions survived at termination")
-    g_host = out.cpu().numpy()
-    corrected = ScalarField(dims, g_host)
+    corrected = ScalarField._owned(dims, to_host_f64(out))
     edits = EditSet.diff(decompressed, corrected)
     result = CorrectionResult(corrected=corrected, edits=edits,
                               iterations=max(b.iterations for b in blocks),
