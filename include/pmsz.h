@@ -208,6 +208,48 @@ pmsz_status pmsz_history(const pmsz_plan* plan, int64_t* out, int64_t cap, int64
 pmsz_status pmsz_bounds_violations(pmsz_plan* plan, const void* f_dev, const double* g_dev,
                                    int64_t* count_out, void* stream);
 
+/* ---- multi-GPU round loop (run_parallel, parallel.py:258-367, one block per rank) ---- */
+#define PMSZ_MAX_RANKS 64
+#define PMSZ_MAX_EXCHANGES 26
+/*
+ * The reference's relaxed / lockstep round loop (parallel.py:289-322) of ONE
+ * rank, driven from C with every exchange over NVLink peer memory: each rank
+ * owns a buffer that every other rank can address (torch symmetric memory;
+ * `bufs` holds all of them as device pointers valid in this process).
+ * Buffer layout (per rank, identical offsets everywhere): two parity areas of
+ * repl_doubles f64 each for the packed overlap replicas (this rank's overlap
+ * with every peer, one box per exchange), then u64 sum slots [2][world][4] at
+ * sums_off, then u64 arrival epochs [world] at flags_off (zero at creation).
+ * A round: pmsz_block_round; pack the replicas into the round's parity area;
+ * publish {edits, shared_dirty} into every peer's slot and raise this rank's
+ * epoch there (release, system scope); wait until every peer's epoch arrived
+ * (acquire); sum; terminate exactly as parallel.py:304-322; else min-merge
+ * every peer's replica straight out of its buffer (pmsz_box_merge_min).
+ * Parity areas and epoch-parity sum slots make a second barrier unnecessary.
+ * epoch and rounds_total persist across calls on the same buffers.
+ */
+typedef struct {
+    int32_t world, rank;
+    int32_t nex;                     /* exchanges of this rank (its overlaps with other blocks) */
+    int32_t lockstep;
+    int64_t cap;                     /* CorrectionConfig.max_outer_iterations (rounds) */
+    int64_t repl_doubles;            /* one parity area (doubles) */
+    int64_t sums_off;                /* u64 offset of the sum slots in every buffer */
+    int64_t flags_off;               /* u64 offset of the arrival epochs in every buffer */
+    uint64_t epoch;                  /* in: last epoch used on these buffers; out: updated */
+    uint64_t rounds_total;           /* in/out: rounds run on these buffers (replica parity) */
+    void* bufs[PMSZ_MAX_RANKS];
+    int32_t ex_peer[PMSZ_MAX_EXCHANGES];
+    int64_t ex_lo[PMSZ_MAX_EXCHANGES][3];     /* overlap box in this rank's ext coordinates */
+    int64_t ex_hi[PMSZ_MAX_EXCHANGES][3];
+    int64_t ex_off[PMSZ_MAX_EXCHANGES];       /* this rank's replica of the box in its buffer (doubles) */
+    int64_t ex_peer_off[PMSZ_MAX_EXCHANGES];  /* the peer's replica of the same box in the peer's buffer */
+} pmsz_rounds_desc;
+/* rounds / syncs (ParallelStats), totals[k] = edits of round k summed over ranks
+ * (edits_per_iteration of run_parallel); result = this block's last pmsz_block_round. */
+pmsz_status pmsz_rounds(pmsz_plan* plan, const void* f_dev, double* g_dev, pmsz_rounds_desc* rd, int64_t* rounds,
+                        int64_t* syncs, int64_t* totals, int64_t totals_cap, pmsz_result* result, void* stream);
+
 /* ---- topology kernels ---------------------------------------------------- */
 /* scan_neighbors (topology.py:47-86): ids of the (value,id)-largest/smallest neighbour
  * and extremum flags.  Outputs are device arrays of n entries. */

@@ -70,6 +70,22 @@ class PmszResult(ctypes.Structure):
     ]
 
 
+MAX_RANKS = 64
+MAX_EXCHANGES = 26
+
+
+class PmszRoundsDesc(ctypes.Structure):
+    _fields_ = [
+        ("world", i32), ("rank", i32), ("nex", i32), ("lockstep", i32),
+        ("cap", i64), ("repl_doubles", i64), ("sums_off", i64), ("flags_off", i64),
+        ("epoch", u64), ("rounds_total", u64),
+        ("bufs", vp * MAX_RANKS),
+        ("ex_peer", i32 * MAX_EXCHANGES),
+        ("ex_lo", (i64 * 3) * MAX_EXCHANGES), ("ex_hi", (i64 * 3) * MAX_EXCHANGES),
+        ("ex_off", i64 * MAX_EXCHANGES), ("ex_peer_off", i64 * MAX_EXCHANGES),
+    ]
+
+
 # name -> (restype, argtypes); every symbol declared in include/pmsz.h.
 SIGNATURES = {
     "pmsz_last_error": (ctypes.c_char_p, []),
@@ -101,6 +117,8 @@ SIGNATURES = {
     "pmsz_box_mark_changed": (i32, [vp, i64p, i64p, vp, vp, vp]),
     "pmsz_box_merge_min": (i32, [vp, vp, i64p, i64p, vp, i64p, vp]),
     "pmsz_residual": (i32, [vp, i64p, vp]),
+    "pmsz_rounds": (i32, [vp, vp, vp, ctypes.POINTER(PmszRoundsDesc), i64p, i64p, i64p, i64,
+                          ctypes.POINTER(PmszResult), vp]),
     "pmsz_perlin": (i32, [i64p, i64p, i64p, ctypes.POINTER(i32), ctypes.c_double, i32, vp, vp, vp]),
     "pmsz_minmax": (i32, [vp, i32, i64, dp, dp, vp]),
     "pmsz_narrow_f32": (i32, [vp, i64, vp, i64p, vp]),

@@ -442,6 +442,44 @@ __global__ void __launch_bounds__(256) k_box_extract(Box b, int64_t gny, const F
     }
 }
 
+// ---- cross-rank epoch barrier carrying the round sums (pmsz_rounds) --------
+struct SigArgs {
+    unsigned long long* sums[PMSZ_MAX_RANKS];    // each rank's sum slots [2][world][4]
+    unsigned long long* flags[PMSZ_MAX_RANKS];   // each rank's arrival epochs [world]
+    unsigned long long v[4];
+    unsigned long long* out;                     // device: the 4 sums over ranks
+    unsigned long long epoch;
+    int world, rank;
+};
+
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Thread q publishes this rank's values into rank q's slot of this epoch's
+// parity and raises this rank's epoch there; then waits for q's epoch here.
+__global__ void __launch_bounds__(PMSZ_MAX_RANKS) k_signal(SigArgs a) {
+    const int q = threadIdx.x;
+    const int par = (int)(a.epoch & 1);
+    if (q < a.world) {
+        unsigned long long* slot = a.sums[q] + ((size_t)par * a.world + a.rank) * 4;
+        slot[0] = a.v[0]; slot[1] = a.v[1]; slot[2] = a.v[2]; slot[3] = a.v[3];
+        st_release_sys(a.flags[q] + a.rank, a.epoch);   // orders the slot stores before the epoch
+        while (ld_acquire_sys(a.flags[a.rank] + q) < a.epoch) __nanosleep(64);
+    }
+    __syncthreads();
+    if (q < 4) {
+        unsigned long long t = 0;
+        for (int r = 0; r < a.world; ++r) t += a.sums[a.rank][((size_t)par * a.world + r) * 4 + q];
+        a.out[q] = t;
+    }
+}
+
 }  // namespace
 
 // ============================================================================
@@ -511,6 +549,8 @@ struct pmsz_plan {
     std::vector<cudaEvent_t> stage_ev;    // [0]: staging free; [1 + c]: slab c landed
     std::vector<int64_t> stage_z;         // slab boundaries in z (nslabs + 1)
     bool stage_pending = false;           // the next K0 waits for the slabs, one launch per slab
+    unsigned long long* dsig = nullptr;   // pmsz_rounds: the summed round values (device) ...
+    unsigned long long* hsig = nullptr;   // ... and their pinned mirror
 };
 
 namespace {
@@ -1238,6 +1278,8 @@ void pmsz_plan_destroy(pmsz_plan* p) {
     if (p->hthist) cudaFreeHost(p->hthist);
     cudaFree(p->stage_f); cudaFree(p->stage_g); cudaFree(p->stage_ids); cudaFree(p->stage_vals);
     for (cudaEvent_t e : p->stage_ev) cudaEventDestroy(e);
+    cudaFree(p->dsig);
+    if (p->hsig) cudaFreeHost(p->hsig);
     if (p->copy_stream) cudaStreamDestroy(p->copy_stream);
     for (cudaEvent_t e : p->prof_ev) cudaEventDestroy(e);
     delete p;
@@ -1442,6 +1484,90 @@ pmsz_status pmsz_box_merge_min(pmsz_plan* p, double* g, const int64_t lo[3], con
     pmsz_status st = after_mark(p, s);
     if (st) return st;
     *changed_out = (int64_t)p->hctr->changed;
+    return PMSZ_OK;
+}
+
+// One epoch of the cross-rank barrier; the four sums land in p->hsig.
+static pmsz_status rounds_signal(pmsz_plan* p, pmsz_rounds_desc* rd, const unsigned long long v[4], cudaStream_t s) {
+    SigArgs a{};
+    for (int r = 0; r < rd->world; ++r) {
+        a.sums[r] = (unsigned long long*)rd->bufs[r] + rd->sums_off;
+        a.flags[r] = (unsigned long long*)rd->bufs[r] + rd->flags_off;
+    }
+    for (int k = 0; k < 4; ++k) a.v[k] = v[k];
+    a.out = p->dsig;
+    a.epoch = ++rd->epoch;
+    a.world = rd->world;
+    a.rank = rd->rank;
+    k_signal<<<1, PMSZ_MAX_RANKS, 0, s>>>(a);
+    LAUNCHED();
+    CUDA_TRY(cudaMemcpyAsync(p->hsig, p->dsig, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    return PMSZ_OK;
+}
+
+pmsz_status pmsz_rounds(pmsz_plan* p, const void* f, double* g, pmsz_rounds_desc* rd, int64_t* rounds_out,
+                        int64_t* syncs_out, int64_t* totals, int64_t totals_cap, pmsz_result* r, void* stream) {
+    if (!p || !f || !g || !rd) return fail(PMSZ_ERR_INVALID, "null argument");
+    if (rd->world < 1 || rd->world > PMSZ_MAX_RANKS || rd->rank < 0 || rd->rank >= rd->world ||
+        rd->nex < 0 || rd->nex > PMSZ_MAX_EXCHANGES)
+        return fail(PMSZ_ERR_INVALID, "bad rounds descriptor");
+    cudaStream_t s = S(stream);
+    if (!p->dsig) {
+        CUDA_TRY(cudaMalloc((void**)&p->dsig, 4 * sizeof(unsigned long long)));
+        CUDA_TRY(cudaMallocHost((void**)&p->hsig, 4 * sizeof(unsigned long long)));
+    }
+    Box boxes[PMSZ_MAX_EXCHANGES];
+    for (int e = 0; e < rd->nex; ++e)
+        if (!make_box(p->dom.nx, p->dom.ny, p->dom.nz, rd->ex_lo[e], rd->ex_hi[e], boxes[e]))
+            return fail(PMSZ_ERR_INVALID, "exchange box outside the domain");
+    const bool lockstep = rd->lockstep != 0;
+    int64_t nr = 0, ns = 0;
+    pmsz_result rr{};
+    for (;;) {
+        if (nr >= rd->cap) return fail(PMSZ_ERR_CONVERGENCE, "no terminal round within the cap");
+        ++nr;
+        int64_t e = 0;
+        memset(&rr, 0, sizeof(rr));
+        pmsz_status st = pmsz_block_round(p, f, g, rd->lockstep, &e, &rr, stream);
+        if (st) return st;
+        // this round's replicas into the parity area of the round
+        const int64_t area = (int64_t)(++rd->rounds_total & 1) * rd->repl_doubles;
+        double* mine = (double*)rd->bufs[rd->rank] + area;
+        for (int x = 0; x < rd->nex; ++x) {
+            const Box& b = boxes[x];
+            const int64_t n = b.ext[0] * b.ext[1] * b.ext[2];
+            if (n == 0) continue;
+            k_box_pack<<<grid_for(n, 256), 256, 0, s>>>(b, g, mine + rd->ex_off[x]);
+            LAUNCHED();
+        }
+        const unsigned long long v[4] = {(unsigned long long)e, rr.shared_dirty ? 1ull : 0ull, 0ull, 0ull};
+        st = rounds_signal(p, rd, v, s);
+        if (st) return st;
+        const int64_t round_edits = (int64_t)p->hsig[0];
+        const bool any_dirty = p->hsig[1] != 0;
+        if (totals && nr - 1 < totals_cap) totals[nr - 1] = round_edits;
+        if (!lockstep && (round_edits == 0 || !any_dirty)) break;   // parallel.py:304-314
+        // _merge_min (parallel.py:122-140) pairwise over the full overlaps
+        int64_t changed = 0;
+        for (int x = 0; x < rd->nex; ++x) {
+            const double* theirs = (const double*)rd->bufs[rd->ex_peer[x]] + area + rd->ex_peer_off[x];
+            int64_t c = 0;
+            st = pmsz_box_merge_min(p, g, rd->ex_lo[x], rd->ex_hi[x], theirs, lockstep ? &c : nullptr, stream);
+            if (st) return st;
+            changed += c;
+        }
+        ++ns;
+        if (lockstep) {   // parallel.py:321-322
+            const unsigned long long w[4] = {(unsigned long long)changed, 0ull, 0ull, 0ull};
+            st = rounds_signal(p, rd, w, s);
+            if (st) return st;
+            if (round_edits == 0 && p->hsig[0] == 0) break;
+        }
+    }
+    if (rounds_out) *rounds_out = nr;
+    if (syncs_out) *syncs_out = ns;
+    if (r) *r = rr;
     return PMSZ_OK;
 }
 

@@ -135,7 +135,12 @@ class PeerTransport:
         self.world = len(blocks)
         self.xs = exchanges(blocks, rank)
         self.sent = 0
-        # layout of every rank's buffer: its overlaps in ascending-peer order, then 8 sum slots
+        # layout of every rank's buffer (identical offsets everywhere):
+        #   [0, R)            overlap replicas in ascending-peer order (parity 0)
+        #   [R, 2R)           the same, parity 1 (pmsz_rounds alternates)
+        #   [2R, 2R + 8)      sum slots of the Python round loop
+        #   sums_off ..       u64 sum slots [2][world][4] of pmsz_rounds
+        #   flags_off ..      u64 arrival epochs [world] of pmsz_rounds (zeroed at connect)
         self.layout = []
         for r in range(self.world):
             offs, o = {}, 0
@@ -143,7 +148,11 @@ class PeerTransport:
                 offs[x.peer] = o
                 o += x.size
             self.layout.append((offs, o))
-        n = max(o for _, o in self.layout) + 8
+        R = max(1, max(o for _, o in self.layout))
+        self.R = R
+        self.sums_off = 2 * R + 8
+        self.flags_off = self.sums_off + 2 * self.world * 4
+        n = self.flags_off + self.world
         self.buf = symm.empty(n, dtype=torch.float64, device=engine.device)
         self.n = n
 
@@ -152,8 +161,14 @@ class PeerTransport:
         n = self.n
         grp = (self.group or dist.group.WORLD).group_name
         self.h = symm.rendezvous(self.buf, grp)
-        self.sums = [self.h.get_buffer(r, (n,), torch.float64)[n - 8:] for r in range(self.world)]
-        self.n = n
+        self.buf.zero_()                  # arrival epochs start at 0 everywhere
+        torch.cuda.current_stream().synchronize()
+        self.h.barrier(channel=0)
+        py = 2 * self.R
+        self.sums = [self.h.get_buffer(r, (n,), torch.float64)[py:py + 8] for r in range(self.world)]
+        self.bufs = [self.h.get_buffer(r, (n,), torch.float64).data_ptr() for r in range(self.world)]
+        self.epoch = 0
+        self.rounds_total = 0
         # pinned staging of the round sums: no pageable copy (and its implicit
         # synchronisation) on the way in, one async copy + stream sync out
         self._hin = torch.zeros(8, dtype=torch.float64, pin_memory=True)
@@ -228,6 +243,43 @@ class PeerTransport:
     def release(self):
         self.h.barrier(channel=0)         # the loop ended without a merge: same protection
 
+    def device_rounds(self, engine, lockstep: bool, cap: int):
+        """The whole round loop in libpmsz (pmsz_rounds): one cross-rank epoch
+        barrier per round (two in lockstep) carrying the sums, replicas read
+        straight out of the peers' buffers; no Python between rounds.
+        Returns (rounds, syncs, edits per round, last block result)."""
+        import ctypes
+        from . import _native as N
+        if self.world > N.MAX_RANKS or len(self.xs) > N.MAX_EXCHANGES:
+            raise ValueError("too many ranks / exchanges for pmsz_rounds")
+        d = N.PmszRoundsDesc()
+        d.world, d.rank, d.nex, d.lockstep = self.world, self.rank, len(self.xs), int(bool(lockstep))
+        d.cap, d.repl_doubles, d.sums_off, d.flags_off = int(cap), self.R, self.sums_off, self.flags_off
+        d.epoch, d.rounds_total = self.epoch, self.rounds_total
+        for r, ptr in enumerate(self.bufs):
+            d.bufs[r] = ptr
+        offs, _ = self.layout[self.rank]
+        for k, x in enumerate(self.xs):
+            d.ex_peer[k] = x.peer
+            for a in range(3):
+                d.ex_lo[k][a] = x.lo[a]
+                d.ex_hi[k][a] = x.hi[a]
+            d.ex_off[k] = offs[x.peer]
+            d.ex_peer_off[k] = self.layout[x.peer][0][self.rank]
+        rounds, syncs = ctypes.c_int64(), ctypes.c_int64()
+        tot = (ctypes.c_int64 * max(1, int(cap)))() if cap <= 1 << 16 else (ctypes.c_int64 * (1 << 16))()
+        res = N.PmszResult()
+        st = N.lib().pmsz_rounds(engine.plan.handle, N.ptr(engine.f), N.ptr(engine.g), ctypes.byref(d),
+                                 ctypes.byref(rounds), ctypes.byref(syncs), tot, len(tot), ctypes.byref(res),
+                                 N.stream_handle())
+        self.epoch, self.rounds_total = int(d.epoch), int(d.rounds_total)
+        if st == N.PMSZ_ERR_CONVERGENCE:
+            raise ConvergenceError(N.last_error())
+        N.check(st, "pmsz_rounds")
+        nr = int(rounds.value)
+        self.sent += int(syncs.value) * sum(x.size * 8 for x in self.xs)
+        return nr, int(syncs.value), [int(tot[i]) for i in range(min(nr, len(tot)))], res
+
 
 def _agree(ok: bool, device, group=None) -> bool:
     """True on every rank iff it is True on every rank (MIN allreduce)."""
@@ -268,6 +320,16 @@ def run_distributed(engine, blocks, grid, rank: int, lockstep: bool, cap: int, g
     trace = os.environ.get("PMSZ_DIST_TRACE") == "1"
     tp = transport if transport is not None else CollectiveTransport(engine, blocks, rank, group)
     sent0 = tp.sent
+    if (isinstance(tp, PeerTransport) and isinstance(engine, DeviceEngine)
+            and os.environ.get("PMSZ_DEVLOOP", "1") != "0"):
+        t0 = time.perf_counter() if trace else 0.0
+        rounds, syncs, totals, res = tp.device_rounds(engine, lockstep, cap)
+        if trace:
+            _tick("device_rounds", t0)
+        engine.last = res
+        it, et, mve = engine.block_stats()
+        return DistStats("lockstep" if lockstep else "relaxed", tuple(int(v) for v in grid), rounds, syncs,
+                         tuple(totals), it, et, mve, tp.sent - sent0)
     rounds = syncs = 0
     totals: list[int] = []
     while True:
@@ -600,7 +662,9 @@ def bench_main(args, metric, unit, ClockSampler, measured_peaks, cpu_sample_inpu
     per_rank = [None] * world
     dist.all_gather_object(per_rank, {"rank": rank, "iterations": st.iterations, "edits": st.edit_total,
                                       "max_vertex_edits": st.max_vertex_edits, "ms": ms_local,
-                                      "sent_bytes_per_step": st.exchanged_bytes, "clocks": clk})
+                                      "sent_bytes_per_step": st.exchanged_bytes, "clocks": clk,
+                                      "trace_ms_per_step": ({k: round(1e3 * v / args.steps, 4) for k, v in TRACE.items()}
+                                                            if TRACE else None)})
     nvox = gdims[0] * gdims[1] * gdims[2]
     if rank == 0:
         peaks = measured_peaks()

@@ -39,10 +39,15 @@ def main():
         he = torch.from_numpy(np.ascontiguousarray(fh.reshape(nz, ny, nx)[sl]).reshape(-1)).to(dev)
         for lockstep in (False, True):
             ref_g, ref = (orc.run_parallel(dims, f, fh, xi, grid, lockstep) if rank == 0 else (None, None))
-            for kind in ("peer", "collective"):
+            for kind in ("peer", "collective", "devloop"):
                 eng = pdist.DeviceEngine(b, dims, fe, he, cfg)
                 eng.prepare()
-                tp = (pdist.PeerTransport if kind == "peer" else pdist.CollectiveTransport)(eng, blocks, rank)
+                os.environ["PMSZ_DEVLOOP"] = "1" if kind == "devloop" else "0"
+                if kind in ("peer", "devloop"):
+                    tp = pdist.PeerTransport(eng, blocks, rank)
+                    tp.connect()
+                else:
+                    tp = pdist.CollectiveTransport(eng, blocks, rank)
                 st = pdist.run_distributed(eng, blocks, grid, rank, lockstep, cfg.max_outer_iterations, transport=tp)
                 sp = eng.spec
                 ed = sp.dims
