@@ -20,6 +20,7 @@
 #include <vector>
 #include <atomic>
 #include <algorithm>
+#include <thread>
 
 #include "../../include/pmsz.h"
 #include "common.cuh"
@@ -480,6 +481,24 @@ __global__ void __launch_bounds__(PMSZ_MAX_RANKS) k_signal(SigArgs a) {
     }
 }
 
+// g_host[ids[i]] = vals[i] (the edit record onto the streamed-back fhat), on
+// a few host threads: ids are ascending, so each thread writes one contiguous
+// range of the field.
+void patch_host(double* g, const int64_t* ids, const double* vals, int64_t m) {
+    const int64_t per = 1 << 18;
+    const int nt = (int)std::min<int64_t>(std::max(1u, std::thread::hardware_concurrency()) / 2 + 1,
+                                          std::max<int64_t>(1, (m + per - 1) / per));
+    auto work = [&](int t) {
+        const int64_t a = m * t / nt, b = m * (t + 1) / nt;
+        for (int64_t i = a; i < b; ++i) g[ids[i]] = vals[i];
+    };
+    if (nt == 1) { work(0); return; }
+    std::vector<std::thread> th;
+    for (int t = 1; t < nt; ++t) th.emplace_back(work, t);
+    work(0);
+    for (auto& x : th) x.join();
+}
+
 }  // namespace
 
 // ============================================================================
@@ -549,6 +568,11 @@ struct pmsz_plan {
     std::vector<cudaEvent_t> stage_ev;    // [0]: staging free; [1 + c]: slab c landed
     std::vector<int64_t> stage_z;         // slab boundaries in z (nslabs + 1)
     bool stage_pending = false;           // the next K0 waits for the slabs, one launch per slab
+    cudaStream_t d2h_stream = nullptr;    // corrected-field slabs back to the host (pmsz_run_correction_host)
+    cudaEvent_t d2h_done = nullptr;
+    int64_t* hrec_ids = nullptr;          // pinned bounce buffers of the edit record (field patch)
+    double* hrec_vals = nullptr;
+    int64_t hrec_cap = 0;
     unsigned long long* dsig = nullptr;   // pmsz_rounds: the summed round values (device) ...
     unsigned long long* hsig = nullptr;   // ... and their pinned mirror
 };
@@ -1279,6 +1303,10 @@ void pmsz_plan_destroy(pmsz_plan* p) {
     cudaFree(p->stage_f); cudaFree(p->stage_g); cudaFree(p->stage_ids); cudaFree(p->stage_vals);
     for (cudaEvent_t e : p->stage_ev) cudaEventDestroy(e);
     cudaFree(p->dsig);
+    if (p->d2h_stream) cudaStreamDestroy(p->d2h_stream);
+    if (p->d2h_done) cudaEventDestroy(p->d2h_done);
+    if (p->hrec_ids) cudaFreeHost(p->hrec_ids);
+    if (p->hrec_vals) cudaFreeHost(p->hrec_vals);
     if (p->hsig) cudaFreeHost(p->hsig);
     if (p->copy_stream) cudaStreamDestroy(p->copy_stream);
     for (cudaEvent_t e : p->prof_ev) cudaEventDestroy(e);
@@ -1766,30 +1794,72 @@ pmsz_status pmsz_run_correction_host(pmsz_plan* p, const void* f_host, const dou
         CUDA_TRY(cudaMemcpyAsync(g + o, fh_host + o, m * 8, cudaMemcpyHostToDevice, p->copy_stream));
         CUDA_TRY(cudaEventRecord(p->stage_ev[1 + c], p->copy_stream));
     }
+    // Corrected field out: g equals fhat except at the edits, so the host copy
+    // is streamed back slab by slab as soon as each fhat slab has landed --
+    // the device-to-host direction of the link runs concurrently with the
+    // host-to-device slabs -- and is patched with the edit record at the end.
+    // (A slab may be read while the loop already edits it: every such vertex
+    // is in the edit record and gets its final value from the patch.)
+    if (g_host) {
+        if (!p->d2h_stream) CUDA_TRY(cudaStreamCreateWithFlags(&p->d2h_stream, cudaStreamNonBlocking));
+        if (!p->d2h_done) CUDA_TRY(cudaEventCreateWithFlags(&p->d2h_done, cudaEventDisableTiming));
+        for (int64_t c = 0; c < nsl; ++c) {
+            const int64_t o = p->stage_z[c] * plane, m = (p->stage_z[c + 1] - p->stage_z[c]) * plane;
+            CUDA_TRY(cudaStreamWaitEvent(p->d2h_stream, p->stage_ev[1 + c], 0));
+            CUDA_TRY(cudaMemcpyAsync(g_host + o, g + o, m * 8, cudaMemcpyDeviceToHost, p->d2h_stream));
+        }
+        CUDA_TRY(cudaEventRecord(p->d2h_done, p->d2h_stream));
+    }
     p->stage_pending = true;
     st = pmsz_run_correction(p, f, g, g, history, history_cap, r, stream);
     p->stage_pending = false;
     CUDA_TRY(cudaStreamWaitEvent(s, p->stage_ev[nsl], 0));   // (already waited by K0 unless it failed early)
-    if (st == PMSZ_OK) {
-        if (g_host) CUDA_TRY(cudaMemcpyAsync(g_host, g, gbytes, cudaMemcpyDeviceToHost, s));
-        if (ids_host && vals_host && edits_cap > 0 && r && r->edit_count > 0) {
-            const int64_t m = std::min(edits_cap, r->edit_count);
-            if (m > p->stage_cap) {
-                cudaFree(p->stage_ids);
-                cudaFree(p->stage_vals);
-                p->stage_ids = nullptr;
-                p->stage_vals = nullptr;
-                p->scratch_bytes -= p->stage_cap * 16;
-                p->stage_cap = 0;
-                const int64_t want = std::min<int64_t>(p->n, std::max<int64_t>(m, m + m / 4));
-                if (!grow((void**)&p->stage_ids, want * 8) || !grow((void**)&p->stage_vals, want * 8))
-                    return fail(PMSZ_ERR_CUDA, "staging allocation failed");
-                p->stage_cap = want;
+    if (g_host) CUDA_TRY(cudaStreamWaitEvent(s, p->d2h_done, 0));
+    if (st == PMSZ_OK && r && r->edit_count > 0 && (g_host || (ids_host && vals_host && edits_cap > 0))) {
+        const int64_t count = r->edit_count;
+        // the whole record when the field is patched from it, else what fits the caller's buffers
+        const int64_t m = g_host ? count : std::min(edits_cap, count);
+        if (m > p->stage_cap) {
+            cudaFree(p->stage_ids);
+            cudaFree(p->stage_vals);
+            p->stage_ids = nullptr;
+            p->stage_vals = nullptr;
+            p->scratch_bytes -= p->stage_cap * 16;
+            p->stage_cap = 0;
+            const int64_t want = std::min<int64_t>(p->n, std::max<int64_t>(m, m + m / 4));
+            if (!grow((void**)&p->stage_ids, want * 8) || !grow((void**)&p->stage_vals, want * 8))
+                return fail(PMSZ_ERR_CUDA, "staging allocation failed");
+            p->stage_cap = want;
+        }
+        st = pmsz_edits_export(p, g, p->stage_ids, p->stage_vals, m, nullptr, stream);
+        if (st == PMSZ_OK) {
+            // host destination of the full record: the caller's buffers when they
+            // hold it, else the plan's pinned bounce buffers
+            const bool direct = ids_host && vals_host && edits_cap >= m;
+            int64_t* hid = ids_host;
+            double* hval = vals_host;
+            if (!direct) {
+                if (p->hrec_cap < m) {
+                    if (p->hrec_ids) cudaFreeHost(p->hrec_ids);
+                    if (p->hrec_vals) cudaFreeHost(p->hrec_vals);
+                    p->hrec_ids = nullptr;
+                    p->hrec_vals = nullptr;
+                    p->hrec_cap = 0;
+                    CUDA_TRY(cudaMallocHost((void**)&p->hrec_ids, m * 8));
+                    CUDA_TRY(cudaMallocHost((void**)&p->hrec_vals, m * 8));
+                    p->hrec_cap = m;
+                }
+                hid = p->hrec_ids;
+                hval = p->hrec_vals;
             }
-            st = pmsz_edits_export(p, g, p->stage_ids, p->stage_vals, m, nullptr, stream);
-            if (st == PMSZ_OK) {
-                CUDA_TRY(cudaMemcpyAsync(ids_host, p->stage_ids, m * 8, cudaMemcpyDeviceToHost, s));
-                CUDA_TRY(cudaMemcpyAsync(vals_host, p->stage_vals, m * 8, cudaMemcpyDeviceToHost, s));
+            CUDA_TRY(cudaMemcpyAsync(hid, p->stage_ids, m * 8, cudaMemcpyDeviceToHost, s));
+            CUDA_TRY(cudaMemcpyAsync(hval, p->stage_vals, m * 8, cudaMemcpyDeviceToHost, s));
+            CUDA_TRY(cudaStreamSynchronize(s));
+            if (g_host) patch_host(g_host, hid, hval, m);
+            if (!direct && ids_host && vals_host && edits_cap > 0) {
+                const int64_t k = std::min(edits_cap, count);
+                memcpy(ids_host, hid, k * 8);
+                memcpy(vals_host, hval, k * 8);
             }
         }
     }
