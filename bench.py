@@ -464,7 +464,8 @@ def e2e_host(args, plan, f32, fh, dims, nvox, dev_res) -> dict:
     return {"value": nvox / dt, "unit": UNIT, "h2d_bytes_per_step": nvox * (4 + 8),
             "d2h_bytes_per_step": nvox * 8 + edits * 16 + 8 * int(res.iterations), "ms_per_step": dt * 1e3,
             "path": "pmsz_run_correction_host (pinned host f32 f + f64 fhat in; corrected f64 field + edit "
-                    "ids/values out; input copied in z-slabs overlapped with K0)",
+                    "ids/values out; input copied in z-slabs overlapped with K0, the field streamed back slab by "
+                    "slab concurrently and patched with the edit record)",
             "check": check}
 
 
