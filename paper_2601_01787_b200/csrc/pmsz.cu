@@ -21,6 +21,7 @@
 #include <atomic>
 #include <algorithm>
 #include <thread>
+#include <chrono>
 
 #include "../../include/pmsz.h"
 #include "common.cuh"
@@ -485,8 +486,10 @@ __global__ void __launch_bounds__(PMSZ_MAX_RANKS) k_signal(SigArgs a) {
 // a few host threads: ids are ascending, so each thread writes one contiguous
 // range of the field.
 void patch_host(double* g, const int64_t* ids, const double* vals, int64_t m) {
-    const int64_t per = 1 << 18;
-    const int nt = (int)std::min<int64_t>(std::max(1u, std::thread::hardware_concurrency()) / 2 + 1,
+    // latency-bound (one cache line per write, ~30 values apart): every host
+    // thread, at least 64 k writes each
+    const int64_t per = 1 << 16;
+    const int nt = (int)std::min<int64_t>(std::min(64u, std::max(1u, std::thread::hardware_concurrency())),
                                           std::max<int64_t>(1, (m + per - 1) / per));
     auto work = [&](int t) {
         const int64_t a = m * t / nt, b = m * (t + 1) / nt;
@@ -1810,11 +1813,19 @@ pmsz_status pmsz_run_correction_host(pmsz_plan* p, const void* f_host, const dou
         }
         CUDA_TRY(cudaEventRecord(p->d2h_done, p->d2h_stream));
     }
+    static const bool etrace = getenv("PMSZ_E2E_TRACE") != nullptr;
+    auto now = [] { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
+    double t0 = etrace ? now() : 0.0, t1 = 0, t2 = 0, t3 = 0;
     p->stage_pending = true;
     st = pmsz_run_correction(p, f, g, g, history, history_cap, r, stream);
     p->stage_pending = false;
+    if (etrace) t1 = now();
     CUDA_TRY(cudaStreamWaitEvent(s, p->stage_ev[nsl], 0));   // (already waited by K0 unless it failed early)
     if (g_host) CUDA_TRY(cudaStreamWaitEvent(s, p->d2h_done, 0));
+    if (etrace) {
+        cudaStreamSynchronize(s);
+        t2 = now();
+    }
     if (st == PMSZ_OK && r && r->edit_count > 0 && (g_host || (ids_host && vals_host && edits_cap > 0))) {
         const int64_t count = r->edit_count;
         // the whole record when the field is patched from it, else what fits the caller's buffers
@@ -1855,6 +1866,7 @@ pmsz_status pmsz_run_correction_host(pmsz_plan* p, const void* f_host, const dou
             CUDA_TRY(cudaMemcpyAsync(hid, p->stage_ids, m * 8, cudaMemcpyDeviceToHost, s));
             CUDA_TRY(cudaMemcpyAsync(hval, p->stage_vals, m * 8, cudaMemcpyDeviceToHost, s));
             CUDA_TRY(cudaStreamSynchronize(s));
+            if (etrace) t3 = now();
             if (g_host) patch_host(g_host, hid, hval, m);
             if (!direct && ids_host && vals_host && edits_cap > 0) {
                 const int64_t k = std::min(edits_cap, count);
@@ -1864,6 +1876,9 @@ pmsz_status pmsz_run_correction_host(pmsz_plan* p, const void* f_host, const dou
         }
     }
     CUDA_TRY(cudaStreamSynchronize(s));
+    if (etrace)
+        fprintf(stderr, "e2e: run %.2f ms, d2h field wait %.2f, record %.2f, patch + copy-out %.2f (total %.2f)\n", t1 - t0,
+                t2 - t1, t3 - t2, now() - t3, now() - t0);
     return st;
 }
 
