@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-dropin", action="store_true", help="skip the drop-in run_correction(ScalarField) timing")
+    ap.add_argument("--f64-original", action="store_true",
+                    help="pass the original field as f64 (the K0 variant for fields that are not f32-exact)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-z", type=int, default=64, help="z-planes of the CPU baseline sample")
     ap.add_argument("--full-sweeps", action="store_true", help="disable incremental dirty-ring sweeps")
@@ -244,8 +246,11 @@ def run_ours_single(args):
     xi = gen.relative_to_absolute_range(lo, hi, args.rel)
     fh = gen.quantize_device(f32, xi, lo, hi)
     cfg = pm.CorrectionConfig(xi_abs=xi)
+    if args.f64_original:   # the same values, handed over as f64 (f64 K0)
+        f32 = f32.double()
     plan = DomainPlan(DomainSpec.whole(dims), cfg.xi_abs, cfg.tau, cfg.max_outer_iterations,
-                      incremental=not args.full_sweeps, f32_original=True, extrema_only=wl["extrema_only"])
+                      incremental=not args.full_sweeps, f32_original=not args.f64_original,
+                      extrema_only=wl["extrema_only"])
     g = torch.empty_like(fh)
     stream = torch.cuda.current_stream()
 
@@ -285,7 +290,7 @@ def run_ours_single(args):
     # roofline of the dominant kernels (algorithmic bytes per launch / event time)
     peaks = measured_peaks()
     peak = float(peaks.get("hbm_gbs", 6650.0))
-    per_voxel = {"sweep_full": 9, "verify": 9, "prep": 4 + 8 + 8 + 1}   # full-domain kernels only
+    per_voxel = {"sweep_full": 9, "verify": 9, "prep": f32.element_size() + 8 + 8 + 1}   # full-domain kernels only
     kernels = {}
     for name, (kms, cnt) in prof.items():
         if name not in per_voxel:
@@ -388,7 +393,7 @@ def reference_pin(args, wl, f32, fh, res) -> dict:
         out["reference_pin"] = "no reference digest for this workload"
         return out
     s = ref["serial"]
-    inputs_ok = _sha(f32) == ref["f32_sha256"] and _sha(fh) == ref["fhat_sha256"]
+    inputs_ok = _sha(f32.float()) == ref["f32_sha256"] and _sha(fh) == ref["fhat_sha256"]
     match = (inputs_ok and out["corrected_sha256"] == s["corrected_sha256"] and out["ids_sha256"] == s["ids_sha256"]
              and out["vals_sha256"] == s["vals_sha256"] and list(res.edits_per_iteration) == s["edits_per_iteration"]
              and res.max_vertex_edits == s["max_vertex_edits"])
@@ -435,7 +440,7 @@ def e2e_host(args, plan, f32, fh, dims, nvox, dev_res) -> dict:
     from paper_2601_01787_b200 import _native as N
     L = N.lib()
     fh_host = torch.empty(nvox, dtype=torch.float64, pin_memory=True)
-    f_host = torch.empty(nvox, dtype=torch.float32, pin_memory=True)
+    f_host = torch.empty(nvox, dtype=f32.dtype, pin_memory=True)
     fh_host.copy_(fh)
     f_host.copy_(f32)
     cap = nvox // 8

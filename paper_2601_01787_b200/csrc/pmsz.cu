@@ -689,7 +689,9 @@ pmsz_status launch_apply(pmsz_plan* p, const void* f, double* g, cudaStream_t s,
     // one CTA per SM: fewer targets in flight keep the z-window of the sorted
     // target list (g, prop, f, counts) L2-resident -- 10 % faster than 8 / SM
     static const int apply_per_sm = getenv("PMSZ_APPLY_PER_SM") ? atoi(getenv("PMSZ_APPLY_PER_SM")) : 1;
-    k_apply_list<FT><<<grid_for(bound, 256, apply_per_sm), 256, 0, s>>>(p->dom, (const FT*)f, g, p->w, nxt);
+    Work w = p->w;
+    w.first_apply = p->iterations == 0 ? 1 : 0;   // nothing edited yet: no counts / editbits reads
+    k_apply_list<FT><<<grid_for(bound, 256, apply_per_sm), 256, 0, s>>>(p->dom, (const FT*)f, g, w, nxt);
     LAUNCHED();
     if (p->w.incremental) {   // list-mode ring marking (no-op when the edits went to the bitmap)
         k_mark_list<<<grid_for(std::min<int64_t>(15 * bound, (int64_t)p->w.mark_limit), 256, 4), 256, 0, s>>>(

@@ -51,7 +51,7 @@ struct Work {
     uint32_t* detbits;          // n bits: centre had a detection at its latest evaluation
     uint32_t* iteredit;         // n bits: edited in this iteration (bitmap-mode marking)
     uint32_t* elist;            // edits of a list-mode iteration (ring marking input)
-    void* counts;               // per-vertex edit counts: u16, or u32 when counts32
+    void* counts;               // per-vertex edit counts MINUS ONE where editbits is set (0 elsewhere): u16, or u32 when counts32
     int counts32;               // the iteration cap exceeds 65535 (a vertex is edited at most once per iteration)
     uint8_t* code;              // packed f-code
     const uint32_t* frag;       // n bits: fragile centres (K0); null = every centre is evaluated
@@ -62,6 +62,7 @@ struct Work {
     int64_t nwords;
     int incremental;
     int track;                  // append first-touched targets to `work`
+    int first_apply;            // the run's first apply: no vertex was edited before (counts / editbits not read)
 };
 
 // Warp-aggregated append: returns the slot of this thread in `counter`.
@@ -324,8 +325,16 @@ struct TargetOps {
 template <typename FT>
 __device__ __forceinline__ TargetOps load_target(const FT* __restrict__ f, const double* __restrict__ g,
                                                  const Work& w, int64_t t) {
-    const unsigned int cnt = w.counts32 ? __ldcg((const unsigned int*)w.counts + t)
-                                        : (unsigned int)__ldcg((const uint16_t*)w.counts + t);
+    // edits so far: 0 unless the ever-edited bit is set, then 1 + the stored
+    // extra count (a first edit writes nothing to `counts`); the run's first
+    // apply knows every count is 0 and reads neither array
+    unsigned int cnt = 0;
+    if (!w.first_apply) {
+        const uint32_t ew = __ldcg(w.editbits + (t >> 5));
+        const unsigned int extra = w.counts32 ? __ldcg((const unsigned int*)w.counts + t)
+                                              : (unsigned int)__ldcg((const uint16_t*)w.counts + t);
+        cnt = ((ew >> (t & 31)) & 1u) ? extra + 1u : 0u;
+    }
     return TargetOps{__ldcg(w.prop + t), __ldcg(g + t), (double)f[t], cnt};
 }
 
@@ -343,8 +352,10 @@ __device__ __forceinline__ void apply_target(const Dom& d, const FT* __restrict_
         g[t] = nv;
         ++acc.edits;
         const unsigned int cnt = op.cnt + 1u;
-        if (w.counts32) ((unsigned int*)w.counts)[t] = cnt;
-        else ((uint16_t*)w.counts)[t] = (uint16_t)cnt;   // cnt <= iterations <= 65535 (plan_create)
+        if (op.cnt) {   // a re-edit: store the extra count (cnt - 1 <= iterations <= 65535 for u16)
+            if (w.counts32) ((unsigned int*)w.counts)[t] = cnt - 1u;
+            else ((uint16_t*)w.counts)[t] = (uint16_t)(cnt - 1u);
+        }
         acc.maxc = max(acc.maxc, cnt);
         atomicOr(w.editbits + (t >> 5), 1u << (t & 31));
         if (w.edited_mask) w.edited_mask[t] = 1;

@@ -346,8 +346,10 @@ __device__ __forceinline__ void t1_apply_mark(const Dom& d, const FT* __restrict
     g[t] = nv;
     ++acc.edits;
     const unsigned int cnt = op.cnt + 1u;
-    if (w.counts32) ((unsigned int*)w.counts)[t] = cnt;
-    else ((uint16_t*)w.counts)[t] = (uint16_t)cnt;
+    if (op.cnt) {   // a re-edit: store the extra count (apply_target)
+        if (w.counts32) ((unsigned int*)w.counts)[t] = cnt - 1u;
+        else ((uint16_t*)w.counts)[t] = (uint16_t)(cnt - 1u);
+    }
     acc.maxc = max(acc.maxc, cnt);
     atomicOr(w.editbits + (t >> 5), 1u << (t & 31));
     acc.shared |= in_shared(d, x, y, z);
