@@ -260,7 +260,7 @@ def run_ours_single(args):
     for _ in range(max(args.warmup, 3)):
         res = step()
     torch.cuda.synchronize()
-    # events around the full-domain launches only: timing all ~190 launches of
+    # events around the full-domain launches only: timing all ~40 launches of
     # a step costs ~0.15 ms (tools/prof_overhead.py); the breakdown of the
     # other kernel classes comes from a separate profiled pass below
     plan.profile(True, full_domain_only=True)

@@ -136,7 +136,7 @@ int64_t pmsz_plan_scratch_bytes(const pmsz_plan* plan);
 /* Time every kernel launch of this plan with CUDA events on its stream
  * (enable != 0; enable == PMSZ_PROFILE_FULL_DOMAIN: only the full-domain
  * classes PREP / SWEEP_FULL / VERIFY, whose events cost nothing measurable --
- * timing all ~190 launches of a step adds ~0.15 ms at 512^3).
+ * timing all ~40 launches of a step adds ~0.15 ms at 512^3).
  * pmsz_profile_read returns the accumulated device time (ms) and launch count
  * per kernel class (arrays of PMSZ_K_COUNT) and optionally resets. */
 #define PMSZ_PROFILE_FULL_DOMAIN 2

@@ -511,7 +511,9 @@ def _e2e_host(args, eng, blocks, grid, rank, lockstep, cap, dev, nvox_total, tp=
     dist.all_reduce(io)
     return {"value": nvox_total / sec, "unit": "voxels/s", "h2d_bytes_per_step": int(io[0].item()),
             "d2h_bytes_per_step": int(io[1].item()), "ms_per_step": sec * 1e3, "bytes": "summed over ranks",
-            "path": "per rank: pinned host ext slab in, DeviceEngine + NCCL round loop, edit record out"}
+            "path": ("per rank: pinned host ext slab in, DeviceEngine + "
+                     + ("pmsz_rounds over NVLink peer memory" if isinstance(tp, PeerTransport) else "NCCL round loop")
+                     + ", edit record out")}
 
 
 # ---------------------------------------------------------------------------

@@ -516,3 +516,29 @@ def test_floor_violation_raises_like_the_reference():
     assert orc.run_correction(dims, f, fh, xi).status == orc.ORC_MONOTONE
     with pytest.raises(AssertionError):
         pm.run_correction(pm.ScalarField(dims, f), pm.ScalarField(dims, fh), pm.CorrectionConfig(xi_abs=xi))
+
+
+def test_residual_and_bound_detection_on_crafted_fields():
+    """The two post-loop checks of run_correction (correction.py:422-426) are
+    unreachable from valid inputs (every zero-edit iteration is clean and g
+    stays in [L, U]); exercise the device checks directly: a full K4 count
+    sweep must report the per-kind detections of a distorted field exactly as
+    the oracle does, and the dense bound check must count g outside [f - xi, f + xi]."""
+    from paper_2601_01787_b200.engine import DomainPlan, DomainSpec
+    dims = (40, 36, 28)
+    f = orc.perlin(dims, 8)
+    xi = orc.relative_to_absolute(f, 1e-2)
+    g = orc.quantize(f, xi)   # a decompressed field with distortions
+    plan = DomainPlan(DomainSpec.whole(dims), xi, xi / 1024.0, 1, incremental=False)
+    fd = torch.from_numpy(f).to(DEV)
+    gd = torch.from_numpy(g).to(DEV)
+    st, _ = plan.prepare(fd, gd, torch.empty_like(gd))
+    assert st == 0
+    kinds = plan.verify(gd)
+    assert kinds == orc.residual_kinds(dims, f, g) and sum(kinds) > 0
+    bad = g.copy()
+    idx = np.array([3, 777, 12345, f.size - 1])
+    bad[idx[:2]] = f[idx[:2]] + 2 * xi     # above U
+    bad[idx[2:]] = f[idx[2:]] - 2 * xi     # below L
+    assert plan.bounds_violations(fd, torch.from_numpy(bad).to(DEV)) == 4
+    plan.close()

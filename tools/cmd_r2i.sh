@@ -1,0 +1,6 @@
+mkdir -p gpurun_out; timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/gputests_r2i.log 2>&1; echo tests=$?; tail -2 gpurun_out/gputests_r2i.log; nproc
+PMSZ_E2E_TRACE=1 timeout 300 python bench.py --no-cpu-baseline --no-dropin --steps 3 2>&1 | grep -E "e2e:" | tail -2
+timeout 300 python bench.py --no-cpu-baseline --no-dropin > gpurun_out/b_r2i.json 2>&1
+timeout 300 python bench.py --no-cpu-baseline --no-dropin --f64-original > gpurun_out/b64.json 2>&1
+for f in b_r2i b64; do python -c "
+import json; d=json.load(open('gpurun_out/$f.json')); print('$f', round(d['ms_per_step'],3), {k:round(v['ms_total_per_step'],3) for k,v in d['roofline']['per_kernel'].items()}, d['e2e']['ms_per_step'], d['result']['reference_pin']['bit_exact'], d['result']['residual'])"; done

@@ -65,10 +65,62 @@ def main():
                     bad += not ok
                     print(f"{'OK ' if ok else 'BAD'} dims={dims} grid={grid} {'lockstep' if lockstep else 'relaxed'} "
                           f"{kind} rounds={st.rounds} syncs={st.syncs}", flush=True)
+    bad += golden_256(rank, world, dev)
     t = torch.tensor([bad], device=dev)
     dist.broadcast(t, 0)
     dist.destroy_process_group()
     return int(t.item())
+
+
+def golden_256(rank, world, dev) -> int:
+    """Benchmark-scale multi-GPU parity: Perlin 256^3 (seed 0, f32, rel 1e-4,
+    quantizer) on z-slabs (1, 1, world), relaxed, the C round loop over NVLink
+    -- the corrected field and the whole ParallelStats against the
+    reference's own run_parallel (tests/golden/golden_large.json, c256)."""
+    import hashlib
+    import json
+    from paper_2601_01787_b200 import inputs as gen
+    ref = json.loads((Path(__file__).resolve().parent.parent / "tests" / "golden" / "golden_large.json").read_text())
+    case = next((c for c in ref["c256"]["parallel"] if c["grid"] == [1, 1, world] and c["strategy"] == "relaxed"), None)
+    if case is None:
+        return 0
+    dims = (256, 256, 256)
+    blocks = pm.decompose(dims, (1, 1, world)).blocks
+    b = blocks[rank]
+    spec = gen.NoiseSpec(dims, 0)
+    f32 = gen.perlin_device(spec, lo=b.ext_start, ext=b.ext_dims, f32=True, device=dev)
+    lo, hi = gen.minmax_device(f32)
+    mm = torch.tensor([-lo, hi], dtype=torch.float64, device=dev)
+    dist.all_reduce(mm, op=dist.ReduceOp.MAX)
+    glo, ghi = -float(mm[0].item()), float(mm[1].item())
+    xi = gen.relative_to_absolute_range(glo, ghi, 1e-4)
+    fh = gen.quantize_device(f32, xi, glo, ghi)
+    cfg = pm.CorrectionConfig(xi_abs=xi)
+    eng = pdist.DeviceEngine(b, dims, f32, fh, cfg)
+    eng.prepare()
+    os.environ["PMSZ_DEVLOOP"] = "1"
+    tp = pdist.make_transport(eng, blocks, rank)
+    st = pdist.run_distributed(eng, blocks, (1, 1, world), rank, False, cfg.max_outer_iterations, transport=tp)
+    sp = eng.spec
+    nx, ny = dims[0], dims[1]
+    core = eng.g[sp.core_lo[2] * nx * ny: sp.core_hi[2] * nx * ny].contiguous()
+    parts = [torch.empty_like(core) for _ in range(world)]   # equal slabs: 256 % world == 0
+    dist.all_gather(parts, core)
+    stats = [None] * world
+    dist.all_gather_object(stats, eng.block_stats())
+    if rank != 0:
+        return 0
+    g = torch.cat(parts).cpu().numpy()
+    d = case["stats"]
+    ok = (hashlib.sha256(g.tobytes()).hexdigest() == case["corrected_sha256"]
+          and (st.rounds, st.syncs) == (d["rounds"], d["syncs"])
+          and list(st.edits_per_round) == case["edits_per_iteration"]
+          and [s[0] for s in stats] == d["per_block_iterations"]
+          and [s[1] for s in stats] == d["per_block_edit_totals"]
+          and [s[2] for s in stats] == d["per_block_max_vertex_edits"])
+    print(f"{'OK ' if ok else 'BAD'} dims={dims} grid=(1, 1, {world}) relaxed devloop vs reference run_parallel "
+          f"(golden_large c256) rounds={st.rounds} syncs={st.syncs}", flush=True)
+    return int(not ok)
 
 
 if __name__ == "__main__":
