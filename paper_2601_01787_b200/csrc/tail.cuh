@@ -277,7 +277,7 @@ constexpr int kT1SetBits = 13;
 constexpr uint32_t kT1Empty = 0xffffffffu;
 // hand-over threshold of the grid tail: the one-CTA iteration beats the grid
 // barriers below about a thousand dirty centres (PMSZ_TAIL1_MAX overrides)
-constexpr int kT1Handover = 1024;
+constexpr int kT1Handover = 512;
 
 struct T1Smem {
     uint32_t dirty[2][kT1Dirty];
