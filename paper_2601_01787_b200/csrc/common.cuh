@@ -128,6 +128,48 @@ __device__ __forceinline__ Scan fold_scan(double vc, const double (&nv)[14]) {
     return s;
 }
 
+// One (value, rank) match; the right operand always holds the higher ranks,
+// so ties go right for the max (larger id) and left for the min (smaller id).
+__device__ __forceinline__ void mmax(double& v, int& r, double v2, int r2) {
+    const bool t = v2 >= v;
+    v = t ? v2 : v;
+    r = t ? r2 : r;
+}
+__device__ __forceinline__ void mmin(double& v, int& r, double v2, int r2) {
+    const bool t = v2 < v;
+    v = t ? v2 : v;
+    r = t ? r2 : r;
+}
+
+// fold_scan (common.cuh) for a complete ring (no missing neighbour) as a
+// balanced tree: the same argmax / argmin under the (value, rank) order.
+__device__ __forceinline__ Scan tree_scan(double vc, const double (&nv)[14]) {
+    double ax[7], an[7];
+    int rx[7], rn[7];
+#pragma unroll
+    for (int k = 0; k < 7; ++k) {
+        // one compare serves both sides (no NaN here): ties -> right for the
+        // max (larger id), left for the min (smaller id)
+        const bool t = nv[2 * k + 1] >= nv[2 * k];
+        ax[k] = t ? nv[2 * k + 1] : nv[2 * k];
+        rx[k] = 2 * k + (t ? 1 : 0);
+        an[k] = t ? nv[2 * k] : nv[2 * k + 1];
+        rn[k] = 2 * k + (t ? 0 : 1);
+    }
+    mmax(ax[0], rx[0], ax[1], rx[1]); mmin(an[0], rn[0], an[1], rn[1]);   // 0-3
+    mmax(ax[2], rx[2], ax[3], rx[3]); mmin(an[2], rn[2], an[3], rn[3]);   // 4-7
+    mmax(ax[4], rx[4], ax[5], rx[5]); mmin(an[4], rn[4], an[5], rn[5]);   // 8-11
+    mmax(ax[0], rx[0], ax[2], rx[2]); mmin(an[0], rn[0], an[2], rn[2]);   // 0-7
+    mmax(ax[4], rx[4], ax[6], rx[6]); mmin(an[4], rn[4], an[6], rn[6]);   // 8-13
+    mmax(ax[0], rx[0], ax[4], rx[4]); mmin(an[0], rn[0], an[4], rn[4]);   // 0-13
+    Scan s;
+    s.vc = vc;
+    s.vmax = ax[0]; s.vmin = an[0]; s.rmax = rx[0]; s.rmin = rn[0];
+    s.is_max = (ax[0] < vc) || (ax[0] == vc && rx[0] <= kCenterBelow);   // topology.py:79
+    s.is_min = (an[0] > vc) || (an[0] == vc && rn[0] > kCenterBelow);    // topology.py:80
+    return s;
+}
+
 __device__ __forceinline__ void coords(const Dom& d, int64_t c, int64_t& x, int64_t& y, int64_t& z) {
     const uint32_t cc = (uint32_t)c;
     const uint32_t zz = fast_div(cc, d.msz);

@@ -83,6 +83,17 @@ __device__ __forceinline__ bool robust2(const T2<double>& a, double thr, double)
            a.sn > __dadd_ru(__dadd_ru(a.mn, thr), 0x1p-50 * fabs(a.mn));
 }
 
+// f64 fields screened in f32 (k_prep_q): rounding to f32 is monotone, so the
+// f32 top-2 / bottom-2 are the images of the f64 ones, each within 2^-24 |v|;
+// the gap test absorbs both roundings (and the 2^-50 |v| of robust2's f64
+// form) in 2^-22 max|v| plus an absolute 2^-120 for subnormal images.  Values
+// beyond the f32 range become +-inf and fail the test (fragile: exact code).
+__device__ __forceinline__ bool robust2_narrowed(const T2<float>& a, float thr32) {
+    const float sx = __fadd_ru(__fmul_ru(0x1p-22f, fmaxf(fabsf(a.mx), fabsf(a.sx))), 0x1p-120f);
+    const float sn = __fadd_ru(__fmul_ru(0x1p-22f, fmaxf(fabsf(a.mn), fabsf(a.sn))), 0x1p-120f);
+    return a.sx < __fsub_rd(__fsub_rd(a.mx, thr32), sx) && a.sn > __fadd_ru(__fadd_ru(a.mn, thr32), sn);
+}
+
 // Exact f-code of a queued centre (fold_scan / tree_scan on V values; NaN =
 // outside the field, only in the fold).
 template <typename V>
@@ -228,7 +239,8 @@ __global__ void __launch_bounds__(256, sizeof(FT) == 4 ? PMSZ_PREP_MINB : 2) k_p
     const int col = xo + tx;                 // staged column of x - 1
     const int row0 = kQRowsPerThread * ty;   // staged row of y_0 - 1
     unsigned nfrag = 0, ndet = 0;
-    using V = FT;
+    using V = FT;       // staged values (exact f-codes of the fragile centres)
+    using SV = float;   // screen values: f32 for both field types (robust2_narrowed for f64)
 
     // The closed ring of centre (x, y_r, p) is covered by four 2 x 2 boxes:
     // D = lb of plane p-1, the in-plane part lb + rb of plane p (they share the
@@ -241,15 +253,15 @@ __global__ void __launch_bounds__(256, sizeof(FT) == 4 ? PMSZ_PREP_MINB : 2) k_p
     //   rp = x-pair (x, y_r+1)-(x+1, y_r+1), leaf = (x+1, y_r)
     auto plane_groups = [&](const V* P, auto&& emit) {
         const V* row = P + row0 * G::kPX + col;
-        V l = row[0], m = row[1], rr = row[2];
-        P2<V> pl = p2(l, m), pr = p2(m, rr), pl1;
-        V leaf_prev = rr;
+        SV l = (SV)row[0], m = (SV)row[1], rr = (SV)row[2];
+        P2<SV> pl = p2(l, m), pr = p2(m, rr), pl1;
+        SV leaf_prev = rr;
 #pragma unroll
         for (int j = 1; j < kQRowsPerThread + 2; ++j) {
             row += G::kPX;
-            l = row[0]; m = row[1];
-            const V rn = row[2];
-            const P2<V> pln = p2(l, m), prn = p2(m, rn);
+            l = (SV)row[0]; m = (SV)row[1];
+            const SV rn = (SV)row[2];
+            const P2<SV> pln = p2(l, m), prn = p2(m, rn);
             if (j >= 2) emit(j - 2, box2(pl1, pl), box2(pr, prn), prn, leaf_prev);
             pl1 = pl; pl = pln;
             pr = prn;
@@ -259,12 +271,13 @@ __global__ void __launch_bounds__(256, sizeof(FT) == 4 ? PMSZ_PREP_MINB : 2) k_p
     };
     __syncthreads();
     // prologue: D boxes of plane zb - 1, partial rings of plane zb
-    T2<V> lbprev[kQRowsPerThread], acc[kQRowsPerThread];
+    T2<SV> lbprev[kQRowsPerThread], acc[kQRowsPerThread];
+    const float thr32 = sizeof(FT) == 4 ? (float)a.thr : __double2float_ru(a.thr);
     wait_plane(0);
     wait_plane(1);
     wait_h(0);
-    plane_groups(S.plane[0], [&](int r, const T2<V>& lb, const T2<V>&, const P2<V>&, V) { lbprev[r] = lb; });
-    plane_groups(S.plane[1], [&](int r, const T2<V>& lb, const T2<V>& rb, const P2<V>&, V) {
+    plane_groups(S.plane[0], [&](int r, const T2<SV>& lb, const T2<SV>&, const P2<SV>&, SV) { lbprev[r] = lb; });
+    plane_groups(S.plane[1], [&](int r, const T2<SV>& lb, const T2<SV>& rb, const P2<SV>&, SV) {
         acc[r] = lbprev[r];
         merge2(acc[r], lb);
         merge2(acc[r], rb);
@@ -287,10 +300,11 @@ __global__ void __launch_bounds__(256, sizeof(FT) == 4 ? PMSZ_PREP_MINB : 2) k_p
             const uint32_t cz = c0 + (uint32_t)k * sz;
             bool want[kQRowsPerThread];
             plane_groups(S.plane[(k + 2) % G::kSlots],
-                         [&](int r, const T2<V>& lb, const T2<V>& rb, const P2<V>& rp, V leaf) {
+                         [&](int r, const T2<SV>& lb, const T2<SV>& rb, const P2<SV>& rp, SV leaf) {
                 merge2(acc[r], rb);   // U group: the ring of centre r is complete
                 const uint32_t c = cz + r * sy;
-                const bool robust = kScreen && robust2(acc[r], (V)a.thr, a.xi);
+                const bool robust = kScreen && (sizeof(FT) == 4 ? robust2(acc[r], thr32, a.xi)
+                                                                : robust2_narrowed(acc[r], thr32));
                 want[r] = live[r] && !robust;
                 if (live[r]) {
                     // validation (correction.py:52-60), hazard H6, g <- fhat

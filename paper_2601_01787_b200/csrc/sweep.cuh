@@ -189,17 +189,18 @@ __global__ void __launch_bounds__(256) k_defer(Dom d, const double* __restrict__
     for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (unsigned long long)gridDim.x * blockDim.x) {
         const int64_t c = w.work[i];
+        const uint8_t fc = w.code[c];
         int64_t x, y, z;
         coords(d, c, x, y, z);
         double nv[14];
-#pragma unroll
-        for (int r = 0; r < 14; ++r) {
-            const bool ok = in_dom(d, x + rank_dx(r), y + rank_dy(r), z + rank_dz(r));
-            nv[r] = ok ? __ldg(g + c + rank_off(d, r)) : nan64();
-        }
-        const Scan s = fold_scan(__ldg(g + c), nv);
+        // interior centres (all but the domain faces): plain pointer arithmetic
+        // and the balanced-tree fold; faces: bounds checks and the NaN fold
+        load_ring(d, g, c, x, y, z, nv, [](const double* q) { return __ldg(q); });
+        const double vc = __ldg(g + c);
+        const bool interior = x > 0 && x + 1 < d.nx && y > 0 && y + 1 < d.ny && z > 0 && z + 1 < d.nz;
+        const Scan s = interior ? tree_scan(vc, nv) : fold_scan(vc, nv);
         EmitRed emit{w};
-        rules<false>(d, w, s, nv, w.code[c], c, emit);
+        rules<false>(d, w, s, nv, fc, c, emit);
     }
 }
 

@@ -443,13 +443,16 @@ def test_ragged_shapes_match_oracle(dims, f32):
     assert 0 <= out.fragile <= dims[0] * dims[1] * dims[2]
 
 
-def test_robust_skipping_changes_nothing(monkeypatch):
+@pytest.mark.parametrize("f64_original", [False, True])
+def test_robust_skipping_changes_nothing(monkeypatch, f64_original):
     """PMSZ_ROBUST=0 / PMSZ_QSWEEP=0 (every centre evaluated by the shared-fold
     sweep) and the default (robust centres never evaluated, queue sweep) give
-    identical trajectories, fields and edit records."""
+    identical trajectories, fields and edit records -- for an f32 original and
+    for an f64 one that is not f32-exact (its robust screen runs on f32 images,
+    prep.cuh robust2_narrowed)."""
     from paper_2601_01787_b200.engine import DomainPlan, DomainSpec
     dims = (96, 80, 64)
-    f32 = gen.perlin_device(gen.NoiseSpec(dims, 4), f32=True)
+    f32 = gen.perlin_device(gen.NoiseSpec(dims, 4), f32=not f64_original)
     xi = gen.relative_to_absolute_device(f32, 1e-4)
     fh = gen.quantize_device(f32, xi)
     cfg = pm.CorrectionConfig(xi_abs=xi)
@@ -459,7 +462,8 @@ def test_robust_skipping_changes_nothing(monkeypatch):
             monkeypatch.delenv(k, raising=False)
         for k, v in env.items():
             monkeypatch.setenv(k, v)
-        plan = DomainPlan(DomainSpec.whole(dims), xi, cfg.tau, cfg.max_outer_iterations, f32_original=True)
+        plan = DomainPlan(DomainSpec.whole(dims), xi, cfg.tau, cfg.max_outer_iterations,
+                          f32_original=not f64_original)
         outs.append(pm.run_correction_device(f32, fh, dims, cfg, plan=plan))
         plan.close()
     a, b = outs
