@@ -493,7 +493,11 @@ void patch_host(double* g, const int64_t* ids, const double* vals, int64_t m) {
                                           std::max<int64_t>(1, (m + per - 1) / per));
     auto work = [&](int t) {
         const int64_t a = m * t / nt, b = m * (t + 1) / nt;
-        for (int64_t i = a; i < b; ++i) g[ids[i]] = vals[i];
+        constexpr int64_t kAhead = 32;   // read-for-ownership of the target lines, this far ahead
+        for (int64_t i = a; i < b; ++i) {
+            if (i + kAhead < b) __builtin_prefetch(g + ids[i + kAhead], 1, 0);
+            g[ids[i]] = vals[i];
+        }
     };
     if (nt == 1) { work(0); return; }
     std::vector<std::thread> th;
