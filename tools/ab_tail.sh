@@ -1,8 +1,7 @@
-# k_tail grid size A/B (PMSZ_TAIL_BLOCKS) with per-iteration device timestamps
 mkdir -p gpurun_out
-for nb in 0 32 8 1; do
-  echo "== nb $nb"
-  PMSZ_TAIL_BLOCKS=$nb PMSZ_TAIL_TRACE=1 python tools/one_run.py 512 2 2>&1 | tail -5
-  PMSZ_TAIL_BLOCKS=$nb python bench.py --no-e2e --no-cpu-baseline > gpurun_out/ab.json 2>/dev/null
-  python -c "import json; d=json.load(open('gpurun_out/ab.json')); k=d['roofline']['per_kernel']; print('nb $nb', round(d['ms_per_step'],3), 'tail', round(k['tail']['ms_total_per_step'],3), k['tail']['launches_per_step'], d['result']['edit_count'])"
+for cfg in "PMSZ_X=0" "PMSZ_DENSE_MIN=262144" "PMSZ_DENSE_MIN=524288" "PMSZ_TAIL_PER_SM=2" "PMSZ_TAIL_PER_SM=2 PMSZ_DENSE_MIN=524288" "PMSZ_TAIL1_MAX=1024" "PMSZ_TAIL1_MAX=256"; do
+  env $cfg timeout 300 python bench.py --no-cpu-baseline --no-e2e --no-dropin --steps 10 > gpurun_out/ab.json 2>&1
+  python -c "
+import json; d=json.load(open('gpurun_out/ab.json'))
+print('$cfg', round(d['ms_per_step'],3), {k:(round(v['ms_total_per_step'],3), v['launches_per_step']) for k,v in d['roofline']['per_kernel'].items()})"
 done
