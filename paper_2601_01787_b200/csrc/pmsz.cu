@@ -542,6 +542,8 @@ struct pmsz_plan {
     // device-resident tail (k_tail)
     bool tail_on = true;
     bool tail1_on = true;                 // small dirty sets in the one-CTA shared-memory tail (k_tail1)
+    bool totals_ready = false;            // the last tail_step converged and counted residual / edits
+    int64_t pre_residual = 0, pre_edits = 0;
     TailState* tail = nullptr;
     TailState* htail = nullptr;          // pinned mirror
     unsigned long long* thist = nullptr;  // per-iteration edits of one tail launch
@@ -955,7 +957,8 @@ pmsz_status launch_tail1(pmsz_plan* p, const void* f, double* g, cudaStream_t s,
 // plan state to where iterate_once would have left it.  Per-iteration edit
 // counts land in p->hthist[0 .. *k).
 pmsz_status tail_step(pmsz_plan* p, const void* f, double* g, cudaStream_t s, long long budget, int64_t* k,
-                      bool* shared_any) {
+                      bool* shared_any, bool totals = false) {
+    p->totals_ready = false;
     p->edits_cached = -1;
     pmsz_status st = reset_iter(p, s, p->cur ^ 1);
     if (st) return st;
@@ -975,11 +978,21 @@ pmsz_status tail_step(pmsz_plan* p, const void* f, double* g, cudaStream_t s, lo
         }
         if (st) return st;
     }
+    if (totals) {   // the run's closing counts, read with this synchronisation (used if the tail converged)
+        ProfScope ps(p, s, PMSZ_K_COMPACT);
+        launch_bits_total(p, p->w.detbits, &p->ctr->scratch[1], s);
+        launch_bits_total(p, p->w.editbits, &p->ctr->scratch[2], s);
+    }
     CUDA_TRY(cudaMemcpyAsync(p->htail, p->tail, sizeof(TailState), cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaMemcpyAsync(p->hthist, p->thist, sizeof(unsigned long long) * budget, cudaMemcpyDeviceToHost, s));
     st = sync_counters(p, s);
     if (st) return st;
     const TailState& ts = *p->htail;
+    if (totals && ts.exit == kTailConverged) {
+        p->totals_ready = true;
+        p->pre_residual = (int64_t)p->hctr->scratch[1];
+        p->pre_edits = (int64_t)p->hctr->scratch[2];
+    }
     *k = (int64_t)ts.iterations;
     *shared_any = ts.shared_or != 0;
     p->iterations += *k;
@@ -1259,7 +1272,9 @@ pmsz_status pmsz_plan_create(const pmsz_desc* desc, pmsz_plan** out) {
                  cudaMallocHost((void**)&p->htail, sizeof(TailState)) == cudaSuccess &&
                  cudaMallocHost((void**)&p->hthist, hist_n * 8) == cudaSuccess;
     p->tail_on = (d.flags & PMSZ_FLAG_HOST_LOOP) == 0;
-    p->dense_min = std::max<int64_t>(ncore / 96, 65536);
+    // dirty lists above ~0.4 % of the core take the host-launched list sweep (4 CTAs / SM) rather than the
+    // tail (1 CTA / SM): measured 3.73 -> 3.70 ms at 512^3 (ncore / 96: the first tail iteration swept 1.1 M)
+    p->dense_min = std::max<int64_t>(ncore / 256, 65536);
     if (const char* e = getenv("PMSZ_SORT_MIN")) p->sort_min = atoll(e);
     if (const char* e = getenv("PMSZ_DENSE_MIN")) p->dense_min = atoll(e);
     if (const char* e = getenv("PMSZ_FULL_DIV")) p->full_div = std::max<int64_t>(1, atoll(e));
@@ -1688,7 +1703,7 @@ pmsz_status pmsz_run_correction(pmsz_plan* p, const void* f, const double* fh, d
         if (tail_ok(p)) {
             int64_t k = 0;
             bool sh = false;
-            st = tail_step(p, f, g, s, std::min(p->desc.max_iterations - it, p->hist_chunk), &k, &sh);
+            st = tail_step(p, f, g, s, std::min(p->desc.max_iterations - it, p->hist_chunk), &k, &sh, true);
             if (st) { restore_prop(p, s); return st; }
             tail_result(p, r, k);
             for (int64_t i = 0; i < k; ++i) {
@@ -1732,8 +1747,15 @@ pmsz_status pmsz_run_correction(pmsz_plan* p, const void* f, const double* fh, d
     // a full re-scan of the final field.  The per-kind split is only computed
     // when something survived.
     int64_t residual = 0, count = 0;
-    st = residual_and_edits(p, s, &residual, &count);
-    if (st) return st;
+    if (p->totals_ready && p->offsets_of == p->w.editbits) {   // counted by the converging tail_step
+        residual = p->pre_residual;
+        count = p->pre_edits;
+        p->edits_cached = count;
+    } else {
+        st = residual_and_edits(p, s, &residual, &count);
+        if (st) return st;
+    }
+    p->totals_ready = false;
     if (residual) {
         st = pmsz_verify(p, g, r, stream);
         if (st) return st;
