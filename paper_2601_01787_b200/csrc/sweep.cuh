@@ -324,11 +324,8 @@ struct TargetOps {
     unsigned int cnt;
 };
 template <typename FT>
-__device__ __forceinline__ TargetOps load_target(const FT* __restrict__ f, const double* __restrict__ g,
-                                                 const Work& w, int64_t t) {
-    // edits so far: 0 unless the ever-edited bit is set, then 1 + the stored
-    // extra count (a first edit writes nothing to `counts`); the run's first
-    // apply knows every count is 0 and reads neither array
+__device__ __forceinline__ TargetOps load_target_nokey(const FT* __restrict__ f, const double* __restrict__ g,
+                                                       const Work& w, int64_t t) {
     unsigned int cnt = 0;
     if (!w.first_apply) {
         const uint32_t ew = __ldcg(w.editbits + (t >> 5));
@@ -336,7 +333,15 @@ __device__ __forceinline__ TargetOps load_target(const FT* __restrict__ f, const
                                               : (unsigned int)__ldcg((const uint16_t*)w.counts + t);
         cnt = ((ew >> (t & 31)) & 1u) ? extra + 1u : 0u;
     }
-    return TargetOps{__ldcg(w.prop + t), __ldcg(g + t), (double)f[t], cnt};
+    return TargetOps{kNoProposal, __ldcg(g + t), (double)f[t], cnt};
+}
+
+template <typename FT>
+__device__ __forceinline__ TargetOps load_target(const FT* __restrict__ f, const double* __restrict__ g,
+                                                 const Work& w, int64_t t) {
+    TargetOps op = load_target_nokey(f, g, w, t);
+    op.key = __ldcg(w.prop + t);
+    return op;
 }
 
 template <typename FT>

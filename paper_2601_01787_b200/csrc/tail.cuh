@@ -272,6 +272,7 @@ namespace pmsz {
 // the next dirty set) and hands back to the host.
 constexpr int kT1Threads = 1024;
 constexpr int kT1Dirty = 4096;      // dirty-list capacity (ping-pong)
+// (shared memory: 32 KB dirty lists + 64 KB keys + 3 x 32 KB sets = 192 KB of the 227 KB)
 constexpr int kT1Set = 8192;        // hash sets (targets / next dirty); power of two
 constexpr int kT1SetBits = 13;
 constexpr uint32_t kT1Empty = 0xffffffffu;
@@ -281,6 +282,7 @@ constexpr int kT1Handover = 512;
 
 struct T1Smem {
     uint32_t dirty[2][kT1Dirty];
+    unsigned long long tkey[kT1Set];   // min-merged proposal key of each target slot (kNoProposal when free)
     uint32_t tset[kT1Set];
     uint32_t dset[kT1Set];
     uint32_t edits[kT1Set];
@@ -289,32 +291,41 @@ struct T1Smem {
 };
 constexpr size_t kT1SmemBytes = sizeof(T1Smem);
 
-// 1 = inserted, 0 = present, 2 = no free slot within the probe limit
-__device__ __forceinline__ int t1_insert(uint32_t* set, uint32_t u) {
+// 1 = inserted, 0 = present, 2 = no free slot within the probe limit; *at = the slot
+__device__ __forceinline__ int t1_insert(uint32_t* set, uint32_t u, uint32_t* at = nullptr) {
     const uint32_t h = (u * 2654435761u) >> (32 - kT1SetBits);
 #pragma unroll 1
     for (int k = 0; k < 64; ++k) {
         const uint32_t slot = (h + (uint32_t)k) & (uint32_t)(kT1Set - 1);
         const uint32_t old = atomicCAS(set + slot, kT1Empty, u);
-        if (old == kT1Empty) return 1;
-        if (old == u) return 0;
+        if (old == kT1Empty || old == u) {
+            if (at) *at = slot;
+            return old == kT1Empty ? 1 : 0;
+        }
     }
     return 2;
 }
 
+// Proposals are min-merged in shared memory (the target's slot key; exactly
+// np.minimum.at, like the RED.MIN of the other forms); global prop is left
+// untouched, so no fence is needed before the apply.  A full set falls back
+// to prop + touched + the global work list (a target is either in the set
+// for all its proposals or for none: slots never free during the sweep).
 struct EmitT1 {
     const Work& w;
     T1Smem& S;
-    bool issued = false;
+    bool issued = false;   // this thread issued global RED.MINs (overflow)
     __device__ __forceinline__ void operator()(int64_t t, double val) {
+        uint32_t slot;
+        if (t1_insert(S.tset, (uint32_t)t, &slot) != 2) {
+            atomicMin(S.tkey + slot, okey(val));
+            return;
+        }
         atomicMin(w.prop + t, okey(val));
         issued = true;
-        if (t1_insert(S.tset, (uint32_t)t) == 2) {
-            // set full: the global target list, deduplicated by the touched bit
-            S.ovf_tgt = 1;
-            const uint32_t bit = 1u << (t & 31);
-            if (!(atomicOr(w.touched + (t >> 5), bit) & bit)) w.work[agg_append(&w.ctr->nwork)] = (uint32_t)t;
-        }
+        S.ovf_tgt = 1;
+        const uint32_t bit = 1u << (t & 31);
+        if (!(atomicOr(w.touched + (t >> 5), bit) & bit)) w.work[agg_append(&w.ctr->nwork)] = (uint32_t)t;
     }
 };
 
@@ -324,7 +335,7 @@ struct EmitT1 {
 template <typename FT>
 __device__ __forceinline__ void t1_apply_mark(const Dom& d, const FT* __restrict__ f, double* __restrict__ g,
                                               const Work& w, T1Smem& S, int b, unsigned dcap, int64_t t,
-                                              ApplyAcc& acc) {
+                                              ApplyAcc& acc, bool smem_key, unsigned long long key) {
     int64_t x, y, z;
     coords(d, t, x, y, z);
     uint32_t fw[15];
@@ -335,9 +346,15 @@ __device__ __forceinline__ void t1_apply_mark(const Dom& d, const FT* __restrict
         const int64_t u = px + py * d.sy + pz * d.sz;
         fw[r + 1] = !in_core(d, px, py, pz) ? 0u : (w.frag ? __ldg(w.frag + (u >> 5)) : ~0u);
     }
-    const TargetOps op = load_target(f, g, w, t);
+    TargetOps op;
+    if (smem_key) {   // the proposal is in shared memory; global prop stays all-ones
+        op = load_target_nokey(f, g, w, t);
+        op.key = key;
+    } else {
+        op = load_target(f, g, w, t);
+        w.prop[t] = kNoProposal;
+    }
     const double p = okey_inv(op.key);
-    w.prop[t] = kNoProposal;
     const double gt = op.gt;
     const double lower = op.fv - d.lxi;                  // BoundsField.lower (correction.py:122)
     const double m = (p < gt) ? p : gt;                  // np.minimum(g, prop)
@@ -366,6 +383,7 @@ __device__ __forceinline__ void t1_apply_mark(const Dom& d, const FT* __restrict
         if (!((fw[r + 1] >> (u & 31)) & 1u)) continue;   // outside the core, or robust (never evaluated)
         const int ins = t1_insert(S.dset, (uint32_t)u);
         if (ins == 1) {
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(w.code + u));   // read by the next sweep
             const unsigned q = atomicAdd(&S.nd[b ^ 1], 1u);
             if (q < dcap) S.dirty[b ^ 1][q] = (uint32_t)u;
             else S.ovf_mark = 1;
@@ -407,7 +425,10 @@ __global__ void __launch_bounds__(kT1Threads, 1) k_tail1(Dom d, const FT* __rest
         S.dirty[0][i] = u;
         atomicAnd(w.actbits + (u >> 5), ~(1u << (u & 31)));
     }
-    for (int i = tid; i < kT1Set; i += kT1Threads) S.tset[i] = kT1Empty;
+    for (int i = tid; i < kT1Set; i += kT1Threads) {
+        S.tset[i] = kT1Empty;
+        S.tkey[i] = kNoProposal;
+    }
     if (tid == 0) {
         S.nd[0] = n0;
         S.nd[1] = 0;
@@ -459,15 +480,17 @@ __global__ void __launch_bounds__(kT1Threads, 1) k_tail1(Dom d, const FT* __rest
         for (int slot = tid; slot < kT1Set; slot += kT1Threads) {
             const uint32_t t = S.tset[slot];
             if (t == kT1Empty) continue;
+            const unsigned long long key = S.tkey[slot];
             S.tset[slot] = kT1Empty;   // empty again for the next S
-            t1_apply_mark(d, f, g, w, S, b, dcap, (int64_t)t, acc);
+            S.tkey[slot] = kNoProposal;
+            t1_apply_mark(d, f, g, w, S, b, dcap, (int64_t)t, acc, true, key);
         }
         if (S.ovf_tgt) {
             const unsigned long long n = __ldcg(&c->nwork);
             for (unsigned long long i = tid; i < n; i += kT1Threads) {
                 const int64_t t = __ldcg(w.work + i);
                 const uint32_t bit = 1u << (t & 31);
-                if (atomicAnd(w.touched + (t >> 5), ~bit) & bit) t1_apply_mark(d, f, g, w, S, b, dcap, t, acc);
+                if (atomicAnd(w.touched + (t >> 5), ~bit) & bit) t1_apply_mark(d, f, g, w, S, b, dcap, t, acc, false, 0ull);
             }
         }
         {
