@@ -32,7 +32,6 @@
 #include "gather.cuh"
 #include "qsweep.cuh"
 #include "prep.cuh"
-#include "rules1.cuh"
 #include "segment.cuh"
 
 using namespace pmsz;
@@ -564,8 +563,6 @@ struct pmsz_plan {
     bool fuse_on = true;                  // K0 also runs the first detection sweep (prep.cuh)
     bool qmask_ok = false;                // dense masked iterations can use the TMA queue sweep (kMaskedQ)
     bool k0_detected = false;             // detbits / ndetect of the first iteration come from K0
-    const double* k0_src = nullptr;       // K0's fhat when g is a separate buffer (rules1.cuh may run iteration 1)
-    bool rules1_on = true;                // iteration 1 as the tiled rules + apply pass (PMSZ_RULES1)
     uint32_t* frag = nullptr;             // fragile-centre bitmap written by K0
     int64_t hist_chunk = 0;               // thist / hthist entries: iterations per tail launch
     std::vector<int64_t> hist_all;        // edits_per_iteration of the last pmsz_run_correction
@@ -822,21 +819,7 @@ pmsz_status iterate_once(pmsz_plan* p, const void* f, double* g, cudaStream_t s)
             CUDA_TRY(cudaMemsetAsync(p->w.actbits, 0, p->nwords * 4, s));
         }
     }
-    // Iteration 1 after K0 with g separate from fhat: rules + apply as one
-    // tiled pass over the detection bits (rules1.cuh) instead of compaction +
-    // k_defer + compaction + k_apply_list
-    bool fused1 = false;
-    if (predetected && nonempty && p->rules1_on && p->k0_src && !p->w.edited_mask) {
-        ProfScope ps(p, s, PMSZ_K_APPLY);
-        uint32_t* ie = p->w.incremental ? p->w.iteredit : nullptr;
-        fused1 = p->f32 ? launch_rules1<float>(d, p->k0_src, g, (const float*)f, p->w.code, p->w.detbits, p->w.editbits,
-                                               ie, p->ctr, s)
-                        : launch_rules1<double>(d, p->k0_src, g, (const double*)f, p->w.code, p->w.detbits,
-                                                p->w.editbits, ie, p->ctr, s);
-        if (fused1) LAUNCHED();
-    }
-    p->k0_src = nullptr;
-    if (mode != kList && nonempty && !gather && !fused1) {
+    if (mode != kList && nonempty && !gather) {
         // centres with a detection (bitmap set by the tiled sweep) -> list -> rules
         {
             ProfScope ps(p, s, PMSZ_K_COMPACT);
@@ -861,11 +844,9 @@ pmsz_status iterate_once(pmsz_plan* p, const void* f, double* g, cudaStream_t s)
         apply_bound = std::min<int64_t>(p->n, 15 * m + 32);
     }
     p->last_mode = mode;
-    if (!fused1) {
-        st = p->f32 ? launch_apply<float>(p, f, g, s, nxt, mode != kList, apply_bound)
-                    : launch_apply<double>(p, f, g, s, nxt, mode != kList, apply_bound);
-        if (st) return st;
-    }
+    st = p->f32 ? launch_apply<float>(p, f, g, s, nxt, mode != kList, apply_bound)
+                : launch_apply<double>(p, f, g, s, nxt, mode != kList, apply_bound);
+    if (st) return st;
     CUDA_TRY(cudaGetLastError());
     st = sync_counters(p, s);
     if (st) return st;
@@ -1099,7 +1080,6 @@ pmsz_status prep(pmsz_plan* p, const void* f, const double* fh, double* g, cudaS
         if (nsl > 0) CUDA_TRY(cudaStreamWaitEvent(s, p->stage_ev[nsl], 0));   // every slab is in
         p->stage_pending = false;
         p->k0_detected = queued && det != nullptr;
-        p->k0_src = g != fh ? fh : nullptr;
         if (!queued) {
             if (p->f32)
                 launch_prep<float>(p->dom, (const float*)f, fh, g, p->w.code, p->frag_out(), p->ctr, s);
@@ -1305,7 +1285,6 @@ pmsz_status pmsz_plan_create(const pmsz_desc* desc, pmsz_plan** out) {
     if (const char* e = getenv("PMSZ_QPREP")) p->qprep_on = atoi(e) != 0;
     if (const char* e = getenv("PMSZ_FUSE")) p->fuse_on = atoi(e) != 0;
     if (const char* e = getenv("PMSZ_TAIL1")) p->tail1_on = atoi(e) != 0;
-    if (const char* e = getenv("PMSZ_RULES1")) p->rules1_on = atoi(e) != 0;
     // measured: the dense masked queue sweep (0.45 ms) plus the dilation (0.08 ms)
     // do not beat the plain queue sweep (0.49 ms) at 512^3, so it is opt-in
     p->qmask_ok = p->qsweep_on && p->gather_on && qsweep_masked_ok(p->dom) && getenv("PMSZ_QMASK") &&
