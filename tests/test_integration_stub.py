@@ -94,3 +94,43 @@ def test_host_entry_truncated_record_and_corrected_field(golden):
             import hashlib
             assert hashlib.sha256(g.tobytes()).hexdigest() == run["corrected_sha256"]
     plan.close()
+
+
+@pytest.mark.parametrize("dims", [(256, 128, 129), (192, 160, 144)])
+def test_host_entry_slab_pipeline_matches_device(dims):
+    """pmsz_run_correction_host above the slab threshold (>= 4 M voxels): the
+    input arrives in 16 z-slabs (nz not a multiple of 16), K0 runs per slab,
+    the corrected field streams back concurrently and is patched with the
+    edit record -- all equal to the device-resident run."""
+    import ctypes
+    import torch
+    import paper_2601_01787_b200 as pm
+    from paper_2601_01787_b200 import _native as N
+    from paper_2601_01787_b200 import inputs as gen
+    from paper_2601_01787_b200.engine import DomainPlan, DomainSpec
+    f32 = gen.perlin_device(gen.NoiseSpec(dims, 3), f32=True)
+    xi = gen.relative_to_absolute_device(f32, 1e-4)
+    fh = gen.quantize_device(f32, xi)
+    cfg = pm.CorrectionConfig(xi_abs=xi)
+    ref = pm.run_correction_device(f32, fh, dims, cfg)
+    n = f32.numel()
+    fh_h = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    f_h = torch.empty(n, dtype=torch.float32, pin_memory=True)
+    fh_h.copy_(fh)
+    f_h.copy_(f32)
+    g_h = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    ids = torch.zeros(n // 4, dtype=torch.int64, pin_memory=True)
+    vals = torch.zeros(n // 4, dtype=torch.float64, pin_memory=True)
+    plan = DomainPlan(DomainSpec.whole(dims), cfg.xi_abs, cfg.tau, cfg.max_outer_iterations, f32_original=True)
+    hist = (ctypes.c_int64 * 256)()
+    for _ in range(2):   # twice: the plan's staging is reused
+        res = N.PmszResult()
+        st = N.lib().pmsz_run_correction_host(plan.handle, N.ptr(f_h), N.ptr(fh_h), N.ptr(g_h), N.ptr(ids),
+                                              N.ptr(vals), ids.numel(), hist, 256, ctypes.byref(res),
+                                              N.stream_handle(torch.cuda.current_stream()))
+        assert st == 0
+        m = int(res.edit_count)
+        assert m == ref.edit_ids.numel() and list(hist[:res.iterations]) == list(ref.edits_per_iteration)
+        assert torch.equal(g_h, ref.corrected.cpu())
+        assert torch.equal(ids[:m], ref.edit_ids.cpu()) and torch.equal(vals[:m], ref.edit_values.cpu())
+    plan.close()
