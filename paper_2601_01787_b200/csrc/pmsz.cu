@@ -576,6 +576,7 @@ struct pmsz_plan {
     cudaStream_t copy_stream = nullptr;   // host-to-device slabs of pmsz_run_correction_host
     std::vector<cudaEvent_t> stage_ev;    // [0]: staging free; [1 + c]: slab c landed
     std::vector<int64_t> stage_z;         // slab boundaries in z (nslabs + 1)
+    std::vector<cudaEvent_t> rec_ev;      // edit-record chunks back on the host
     bool stage_pending = false;           // the next K0 waits for the slabs, one launch per slab
     cudaStream_t d2h_stream = nullptr;    // corrected-field slabs back to the host (pmsz_run_correction_host)
     cudaEvent_t d2h_done = nullptr;
@@ -1326,6 +1327,7 @@ void pmsz_plan_destroy(pmsz_plan* p) {
     if (p->hthist) cudaFreeHost(p->hthist);
     cudaFree(p->stage_f); cudaFree(p->stage_g); cudaFree(p->stage_ids); cudaFree(p->stage_vals);
     for (cudaEvent_t e : p->stage_ev) cudaEventDestroy(e);
+    for (cudaEvent_t e : p->rec_ev) cudaEventDestroy(e);
     cudaFree(p->dsig);
     if (p->d2h_stream) cudaStreamDestroy(p->d2h_stream);
     if (p->d2h_done) cudaEventDestroy(p->d2h_done);
@@ -1891,11 +1893,26 @@ pmsz_status pmsz_run_correction_host(pmsz_plan* p, const void* f_host, const dou
                 hid = p->hrec_ids;
                 hval = p->hrec_vals;
             }
-            CUDA_TRY(cudaMemcpyAsync(hid, p->stage_ids, m * 8, cudaMemcpyDeviceToHost, s));
-            CUDA_TRY(cudaMemcpyAsync(hval, p->stage_vals, m * 8, cudaMemcpyDeviceToHost, s));
-            CUDA_TRY(cudaStreamSynchronize(s));
+            // the record comes back in a few chunks; the host patches chunk c of
+            // the field while chunk c + 1 is still on the link
+            const int nch = g_host ? (int)std::min<int64_t>(8, std::max<int64_t>(1, m >> 18)) : 1;
+            while ((int)p->rec_ev.size() < nch) {
+                cudaEvent_t e;
+                CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+                p->rec_ev.push_back(e);
+            }
+            for (int c = 0; c < nch; ++c) {
+                const int64_t a = m * c / nch, b = m * (c + 1) / nch;
+                CUDA_TRY(cudaMemcpyAsync(hid + a, p->stage_ids + a, (b - a) * 8, cudaMemcpyDeviceToHost, s));
+                CUDA_TRY(cudaMemcpyAsync(hval + a, p->stage_vals + a, (b - a) * 8, cudaMemcpyDeviceToHost, s));
+                CUDA_TRY(cudaEventRecord(p->rec_ev[c], s));
+            }
             if (etrace) t3 = now();
-            if (g_host) patch_host(g_host, hid, hval, m);
+            for (int c = 0; c < nch; ++c) {
+                CUDA_TRY(cudaEventSynchronize(p->rec_ev[c]));
+                const int64_t a = m * c / nch, b = m * (c + 1) / nch;
+                if (g_host) patch_host(g_host, hid + a, hval + a, b - a);
+            }
             if (!direct && ids_host && vals_host && edits_cap > 0) {
                 const int64_t k = std::min(edits_cap, count);
                 memcpy(ids_host, hid, k * 8);
@@ -1905,7 +1922,7 @@ pmsz_status pmsz_run_correction_host(pmsz_plan* p, const void* f_host, const dou
     }
     CUDA_TRY(cudaStreamSynchronize(s));
     if (etrace)
-        fprintf(stderr, "e2e: run %.2f ms, d2h field wait %.2f, record %.2f, patch + copy-out %.2f (total %.2f)\n", t1 - t0,
+        fprintf(stderr, "e2e: run %.2f ms, d2h field wait %.2f, export %.2f, record + patch + copy-out %.2f (total %.2f)\n", t1 - t0,
                 t2 - t1, t3 - t2, now() - t3, now() - t0);
     return st;
 }
