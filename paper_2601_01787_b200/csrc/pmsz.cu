@@ -485,7 +485,10 @@ __global__ void __launch_bounds__(PMSZ_MAX_RANKS) k_signal(SigArgs a) {
 // g_host[ids[i]] = vals[i] (the edit record onto the streamed-back fhat), on
 // a few host threads: ids are ascending, so each thread writes one contiguous
 // range of the field.
-void patch_host(double* g, const int64_t* ids, const double* vals, int64_t m) {
+// The record arrives in nch chunks (event ev[c] = chunk c landed); thread t
+// owns one contiguous share of the record and patches it chunk by chunk as
+// the chunks land, so the patch overlaps the transfer.
+void patch_host(double* g, const int64_t* ids, const double* vals, int64_t m, cudaEvent_t* ev, int nch) {
     // latency-bound (one cache line per write, ~30 values apart): every host
     // thread, at least 64 k writes each
     const int64_t per = 1 << 16;
@@ -494,9 +497,15 @@ void patch_host(double* g, const int64_t* ids, const double* vals, int64_t m) {
     auto work = [&](int t) {
         const int64_t a = m * t / nt, b = m * (t + 1) / nt;
         constexpr int64_t kAhead = 32;   // read-for-ownership of the target lines, this far ahead
-        for (int64_t i = a; i < b; ++i) {
-            if (i + kAhead < b) __builtin_prefetch(g + ids[i + kAhead], 1, 0);
-            g[ids[i]] = vals[i];
+        int c = 0;
+        for (int64_t i = a; i < b;) {
+            while (m * (c + 1) / nch <= i) ++c;                 // chunk holding record entry i
+            cudaEventSynchronize(ev[c]);
+            const int64_t e = std::min<int64_t>(b, m * (c + 1) / nch);
+            for (; i < e; ++i) {
+                if (i + kAhead < e) __builtin_prefetch(g + ids[i + kAhead], 1, 0);
+                g[ids[i]] = vals[i];
+            }
         }
     };
     if (nt == 1) { work(0); return; }
@@ -1908,10 +1917,10 @@ pmsz_status pmsz_run_correction_host(pmsz_plan* p, const void* f_host, const dou
                 CUDA_TRY(cudaEventRecord(p->rec_ev[c], s));
             }
             if (etrace) t3 = now();
-            for (int c = 0; c < nch; ++c) {
-                CUDA_TRY(cudaEventSynchronize(p->rec_ev[c]));
-                const int64_t a = m * c / nch, b = m * (c + 1) / nch;
-                if (g_host) patch_host(g_host, hid + a, hval + a, b - a);
+            if (g_host) {
+                patch_host(g_host, hid, hval, m, p->rec_ev.data(), nch);
+            } else {
+                CUDA_TRY(cudaEventSynchronize(p->rec_ev[nch - 1]));
             }
             if (!direct && ids_host && vals_host && edits_cap > 0) {
                 const int64_t k = std::min(edits_cap, count);
