@@ -421,13 +421,17 @@ def dropin_api(args, f32, fh, dims, cfg, dev_res) -> dict:
         r = pm.run_correction(f, fhat, cfg)
     dt = (time.perf_counter() - t0) / steps
     ok = (list(r.edits_per_iteration) == list(dev_res.edits_per_iteration) and r.edits.count == dev_res.edit_ids.numel()
-          and _sha(r.corrected.values) == _sha(dev_res.corrected))
+          and _sha(r.corrected.values) == _sha(dev_res.corrected) and _sha(r.edits.ids) == _sha(dev_res.edit_ids)
+          and _sha(r.edits.values) == _sha(dev_res.edit_values))
     if not ok:
         raise SystemExit("drop-in run_correction differs from the device-resident run")
     n = dims[0] * dims[1] * dims[2]
     return {"ms_per_call": dt * 1e3, "voxels_per_s": n / dt, "calls": steps, "matches_device": ok,
             "path": "paper_2601_01787_b200.run_correction(ScalarField f64 x2, CorrectionConfig) -> CorrectionResult "
-                    "(pageable host f64 in, corrected ScalarField + EditSet out; f32-exact original detected on device)"}
+                    "(pageable host f64 in, corrected ScalarField + EditSet out): pmsz_run_correction_host staging "
+                    "the numpy arrays through a pinned ring, f64 original narrowed to f32 while staged, field "
+                    "filled from fhat on the host and patched with the edit record",
+            "ids_sha256": _sha(r.edits.ids), "values_sha256": _sha(r.edits.values)}
 
 
 def e2e_host(args, plan, f32, fh, dims, nvox, dev_res) -> dict:

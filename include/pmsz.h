@@ -36,7 +36,9 @@ typedef enum {
     PMSZ_ERR_MONOTONE = 3,     /* AssertionError "edit raised a value" (correction.py:240-241) */
     PMSZ_ERR_CONVERGENCE = 4,  /* ConvergenceError (correction.py:48-49,417-429) */
     PMSZ_ERR_CUDA = 5,         /* CUDA runtime failure */
-    PMSZ_ERR_NONFINITE = 6     /* ValueError "field values must all be finite" (grid.py:62-63) */
+    PMSZ_ERR_NONFINITE = 6,    /* ValueError "field values must all be finite" (grid.py:62-63) */
+    PMSZ_ERR_INEXACT = 7       /* PMSZ_FLAG_HOST_F64: the f64 original did not narrow exactly to
+                                  float32 -- no error in the reference; rerun with an f64 plan */
 } pmsz_status;
 
 /* ConvergenceError sub-kinds, reported in pmsz_result.convergence_kind. */
@@ -56,9 +58,14 @@ enum {
                                     and synchronised from the host (A/B and tests) */
     PMSZ_FLAG_NO_ROBUST = 16,    /* evaluate every centre: required when g may leave
                                     [f - xi, f + xi] (local_converge on arbitrary inputs) */
-    PMSZ_FLAG_LOWER = 32         /* pmsz_iterate / pmsz_block_round receive the f64 lower
+    PMSZ_FLAG_LOWER = 32,        /* pmsz_iterate / pmsz_block_round receive the f64 lower
                                     bound L itself in place of f (local_converge's lower_ext,
                                     parallel.py:150-172): the apply clamps to L, not f - xi */
+    PMSZ_FLAG_HOST_F64 = 64      /* with PMSZ_FLAG_F32_ORIGINAL: pmsz_run_correction_host gets an
+                                    f64 host original and narrows it while staging; returns
+                                    PMSZ_ERR_INEXACT (before any iteration) when a value does
+                                    not round-trip (the reference's ScalarField is always f64,
+                                    grid.py:57; fields read from f32 files narrow exactly) */
 };
 
 /* Distortion kinds, in the reference declaration order (correction.py:133-139). */
@@ -167,11 +174,23 @@ pmsz_status pmsz_run_correction(pmsz_plan* plan, const void* f_dev, const double
  * allocated on the first call and reused.  The host-to-device copy runs in
  * z-slabs on a second stream and K0 starts on each slab as soon as it (and
  * its upper neighbour plane) has landed.
+ * Any buffer may be pageable (plain malloc / numpy memory): pageable inputs
+ * are staged through a pinned ring by host threads while the previous chunk
+ * is on the link; a pageable g_host is filled from fhat_host on the host and
+ * patched with the edit record (no device-to-host copy of the field).  With
+ * g_host given and no (pinned, large enough) ids/vals buffers the whole
+ * record stays in the plan's pinned buffers for pmsz_edits_host.
  */
 pmsz_status pmsz_run_correction_host(pmsz_plan* plan, const void* f_host, const double* fhat_host,
                                      double* g_host, int64_t* ids_host, double* vals_host,
                                      int64_t edits_cap, int64_t* history_host, int64_t history_cap,
                                      pmsz_result* result, void* stream);
+
+/* The edit record of the last pmsz_run_correction_host call when the plan
+ * kept it (see there): the first min(cap, count) entries into host buffers;
+ * *count_out = the full count.  PMSZ_ERR_INVALID when no record is held. */
+pmsz_status pmsz_edits_host(pmsz_plan* plan, int64_t* ids_host, double* vals_host, int64_t cap,
+                            int64_t* count_out);
 
 /* Ascending ids where g != fhat and the corrected values (EditSet.diff). */
 pmsz_status pmsz_edits_export(pmsz_plan* plan, const double* g_dev, int64_t* ids_dev,

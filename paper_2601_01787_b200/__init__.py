@@ -7,7 +7,7 @@ hand-written sm_100a kernels behind the C ABI of include/pmsz.h.
 
 from .grid import (RANK_OFFSETS, STENCIL, ScalarField, linear_index, neighbors, precedes,
                    vertex_coords)
-from .engine import BoundViolationError, ConvergenceError
+from .engine import BoundViolationError, ConvergenceError, empty_host_cache
 from .topology import (DistortionReport, ExtremaSet, NeighborScan, SegmentationLabels, compare_plmss,
                        compute_segmentation, field_scan, find_extrema, scan_neighbors)
 from .correction import (BoundsField, CorrectionConfig, CorrectionResult, DeviceCorrection, EditSet,

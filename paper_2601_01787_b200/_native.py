@@ -22,6 +22,7 @@ PMSZ_ERR_MONOTONE = 3
 PMSZ_ERR_CONVERGENCE = 4
 PMSZ_ERR_CUDA = 5
 PMSZ_ERR_NONFINITE = 6
+PMSZ_ERR_INEXACT = 7
 
 PMSZ_CONV_NONE = 0
 PMSZ_CONV_CAP = 1
@@ -39,6 +40,7 @@ FLAG_F32_ORIGINAL = 4
 FLAG_HOST_LOOP = 8
 FLAG_NO_ROBUST = 16
 FLAG_LOWER = 32
+FLAG_HOST_F64 = 64
 
 i64 = ctypes.c_int64
 i32 = ctypes.c_int32
@@ -100,6 +102,7 @@ SIGNATURES = {
     "pmsz_run_correction_host": (i32, [vp, vp, vp, vp, vp, vp, i64, i64p, i64,
                                        ctypes.POINTER(PmszResult), vp]),
     "pmsz_edits_export": (i32, [vp, vp, vp, vp, i64, i64p, vp]),
+    "pmsz_edits_host": (i32, [vp, vp, vp, i64, i64p]),
     "pmsz_prepare": (i32, [vp, vp, vp, vp, ctypes.POINTER(PmszResult), vp]),
     "pmsz_iterate": (i32, [vp, vp, vp, vp, ctypes.POINTER(PmszResult), vp]),
     "pmsz_block_round": (i32, [vp, vp, vp, i32, i64p, ctypes.POINTER(PmszResult), vp]),

@@ -27,7 +27,7 @@ import torch
 
 from . import _native as N
 from .engine import (BoundViolationError, ConvergenceError, DomainPlan, DomainSpec,
-                     as_device_f64, narrow_if_exact, raise_for, to_host_f64)
+                     HOST_FIELDS, as_device_f64, narrow_if_exact, raise_for, to_host_f64)
 from .grid import ScalarField
 from .topology import DistortionReport
 
@@ -137,6 +137,22 @@ class EditSet:
         object.__setattr__(self, "values", values)
         object.__setattr__(self, "vertex_count", int(self.vertex_count))
 
+    @classmethod
+    def _owned(cls, ids: np.ndarray, values: np.ndarray, vertex_count: int) -> "EditSet":
+        """The record of a device run, in fresh arrays this package just
+        produced: the export walks the edited bitmap in id order (strictly
+        ascending, in range) and every value is a finite f64 the kernels
+        computed, so the O(count) validation scans are skipped."""
+        obj = object.__new__(cls)
+        ids = np.asarray(ids, dtype=np.int64).reshape(-1)
+        values = np.asarray(values, dtype=np.float64).reshape(-1)
+        ids.setflags(write=False)
+        values.setflags(write=False)
+        object.__setattr__(obj, "ids", ids)
+        object.__setattr__(obj, "values", values)
+        object.__setattr__(obj, "vertex_count", int(vertex_count))
+        return obj
+
     @property
     def count(self) -> int:
         return int(self.ids.size)
@@ -191,16 +207,17 @@ _PLAN_CACHE: dict = {}
 
 
 def _plan_for(dims, config: CorrectionConfig, *, incremental: bool, extrema_only: bool,
-              f32_original: bool) -> DomainPlan:
+              f32_original: bool, host_f64: bool = False) -> DomainPlan:
     key = (tuple(dims), config.xi_abs, config.tau, config.max_outer_iterations, incremental,
-           extrema_only, f32_original, torch.cuda.current_device())
+           extrema_only, f32_original, host_f64, torch.cuda.current_device())
     plan = _PLAN_CACHE.get(key)
     if plan is None:
         if len(_PLAN_CACHE) >= 4:
             _PLAN_CACHE.pop(next(iter(_PLAN_CACHE))).close()
         plan = DomainPlan(DomainSpec.whole(dims), config.xi_abs, config.tau,
                           config.max_outer_iterations, incremental=incremental,
-                          extrema_only=extrema_only, f32_original=f32_original)
+                          extrema_only=extrema_only, f32_original=f32_original,
+                          host_f64=host_f64)
         _PLAN_CACHE[key] = plan
     return plan
 
@@ -241,28 +258,32 @@ def run_correction_device(f: torch.Tensor, fhat: torch.Tensor, dims, config: Cor
 
 def run_correction(original: ScalarField, decompressed: ScalarField, config: CorrectionConfig,
                    *, incremental: bool = True) -> CorrectionResult:
-    """Drop-in for topocorrect.run_correction (correction.py:391-436)."""
+    """Drop-in for topocorrect.run_correction (correction.py:391-436).
+
+    One pmsz_run_correction_host call on the ScalarFields' own (pageable)
+    arrays: host threads stage the inputs through a pinned ring while K0 runs
+    slab by slab, the corrected field is filled from fhat on the host and
+    patched with the edit record (include/pmsz.h).  ScalarField always holds
+    f64 (grid.py:57); the original is narrowed to f32 while it is staged and
+    runs the f32 K0 when every value survives the round trip (fields read
+    from f32 files, codec.py:86-87) -- otherwise the call reruns on an f64
+    plan before any iteration has run."""
     if original.dims != decompressed.dims:
         raise ValueError(f"dims differ: {original.dims} vs {decompressed.dims}")
-    dev = torch.device("cuda", torch.cuda.current_device())
-    f = as_device_f64(original.values, dev)
-    fh = as_device_f64(decompressed.values, dev)
-    # ScalarField always holds f64 (grid.py:57); an f32-exact field (every
-    # field read from an f32 file, codec.py:86-87) runs the f32 K0
-    f32 = narrow_if_exact(f)
-    if f32 is not None:
-        f = f32
-    plan = _plan_for(original.dims, config, incremental=incremental, extrema_only=False,
-                     f32_original=f32 is not None)
-    st, res, hist = plan.run(f, fh, fh)   # in place: fh is this call's own device copy
+    dims = original.dims
+    f = np.ascontiguousarray(original.values, dtype=np.float64).reshape(-1)
+    fh = np.ascontiguousarray(decompressed.values, dtype=np.float64).reshape(-1)
+    g = HOST_FIELDS.take(f.size)   # a recycled array when a previous result was dropped
+    for narrow in (True, False):
+        plan = _plan_for(dims, config, incremental=incremental, extrema_only=False,
+                         f32_original=narrow, host_f64=narrow)
+        st, res, hist, ids, vals = plan.run_host(f, fh, g)
+        if st != N.PMSZ_ERR_INEXACT:
+            break
     raise_for(st, res, original.values, decompressed.values, config.xi_abs)
-    g = fh
-    ids, vals = plan.export_edits(g)
-    corrected = ScalarField._owned(original.dims, to_host_f64(g))
-    edits = EditSet(ids=ids.cpu().numpy(), values=vals.cpu().numpy(),
-                    vertex_count=original.vertex_count)
-    return CorrectionResult(corrected=corrected, edits=edits, iterations=int(res.iterations),
-                            edits_per_iteration=tuple(hist),
+    return CorrectionResult(corrected=ScalarField._owned(dims, g),
+                            edits=EditSet._owned(ids, vals, original.vertex_count),
+                            iterations=int(res.iterations), edits_per_iteration=tuple(hist),
                             max_vertex_edits=int(res.max_vertex_edits),
                             verification=DistortionReport.clean())
 

@@ -33,6 +33,7 @@
 #include "qsweep.cuh"
 #include "prep.cuh"
 #include "segment.cuh"
+#include "hoststage.h"
 
 using namespace pmsz;
 
@@ -592,6 +593,12 @@ struct pmsz_plan {
     int64_t* hrec_ids = nullptr;          // pinned bounce buffers of the edit record (field patch)
     double* hrec_vals = nullptr;
     int64_t hrec_cap = 0;
+    int64_t hrec_count = -1;              // record entries held there after a host run (pmsz_edits_host)
+    StageFeed* feed = nullptr;            // host staging thread of a pageable-input host run
+    char* hring = nullptr;                // pinned staging ring (pageable inputs): hring_n x hring_chunk
+    size_t hring_chunk = 0;
+    int hring_n = 0;
+    std::vector<cudaEvent_t> hring_ev;    // ring slot c free again
     unsigned long long* dsig = nullptr;   // pmsz_rounds: the summed round values (device) ...
     unsigned long long* hsig = nullptr;   // ... and their pinned mirror
 };
@@ -1075,7 +1082,9 @@ pmsz_status prep(pmsz_plan* p, const void* f, const double* fh, double* g, cudaS
             // input still arriving in z-slabs: K0 over slab c once slab c and
             // the first plane of slab c + 1 (its upper halo) have landed
             for (size_t c = 0; c < nsl; ++c) {
-                CUDA_TRY(cudaStreamWaitEvent(s, p->stage_ev[1 + std::min(c + 1, nsl - 1)], 0));
+                const size_t j = std::min(c + 1, nsl - 1);
+                if (p->feed && !p->feed->wait((int)j + 1)) break;   // staged on the host: enqueued yet?
+                CUDA_TRY(cudaStreamWaitEvent(s, p->stage_ev[1 + j], 0));
                 queued = p->f32 ? launch_prep_q<float>(p->dom, (const float*)f, fh, g, p->w.code, p->frag_out(), p->ctr,
                                                        det, s, p->stage_z[c], p->stage_z[c + 1])
                                 : launch_prep_q<double>(p->dom, (const double*)f, fh, g, p->w.code, p->frag_out(),
@@ -1086,6 +1095,11 @@ pmsz_status prep(pmsz_plan* p, const void* f, const double* fh, double* g, cudaS
         } else if (p->qprep_on) {
             queued = p->f32 ? launch_prep_q<float>(p->dom, (const float*)f, fh, g, p->w.code, p->frag_out(), p->ctr, det, s)
                             : launch_prep_q<double>(p->dom, (const double*)f, fh, g, p->w.code, p->frag_out(), p->ctr, det, s);
+        }
+        if (nsl > 0 && p->feed && !p->feed->wait((int)nsl)) {
+            p->stage_pending = false;
+            if (p->feed->inexact) return fail(PMSZ_ERR_INEXACT, "original is not exactly representable in float32");
+            return fail(PMSZ_ERR_CUDA, std::string("host staging: ") + cudaGetErrorString(p->feed->err));
         }
         if (nsl > 0) CUDA_TRY(cudaStreamWaitEvent(s, p->stage_ev[nsl], 0));   // every slab is in
         p->stage_pending = false;
@@ -1342,6 +1356,8 @@ void pmsz_plan_destroy(pmsz_plan* p) {
     if (p->d2h_done) cudaEventDestroy(p->d2h_done);
     if (p->hrec_ids) cudaFreeHost(p->hrec_ids);
     if (p->hrec_vals) cudaFreeHost(p->hrec_vals);
+    if (p->hring) cudaFreeHost(p->hring);
+    for (cudaEvent_t e : p->hring_ev) cudaEventDestroy(e);
     if (p->hsig) cudaFreeHost(p->hsig);
     if (p->copy_stream) cudaStreamDestroy(p->copy_stream);
     for (cudaEvent_t e : p->prof_ev) cudaEventDestroy(e);
@@ -1795,12 +1811,106 @@ pmsz_status pmsz_edits_export(pmsz_plan* p, const double* g, int64_t* ids, doubl
     return PMSZ_OK;
 }
 
+namespace {
+// Staging thread of a host run with pageable buffers (hoststage.h): per z-slab,
+// the f and fhat bytes go pageable -> pinned ring slot (all pool threads) ->
+// device (copy_stream), chunk by chunk, so the memcpy of chunk k + 1 overlaps
+// the DMA of chunk k; a pageable corrected field is filled from the fhat chunk
+// in the same pass.  stage_ev[1 + c] is recorded and published per slab for
+// K0's slab launches (prep()).
+void feed_slabs(pmsz_plan* p, StageFeed* fd, int dev, const char* fsrc, bool f_pin, bool narrow, const double* hsrc,
+                bool h_pin, char* fdst, double* hdst, double* gfill, double* gpinned, int64_t plane) {
+    cudaError_t err = cudaSetDevice(dev);
+    bool inexact = false;
+    HostPool& pool = HostPool::get();
+    const size_t fel = p->f32 ? 4 : 8, sel = narrow ? 8 : fel;
+    static const int want = [] {
+        const char* e = getenv("PMSZ_STAGE_THREADS");
+        return e ? atoi(e) : 0;
+    }();
+    static const bool trace = getenv("PMSZ_E2E_TRACE") != nullptr;
+    auto now = [] { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
+    double t_wait = 0, t_copy = 0, t_start = trace ? now() : 0.0;
+    int k = 0;
+    // dbytes device bytes from src (narrow: f64 source, f32 destination)
+    auto stage = [&](char* dst, const char* src, size_t dbytes, bool nar, double* fill) -> cudaError_t {
+        for (size_t o = 0; o < dbytes; o += p->hring_chunk) {
+            if (fd->stop.load(std::memory_order_relaxed)) return cudaSuccess;
+            const size_t len = std::min(p->hring_chunk, dbytes - o);
+            const int r = k++ % p->hring_n;
+            double ta = trace ? now() : 0.0;
+            cudaError_t e = cudaEventSynchronize(p->hring_ev[r]);   // the slot's previous DMA is done
+            if (e != cudaSuccess) return e;
+            double tb = trace ? now() : 0.0;
+            char* pin = p->hring + (size_t)r * p->hring_chunk;
+            std::atomic<bool> bad{false};
+            pool.run([&](int t, int nt) {
+                size_t x0, x1;
+                if (fill)
+                    share_at((uintptr_t)fill + o, len, t, nt, (size_t)2 << 20, &x0, &x1);
+                else
+                    share(len, t, nt, &x0, &x1);
+                if (nar) {   // NaN and overflow fail the round trip too: the f64 plan reports them
+                    if (nt_narrow((float*)(pin + x0), (const double*)src + (o + x0) / 4, (x1 - x0) / 4))
+                        bad.store(true, std::memory_order_relaxed);
+                } else {
+                    nt_copy(pin + x0, fill ? (char*)fill + o + x0 : nullptr, src + o + x0, x1 - x0);
+                }
+                _mm_sfence();   // the streaming stores are visible before the DMA is issued
+            }, want);
+            if (trace) {
+                const double tc = now();
+                t_wait += tb - ta;
+                t_copy += tc - tb;
+            }
+            if (bad.load()) {
+                inexact = true;
+                fd->mark_inexact();
+                return cudaSuccess;
+            }
+            e = cudaMemcpyAsync(dst + o, pin, len, cudaMemcpyHostToDevice, p->copy_stream);
+            if (e == cudaSuccess) e = cudaEventRecord(p->hring_ev[r], p->copy_stream);
+            if (e != cudaSuccess) return e;
+        }
+        return cudaSuccess;
+    };
+    const int64_t nsl = (int64_t)p->stage_z.size() - 1;
+    for (int64_t c = 0; c < nsl && err == cudaSuccess && !inexact && !fd->stop.load(); ++c) {
+        const int64_t o = p->stage_z[c] * plane, m = (p->stage_z[c + 1] - p->stage_z[c]) * plane;
+        if (f_pin)
+            err = cudaMemcpyAsync(fdst + o * fel, fsrc + o * fel, m * fel, cudaMemcpyHostToDevice, p->copy_stream);
+        else
+            err = stage(fdst + o * fel, fsrc + o * sel, m * fel, narrow, nullptr);
+        if (err != cudaSuccess || inexact) break;
+        if (h_pin) {
+            err = cudaMemcpyAsync(hdst + o, hsrc + o, m * 8, cudaMemcpyHostToDevice, p->copy_stream);
+            if (gfill) pool_memcpy(gfill + o, hsrc + o, m * 8);
+        } else {
+            err = stage((char*)(hdst + o), (const char*)(hsrc + o), m * 8, false, gfill ? gfill + o : nullptr);
+        }
+        if (err == cudaSuccess) err = cudaEventRecord(p->stage_ev[1 + c], p->copy_stream);
+        if (gpinned && err == cudaSuccess) {   // pinned field out: the slab streams back (see the caller)
+            err = cudaStreamWaitEvent(p->d2h_stream, p->stage_ev[1 + c], 0);
+            if (err == cudaSuccess)
+                err = cudaMemcpyAsync(gpinned + o, hdst + o, m * 8, cudaMemcpyDeviceToHost, p->d2h_stream);
+        }
+        if (err != cudaSuccess) break;
+        fd->publish((int)c + 1);
+    }
+    if (trace)
+        fprintf(stderr, "stage: %d chunks of %zu MiB, %.2f ms (slot waits %.2f, host copies %.2f), %d threads\n", k,
+                p->hring_chunk >> 20, now() - t_start, t_wait, t_copy, want > 0 ? std::min(want, pool.threads()) : pool.threads());
+    fd->finish(err, inexact);
+}
+}  // namespace
+
 pmsz_status pmsz_run_correction_host(pmsz_plan* p, const void* f_host, const double* fh_host, double* g_host,
                                      int64_t* ids_host, double* vals_host, int64_t edits_cap, int64_t* history,
                                      int64_t history_cap, pmsz_result* r, void* stream) {
     if (!p || !f_host || !fh_host) return fail(PMSZ_ERR_INVALID, "null argument");
     cudaStream_t s = S(stream);
     const size_t fbytes = p->n * (p->f32 ? 4 : 8), gbytes = p->n * 8;
+    p->hrec_count = -1;
     // device staging owned by the plan (allocated on first use, reused: a
     // per-call allocation would remap ~12 bytes/voxel of device memory)
     auto grow = [&](void** ptr, size_t bytes) -> bool {
@@ -1828,29 +1938,72 @@ pmsz_status pmsz_run_correction_host(pmsz_plan* p, const void* f_host, const dou
     for (int64_t c = 0; c <= nsl; ++c) p->stage_z[c] = nz * c / nsl;
     CUDA_TRY(cudaEventRecord(p->stage_ev[0], s));   // earlier work on the staging buffers is done
     CUDA_TRY(cudaStreamWaitEvent(p->copy_stream, p->stage_ev[0], 0));
-    const size_t fel = p->f32 ? 4 : 8;
-    for (int64_t c = 0; c < nsl; ++c) {
-        const int64_t o = p->stage_z[c] * plane, m = (p->stage_z[c + 1] - p->stage_z[c]) * plane;
-        CUDA_TRY(cudaMemcpyAsync((char*)f + o * fel, (const char*)f_host + o * fel, m * fel, cudaMemcpyHostToDevice,
-                                 p->copy_stream));
-        CUDA_TRY(cudaMemcpyAsync(g + o, fh_host + o, m * 8, cudaMemcpyHostToDevice, p->copy_stream));
-        CUDA_TRY(cudaEventRecord(p->stage_ev[1 + c], p->copy_stream));
+    const bool narrow = p->f32 && (p->desc.flags & PMSZ_FLAG_HOST_F64);
+    const bool f_pin = !narrow && host_pinned(f_host), h_pin = host_pinned(fh_host);
+    const bool g_pin = g_host && host_pinned(g_host);
+    double* g_fill = (g_host && !g_pin) ? g_host : nullptr;   // pageable field out: filled from fhat on the host
+    std::thread feeder;
+    if (f_pin && h_pin && !g_fill) {
+        const size_t fel = p->f32 ? 4 : 8;
+        for (int64_t c = 0; c < nsl; ++c) {
+            const int64_t o = p->stage_z[c] * plane, m = (p->stage_z[c + 1] - p->stage_z[c]) * plane;
+            CUDA_TRY(cudaMemcpyAsync((char*)f + o * fel, (const char*)f_host + o * fel, m * fel, cudaMemcpyHostToDevice,
+                                     p->copy_stream));
+            CUDA_TRY(cudaMemcpyAsync(g + o, fh_host + o, m * 8, cudaMemcpyHostToDevice, p->copy_stream));
+            CUDA_TRY(cudaEventRecord(p->stage_ev[1 + c], p->copy_stream));
+        }
+    } else {
+        if (!f_pin || !h_pin) {
+            static const size_t chunk = [] {
+                const char* e = getenv("PMSZ_STAGE_CHUNK_MB");
+                const long mb = e ? atol(e) : 32;
+                return (size_t)std::max(1L, std::min(256L, mb)) << 20;
+            }();
+            if (p->hring_chunk != chunk) {
+                if (p->hring) cudaFreeHost(p->hring);
+                p->hring = nullptr;
+                p->hring_chunk = 0;
+                p->hring_n = 4;
+                CUDA_TRY(cudaMallocHost((void**)&p->hring, chunk * p->hring_n));
+                p->hring_chunk = chunk;
+            }
+            while ((int)p->hring_ev.size() < p->hring_n) {
+                cudaEvent_t e;
+                CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+                p->hring_ev.push_back(e);
+            }
+        }
+        int dev = 0;
+        CUDA_TRY(cudaGetDevice(&dev));
+        p->feed = new StageFeed();
+        if (g_pin && !p->d2h_stream) CUDA_TRY(cudaStreamCreateWithFlags(&p->d2h_stream, cudaStreamNonBlocking));
+        feeder = std::thread(feed_slabs, p, p->feed, dev, (const char*)f_host, f_pin, narrow, fh_host, h_pin, (char*)f, g,
+                             g_fill, g_pin ? g_host : nullptr, plane);
     }
-    // Corrected field out: g equals fhat except at the edits, so the host copy
+    // Pinned field out: g equals fhat except at the edits, so the host copy
     // is streamed back slab by slab as soon as each fhat slab has landed --
     // the device-to-host direction of the link runs concurrently with the
     // host-to-device slabs -- and is patched with the edit record at the end.
     // (A slab may be read while the loop already edits it: every such vertex
     // is in the edit record and gets its final value from the patch.)
-    if (g_host) {
+    auto finish_feed = [&]() -> pmsz_status {
+        if (!feeder.joinable()) return PMSZ_OK;
+        p->feed->stop = true;   // a run that failed early stops the staging
+        feeder.join();
+        const cudaError_t e = p->feed->err;
+        delete p->feed;
+        p->feed = nullptr;
+        if (e != cudaSuccess) return fail(PMSZ_ERR_CUDA, std::string("host staging: ") + cudaGetErrorString(e));
+        return PMSZ_OK;
+    };
+    if (g_pin) {
         if (!p->d2h_stream) CUDA_TRY(cudaStreamCreateWithFlags(&p->d2h_stream, cudaStreamNonBlocking));
         if (!p->d2h_done) CUDA_TRY(cudaEventCreateWithFlags(&p->d2h_done, cudaEventDisableTiming));
-        for (int64_t c = 0; c < nsl; ++c) {
+        for (int64_t c = 0; c < nsl && !feeder.joinable(); ++c) {   // (with a staging thread it issues these)
             const int64_t o = p->stage_z[c] * plane, m = (p->stage_z[c + 1] - p->stage_z[c]) * plane;
             CUDA_TRY(cudaStreamWaitEvent(p->d2h_stream, p->stage_ev[1 + c], 0));
             CUDA_TRY(cudaMemcpyAsync(g_host + o, g + o, m * 8, cudaMemcpyDeviceToHost, p->d2h_stream));
         }
-        CUDA_TRY(cudaEventRecord(p->d2h_done, p->d2h_stream));
     }
     static const bool etrace = getenv("PMSZ_E2E_TRACE") != nullptr;
     auto now = [] { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
@@ -1858,13 +2011,21 @@ pmsz_status pmsz_run_correction_host(pmsz_plan* p, const void* f_host, const dou
     p->stage_pending = true;
     st = pmsz_run_correction(p, f, g, g, history, history_cap, r, stream);
     p->stage_pending = false;
+    {
+        const pmsz_status fs = finish_feed();
+        if (st == PMSZ_OK) st = fs;
+    }
     if (etrace) t1 = now();
     CUDA_TRY(cudaStreamWaitEvent(s, p->stage_ev[nsl], 0));   // (already waited by K0 unless it failed early)
-    if (g_host) CUDA_TRY(cudaStreamWaitEvent(s, p->d2h_done, 0));
+    if (g_pin) {
+        CUDA_TRY(cudaEventRecord(p->d2h_done, p->d2h_stream));
+        CUDA_TRY(cudaStreamWaitEvent(s, p->d2h_done, 0));
+    }
     if (etrace) {
         cudaStreamSynchronize(s);
         t2 = now();
     }
+    if (st == PMSZ_OK && r && r->edit_count == 0) p->hrec_count = 0;
     if (st == PMSZ_OK && r && r->edit_count > 0 && (g_host || (ids_host && vals_host && edits_cap > 0))) {
         const int64_t count = r->edit_count;
         // the whole record when the field is patched from it, else what fits the caller's buffers
@@ -1884,8 +2045,8 @@ pmsz_status pmsz_run_correction_host(pmsz_plan* p, const void* f_host, const dou
         st = pmsz_edits_export(p, g, p->stage_ids, p->stage_vals, m, nullptr, stream);
         if (st == PMSZ_OK) {
             // host destination of the full record: the caller's buffers when they
-            // hold it, else the plan's pinned bounce buffers
-            const bool direct = ids_host && vals_host && edits_cap >= m;
+            // are pinned and hold it, else the plan's pinned bounce buffers
+            const bool direct = ids_host && vals_host && edits_cap >= m && host_pinned(ids_host) && host_pinned(vals_host);
             int64_t* hid = ids_host;
             double* hval = vals_host;
             if (!direct) {
@@ -1922,10 +2083,13 @@ pmsz_status pmsz_run_correction_host(pmsz_plan* p, const void* f_host, const dou
             } else {
                 CUDA_TRY(cudaEventSynchronize(p->rec_ev[nch - 1]));
             }
-            if (!direct && ids_host && vals_host && edits_cap > 0) {
-                const int64_t k = std::min(edits_cap, count);
-                memcpy(ids_host, hid, k * 8);
-                memcpy(vals_host, hval, k * 8);
+            if (!direct) {
+                if (m == count) p->hrec_count = m;
+                if (ids_host && vals_host && edits_cap > 0) {
+                    const int64_t k = std::min(edits_cap, count);
+                    pool_memcpy(ids_host, hid, k * 8);
+                    pool_memcpy(vals_host, hval, k * 8);
+                }
             }
         }
     }
@@ -1934,6 +2098,18 @@ pmsz_status pmsz_run_correction_host(pmsz_plan* p, const void* f_host, const dou
         fprintf(stderr, "e2e: run %.2f ms, d2h field wait %.2f, export %.2f, record + patch + copy-out %.2f (total %.2f)\n", t1 - t0,
                 t2 - t1, t3 - t2, now() - t3, now() - t0);
     return st;
+}
+
+pmsz_status pmsz_edits_host(pmsz_plan* p, int64_t* ids_host, double* vals_host, int64_t cap, int64_t* count_out) {
+    if (!p) return fail(PMSZ_ERR_INVALID, "null argument");
+    if (p->hrec_count < 0) return fail(PMSZ_ERR_INVALID, "the plan holds no edit record (see pmsz_run_correction_host)");
+    if (count_out) *count_out = p->hrec_count;
+    const int64_t k = std::min(cap, p->hrec_count);
+    if (k > 0 && ids_host && vals_host) {
+        pool_memcpy(ids_host, p->hrec_ids, k * 8);
+        pool_memcpy(vals_host, p->hrec_vals, k * 8);
+    }
+    return PMSZ_OK;
 }
 
 // ---- topology -------------------------------------------------------------

@@ -58,7 +58,7 @@ class DomainPlan:
     def __init__(self, spec: DomainSpec, xi: float, tau: float, max_iterations: int,
                  *, incremental: bool = True, extrema_only: bool = False,
                  f32_original: bool = False, host_loop: bool = False, no_robust: bool = False,
-                 explicit_lower: bool = False):
+                 explicit_lower: bool = False, host_f64: bool = False):
         self.lib = N.lib()
         self.spec = spec
         self.xi, self.tau, self.max_iterations = float(xi), float(tau), int(max_iterations)
@@ -76,7 +76,8 @@ class DomainPlan:
                    | (N.FLAG_F32_ORIGINAL if f32_original else 0)
                    | (N.FLAG_HOST_LOOP if host_loop else 0)
                    | (N.FLAG_NO_ROBUST if no_robust else 0)
-                   | (N.FLAG_LOWER if explicit_lower else 0))
+                   | (N.FLAG_LOWER if explicit_lower else 0)
+                   | (N.FLAG_HOST_F64 if host_f64 else 0))
         h = ctypes.c_void_p()
         st = self.lib.pmsz_plan_create(ctypes.byref(d), ctypes.byref(h))
         if st == N.PMSZ_ERR_INVALID:
@@ -128,6 +129,30 @@ class DomainPlan:
         if n_hist <= cap:
             return st, res, [int(hist[i]) for i in range(n_hist)]
         return st, res, self.history()
+
+    def run_host(self, f: np.ndarray, fhat: np.ndarray, g: np.ndarray | None):
+        """pmsz_run_correction_host on host arrays (pageable or pinned): f (f64,
+        or f32 with f32_original; f64 with host_f64), fhat f64, g the f64
+        corrected field out (or None).  Returns (status, PmszResult, history,
+        edit ids, edit values); the record is read back from the plan
+        (pmsz_edits_host) when g is given."""
+        cap = min(self.max_iterations, self.HIST_BUF)
+        hist = (ctypes.c_int64 * cap)()
+        res = N.PmszResult()
+        st = self.lib.pmsz_run_correction_host(self.handle, f.ctypes.data, fhat.ctypes.data,
+                                               None if g is None else g.ctypes.data, None, None, 0,
+                                               hist, cap, ctypes.byref(res), None)
+        n_hist = int(res.iterations)
+        history = [int(hist[i]) for i in range(n_hist)] if n_hist <= cap else self.history()
+        if st != N.PMSZ_OK or g is None:
+            return st, res, history, None, None
+        m = int(res.edit_count)
+        ids = np.empty(m, dtype=np.int64)
+        vals = np.empty(m, dtype=np.float64)
+        cnt = ctypes.c_int64()
+        N.check(self.lib.pmsz_edits_host(self.handle, ids.ctypes.data, vals.ctypes.data, m, ctypes.byref(cnt)),
+                "pmsz_edits_host")
+        return st, res, history, ids, vals
 
     def history(self) -> list[int]:
         """edits_per_iteration of the plan's last run (pmsz_history)."""
@@ -248,6 +273,58 @@ def narrow_if_exact(f64: torch.Tensor) -> torch.Tensor | None:
     N.check(N.lib().pmsz_narrow_f32(N.ptr(f64), f64.numel(), N.ptr(out), ctypes.byref(bad), N.stream_handle()),
             "pmsz_narrow_f32")
     return out if bad.value == 0 else None
+
+
+class HostFieldCache:
+    """Recycled host arrays for corrected fields (the drop-in's output).
+
+    A fresh 1 GB numpy array costs ~15-20 ms of page faults and kernel
+    zeroing before the first value lands (measured on the B200 boxes' hosts;
+    DESIGN.md §8), on a path that is host-memory-bound.  Like a caching host
+    allocator, this keeps the arrays it handed out and reuses one once nobody
+    else references it: every numpy view, slice or memoryview of the array
+    holds a reference to it (views collapse their base to the owning array),
+    so a reference count at the cache's own baseline means it is free.  At
+    most ``max_idle`` idle arrays are kept; ``PMSZ_HOST_CACHE=0`` disables
+    the cache, ``empty_host_cache()`` drops the idle arrays."""
+
+    def __init__(self, max_idle: int = 2):
+        import os
+        self.enabled = os.environ.get("PMSZ_HOST_CACHE", "1") != "0"
+        self.max_idle = max_idle
+        self.arrays: list[np.ndarray] = []
+
+    def _idle(self, i: int) -> bool:
+        import sys
+        # references: the cache's list and getrefcount's argument only
+        return sys.getrefcount(self.arrays[i]) <= 2
+
+    def take(self, n: int) -> np.ndarray:
+        if not self.enabled:
+            return np.empty(n, dtype=np.float64)
+        hit = next((i for i in range(len(self.arrays)) if self.arrays[i].size == n and self._idle(i)), None)
+        if hit is not None:
+            self.arrays.append(self.arrays.pop(hit))     # most recently used last
+        # keep at most max_idle spare arrays besides the one handed out
+        idle = [i for i in range(len(self.arrays) - (hit is not None)) if self._idle(i)]
+        if len(idle) > self.max_idle - (hit is None):
+            drop = set(idle[:len(idle) - self.max_idle + (hit is None)])
+            self.arrays = [self.arrays[i] for i in range(len(self.arrays)) if i not in drop]
+        if hit is None:
+            self.arrays.append(np.empty(n, dtype=np.float64))
+        return self.arrays[-1]
+
+    def clear(self):
+        keep = [i for i in range(len(self.arrays)) if not self._idle(i)]
+        self.arrays = [self.arrays[i] for i in keep]
+
+
+HOST_FIELDS = HostFieldCache()
+
+
+def empty_host_cache() -> None:
+    """Release the idle recycled host field arrays (HostFieldCache)."""
+    HOST_FIELDS.clear()
 
 
 def to_host_f64(t: torch.Tensor) -> np.ndarray:

@@ -96,3 +96,36 @@ def test_apply_edit_rule():
     assert pm.apply_edit(0.1, -0.5, 0.0) == 0.0
     assert pm.apply_edit(0.2, 0.9, 0.0) == 0.2
     assert pm.apply_edit(0.4, 0.25, -10.0) == 0.25
+
+
+def test_host_field_cache_reuses_only_unreferenced_arrays():
+    """HostFieldCache (the drop-in's recycled output arrays): an array is
+    reused only when no array, view or memoryview of it is alive, and at most
+    max_idle spare arrays are kept."""
+    import numpy as np
+    from paper_2601_01787_b200.engine import HostFieldCache
+    c = HostFieldCache(max_idle=2)
+    c.enabled = True
+    a = c.take(16)
+    v = a[3:9]
+    m = memoryview(a)
+    del a
+    b = c.take(16)
+    assert b is not v.base                   # the view still holds the first array
+    del v
+    assert c.take(16) is not b and len(c.arrays) == 3   # the memoryview still holds it
+    m.release()
+    del m
+    first = c.arrays[0]
+    del first
+    again = c.take(16)
+    assert again is c.arrays[-1]
+    arrs = [c.take(8) for _ in range(5)]
+    del arrs
+    keep = c.take(32)
+    idle = sum(1 for i in range(len(c.arrays)) if c._idle(i))
+    assert idle <= 2
+    c.clear()
+    assert all(not c._idle(i) for i in range(len(c.arrays)))
+    assert keep.size == 32
+    assert isinstance(np.asarray(keep), np.ndarray)

@@ -134,3 +134,127 @@ def test_host_entry_slab_pipeline_matches_device(dims):
         assert torch.equal(g_h, ref.corrected.cpu())
         assert torch.equal(ids[:m], ref.edit_ids.cpu()) and torch.equal(vals[:m], ref.edit_values.cpu())
     plan.close()
+
+
+def _slab_case(dims, seed=3):
+    import paper_2601_01787_b200 as pm
+    from paper_2601_01787_b200 import inputs as gen
+    f32 = gen.perlin_device(gen.NoiseSpec(dims, seed), f32=True)
+    xi = gen.relative_to_absolute_device(f32, 1e-4)
+    fh = gen.quantize_device(f32, xi)
+    cfg = pm.CorrectionConfig(xi_abs=xi)
+    return f32, fh, cfg
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["pageable", "narrow", "mixed"])
+def test_host_entry_pageable_buffers(mode):
+    """pmsz_run_correction_host on pageable (numpy) buffers: the inputs are
+    staged through the plan's pinned ring by host threads, the corrected field
+    is filled from fhat on the host and patched; 'narrow' hands an f64
+    original to an f32 plan (PMSZ_FLAG_HOST_F64); 'mixed' has pinned f / g and
+    a pageable fhat and truncated pageable record buffers."""
+    import ctypes
+    import torch
+    import paper_2601_01787_b200 as pm
+    from paper_2601_01787_b200 import _native as N
+    from paper_2601_01787_b200.engine import DomainPlan, DomainSpec
+    dims = (256, 128, 129)
+    f32, fh, cfg = _slab_case(dims)
+    ref = pm.run_correction_device(f32, fh, dims, cfg)
+    n = f32.numel()
+    ref_g = ref.corrected.cpu().numpy()
+    plan = DomainPlan(DomainSpec.whole(dims), cfg.xi_abs, cfg.tau, cfg.max_outer_iterations, f32_original=True,
+                      host_f64=(mode == "narrow"))
+    for _ in range(2):   # twice: the ring and the record bounce are reused
+        if mode == "mixed":
+            f_h = torch.empty(n, dtype=torch.float32, pin_memory=True)
+            f_h.copy_(f32)
+            g_h = torch.empty(n, dtype=torch.float64, pin_memory=True)
+            fh_h = fh.cpu().numpy()
+            cap = ref.edit_ids.numel() // 3
+            ids = np.zeros(cap, dtype=np.int64)
+            vals = np.zeros(cap, dtype=np.float64)
+            hist = (ctypes.c_int64 * 256)()
+            res = N.PmszResult()
+            st = N.lib().pmsz_run_correction_host(plan.handle, N.ptr(f_h), fh_h.ctypes.data, N.ptr(g_h),
+                                                  ids.ctypes.data, vals.ctypes.data, cap, hist, 256,
+                                                  ctypes.byref(res), None)
+            assert st == 0 and int(res.edit_count) == ref.edit_ids.numel()
+            assert np.array_equal(g_h.numpy(), ref_g)
+            assert np.array_equal(ids, ref.edit_ids[:cap].cpu().numpy())
+            assert np.array_equal(vals, ref.edit_values[:cap].cpu().numpy())
+            continue
+        f_h = f32.cpu().numpy() if mode == "pageable" else f32.double().cpu().numpy()
+        fh_h = fh.cpu().numpy()
+        g_h = np.empty(n, dtype=np.float64)
+        st, res, hist, ids, vals = plan.run_host(f_h, fh_h, g_h)
+        assert st == 0
+        assert list(hist) == list(ref.edits_per_iteration)
+        assert np.array_equal(g_h, ref_g)
+        assert np.array_equal(ids, ref.edit_ids.cpu().numpy())
+        assert np.array_equal(vals, ref.edit_values.cpu().numpy())
+    plan.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("where", ["first", "last"])
+def test_host_f64_inexact_original(where):
+    """PMSZ_FLAG_HOST_F64 with an original that does not narrow exactly: the
+    staging thread reports it before K0 has seen the slab, the call returns
+    PMSZ_ERR_INEXACT with no iteration run, and the drop-in reruns on an f64
+    plan -- equal to the device f64 run."""
+    import torch
+    import paper_2601_01787_b200 as pm
+    from paper_2601_01787_b200 import _native as N
+    from paper_2601_01787_b200.engine import DomainPlan, DomainSpec
+    dims = (256, 128, 129)
+    f32, fh, cfg = _slab_case(dims, seed=5)
+    f64 = f32.double()
+    i = 7 if where == "first" else f64.numel() - 300
+    f64[i] = f64[i] + abs(float(f64[i])) * 2.0 ** -40 + 1e-300   # no longer an f32 value, same order
+    plan = DomainPlan(DomainSpec.whole(dims), cfg.xi_abs, cfg.tau, cfg.max_outer_iterations, f32_original=True,
+                      host_f64=True)
+    st, res, hist, ids, vals = plan.run_host(f64.cpu().numpy(), fh.cpu().numpy(), np.empty(f64.numel()))
+    assert st == N.PMSZ_ERR_INEXACT and res.iterations == 0
+    plan.close()
+    ref = pm.run_correction_device(f64, fh, dims, cfg)
+    out = pm.run_correction(pm.ScalarField(dims, f64.cpu().numpy()), pm.ScalarField(dims, fh.cpu().numpy()), cfg)
+    assert np.array_equal(out.corrected.values, ref.corrected.cpu().numpy())
+    assert np.array_equal(out.edits.ids, ref.edit_ids.cpu().numpy())
+    assert np.array_equal(out.edits.values, ref.edit_values.cpu().numpy())
+    assert out.edits_per_iteration == ref.edits_per_iteration
+    assert out.max_vertex_edits == ref.max_vertex_edits
+
+
+@pytest.mark.gpu
+def test_dropin_at_slab_size_matches_device():
+    """The drop-in run_correction(ScalarField, ...) above the slab threshold
+    (narrowed f32 original, pageable arrays) equals the device run."""
+    import paper_2601_01787_b200 as pm
+    dims = (192, 160, 144)
+    f32, fh, cfg = _slab_case(dims, seed=9)
+    ref = pm.run_correction_device(f32, fh, dims, cfg)
+    out = pm.run_correction(pm.ScalarField(dims, f32.double().cpu().numpy()),
+                            pm.ScalarField(dims, fh.cpu().numpy()), cfg)
+    assert np.array_equal(out.corrected.values, ref.corrected.cpu().numpy())
+    assert np.array_equal(out.edits.ids, ref.edit_ids.cpu().numpy())
+    assert np.array_equal(out.edits.values, ref.edit_values.cpu().numpy())
+    assert np.all(np.diff(out.edits.ids) > 0)
+    assert out.iterations == ref.iterations and out.edits_per_iteration == ref.edits_per_iteration
+    # recycled output arrays (HostFieldCache): a held result is never overwritten,
+    # a dropped one is reused
+    ref_g = ref.corrected.cpu().numpy()
+    held = out.corrected.values[::7]           # a view keeps the array alive
+    base = id(out.corrected.values.base)     # (an id: a reference would keep it busy)
+    del out
+    f = pm.ScalarField(dims, f32.double().cpu().numpy())
+    fhat = pm.ScalarField(dims, fh.cpu().numpy())
+    second = pm.run_correction(f, fhat, cfg)
+    assert id(second.corrected.values.base) != base
+    del held
+    third = pm.run_correction(f, fhat, cfg)
+    assert id(third.corrected.values.base) == base
+    for r in (second, third):
+        assert np.array_equal(r.corrected.values, ref_g)
+        assert np.array_equal(r.edits.ids, ref.edit_ids.cpu().numpy())

@@ -1,0 +1,12 @@
+#!/bin/bash
+mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build_di.log 2>&1 || { tail -20 gpurun_out/build_di.log; exit 1; }
+timeout 900 python -m pytest tests/test_integration_stub.py tests/test_gpu_parity.py tests/test_parallel_api.py -x -q -m gpu > gpurun_out/gputests_di.log 2>&1
+echo tests=$?; tail -3 gpurun_out/gputests_di.log
+timeout 600 python bench.py --steps 5 --warmup 3 > gpurun_out/b_di.json 2> gpurun_out/b_di.err
+echo bench=$?
+python - <<'P'
+import json
+d=json.loads(open('gpurun_out/b_di.json').read().strip().splitlines()[-1])
+print(d['ms_per_step'], d['e2e']['value'], d.get('dropin',{}).get('ms_per_call'), d.get('dropin',{}).get('matches_device'))
+P
