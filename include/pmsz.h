@@ -335,6 +335,18 @@ pmsz_status pmsz_perlin(const int64_t gdims[3], const int64_t lo[3], const int64
  * (f32 fields promoted to f64 survive it exactly, codec.py:86-87; the drop-in
  * then runs the f32 K0). */
 pmsz_status pmsz_narrow_f32(const double* v_dev, int64_t n, float* out_dev, int64_t* inexact, void* stream);
+/* Synchronous copies between a HOST array (pageable or pinned) and device
+ * memory, for callers that hold whole fields in plain host memory (the
+ * drop-in's numpy arrays): pageable memory is staged through a process-wide
+ * pinned ring by host threads with streaming stores (see
+ * pmsz_run_correction_host).  pmsz_host_to_device copies n bytes, or with
+ * narrow_f64 != 0 converts n f64 host values to f32 on the device side of the
+ * ring; *inexact = 1 when some value did not survive the round trip.  Both
+ * order themselves after the work already queued on `stream` and return when
+ * the copy is complete. */
+pmsz_status pmsz_host_to_device(void* dst_dev, const void* src_host, int64_t n, int32_t narrow_f64,
+                                int64_t* inexact, void* stream);
+pmsz_status pmsz_device_to_host(void* dst_host, const void* src_dev, int64_t bytes, void* stream);
 /* min / max of n values (f32 or f64); result on the host. */
 pmsz_status pmsz_minmax(const void* values_dev, int32_t is_f32, int64_t n, double* mn, double* mx,
                         void* stream);

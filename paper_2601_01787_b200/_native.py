@@ -125,6 +125,8 @@ SIGNATURES = {
     "pmsz_perlin": (i32, [i64p, i64p, i64p, ctypes.POINTER(i32), ctypes.c_double, i32, vp, vp, vp]),
     "pmsz_minmax": (i32, [vp, i32, i64, dp, dp, vp]),
     "pmsz_narrow_f32": (i32, [vp, i64, vp, i64p, vp]),
+    "pmsz_host_to_device": (i32, [vp, vp, i64, i32, i64p, vp]),
+    "pmsz_device_to_host": (i32, [vp, vp, i64, vp]),
     "pmsz_quantize": (i32, [vp, i32, i64, ctypes.c_double, ctypes.c_double, vp, i64p, vp]),
     "pmsz_bounded_noise": (i32, [vp, i32, i64, i64, i64, i64p, i64p, ctypes.c_double, u64, vp, vp]),
     "pmsz_box_extract": (i32, [i64p, vp, i32, i64p, i64p, vp, vp]),

@@ -14,6 +14,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <emmintrin.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <atomic>
@@ -113,8 +114,19 @@ inline bool nt_narrow(float* dst, const double* src, size_t n) {
 class HostPool {
    public:
     static HostPool& get() {
-        static HostPool* pool = new HostPool();   // never destroyed: idle workers at exit
-        return *pool;
+        // never destroyed (idle workers at exit); a forked child, which has no
+        // copies of the workers, builds its own
+        static std::atomic<HostPool*> pool{nullptr};
+        static std::mutex m;
+        HostPool* p = pool.load();
+        if (p && p->pid_ == getpid()) return *p;
+        std::lock_guard<std::mutex> lk(m);
+        p = pool.load();
+        if (!p || p->pid_ != getpid()) {
+            p = new HostPool();
+            pool.store(p);
+        }
+        return *p;
     }
     int threads() const { return nt_; }
     void run(const std::function<void(int, int)>& fn, int want = 0) {
@@ -138,7 +150,7 @@ class HostPool {
     }
 
    private:
-    HostPool() {
+    HostPool() : pid_(getpid()) {
         const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
         nt_ = (int)std::min(16u, hw);
         for (int t = 1; t < nt_; ++t) std::thread([this, t] { loop(t); }).detach();
@@ -157,6 +169,7 @@ class HostPool {
             if (--pending_ == 0) done_cv_.notify_one();
         }
     }
+    pid_t pid_;
     int nt_ = 1;
     std::mutex run_m_, m_;
     std::condition_variable cv_, done_cv_;

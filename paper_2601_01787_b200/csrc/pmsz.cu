@@ -2112,6 +2112,143 @@ pmsz_status pmsz_edits_host(pmsz_plan* p, int64_t* ids_host, double* vals_host, 
     return PMSZ_OK;
 }
 
+// ---- host <-> device copies of pageable arrays ----------------------------
+// The staging of pmsz_run_correction_host as a plain copy (the block-parallel
+// drop-in, local_converge, ... move whole host fields too): one process-wide
+// pinned ring, pool threads on the host side, streaming stores.
+namespace {
+struct CopyRing {
+    std::mutex m;   // one copy at a time
+    char* buf = nullptr;
+    size_t chunk = 0;
+    int n = 0;
+    std::vector<cudaEvent_t> ev;
+    cudaStream_t st = nullptr;
+    int dev = -1;
+};
+CopyRing& copy_ring() {
+    static CopyRing* r = new CopyRing();
+    return *r;
+}
+// (under r.m) the ring on the current device
+cudaError_t copy_ring_ready(CopyRing& r) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (r.buf && r.dev == dev) return cudaSuccess;
+    if (r.buf) {   // another device: rebuild (events and streams belong to a device)
+        cudaFreeHost(r.buf);
+        for (cudaEvent_t x : r.ev) cudaEventDestroy(x);
+        r.ev.clear();
+        if (r.st) cudaStreamDestroy(r.st);
+        r.buf = nullptr;
+        r.st = nullptr;
+    }
+    r.chunk = (size_t)32 << 20;
+    r.n = 4;
+    if ((e = cudaMallocHost((void**)&r.buf, r.chunk * r.n)) != cudaSuccess) return e;
+    if ((e = cudaStreamCreateWithFlags(&r.st, cudaStreamNonBlocking)) != cudaSuccess) return e;
+    for (int i = 0; i < r.n; ++i) {
+        cudaEvent_t x;
+        if ((e = cudaEventCreateWithFlags(&x, cudaEventDisableTiming)) != cudaSuccess) return e;
+        r.ev.push_back(x);
+    }
+    r.dev = dev;
+    return cudaSuccess;
+}
+}  // namespace
+
+pmsz_status pmsz_host_to_device(void* dst_dev, const void* src_host, int64_t n, int32_t narrow_f64, int64_t* inexact,
+                                void* stream) {
+    if (inexact) *inexact = 0;
+    if (n < 0 || (n > 0 && (!dst_dev || !src_host))) return fail(PMSZ_ERR_INVALID, "bad arguments");
+    if (n == 0) return PMSZ_OK;
+    cudaStream_t s = S(stream);
+    const size_t dbytes = (size_t)n * (narrow_f64 ? 4 : 1);
+    if (!narrow_f64 && host_pinned(src_host)) {
+        CUDA_TRY(cudaMemcpyAsync(dst_dev, src_host, dbytes, cudaMemcpyHostToDevice, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        return PMSZ_OK;
+    }
+    CopyRing& r = copy_ring();
+    std::lock_guard<std::mutex> lk(r.m);
+    CUDA_TRY(copy_ring_ready(r));
+    cudaEvent_t start;
+    CUDA_TRY(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventRecord(start, s));                 // earlier work on dst is ordered first
+    CUDA_TRY(cudaStreamWaitEvent(r.st, start, 0));
+    cudaEventDestroy(start);
+    HostPool& pool = HostPool::get();
+    bool bad = false;
+    int k = 0;
+    for (size_t o = 0; o < dbytes && !bad; o += r.chunk, ++k) {
+        const size_t len = std::min(r.chunk, dbytes - o);
+        char* pin = r.buf + (size_t)(k % r.n) * r.chunk;
+        CUDA_TRY(cudaEventSynchronize(r.ev[k % r.n]));
+        std::atomic<bool> nb{false};
+        pool.run([&](int t, int nt) {
+            size_t a, b;
+            share(len, t, nt, &a, &b);
+            if (narrow_f64) {
+                if (nt_narrow((float*)(pin + a), (const double*)src_host + (o + a) / 4, (b - a) / 4))
+                    nb.store(true, std::memory_order_relaxed);
+            } else {
+                nt_copy(pin + a, nullptr, (const char*)src_host + o + a, b - a);
+            }
+            _mm_sfence();
+        });
+        if (nb.load()) bad = true;
+        CUDA_TRY(cudaMemcpyAsync((char*)dst_dev + o, pin, len, cudaMemcpyHostToDevice, r.st));
+        CUDA_TRY(cudaEventRecord(r.ev[k % r.n], r.st));
+    }
+    CUDA_TRY(cudaStreamSynchronize(r.st));
+    if (inexact) *inexact = bad ? 1 : 0;
+    return PMSZ_OK;
+}
+
+pmsz_status pmsz_device_to_host(void* dst_host, const void* src_dev, int64_t bytes, void* stream) {
+    if (bytes < 0 || (bytes > 0 && (!dst_host || !src_dev))) return fail(PMSZ_ERR_INVALID, "bad arguments");
+    if (bytes == 0) return PMSZ_OK;
+    cudaStream_t s = S(stream);
+    if (host_pinned(dst_host)) {
+        CUDA_TRY(cudaMemcpyAsync(dst_host, src_dev, (size_t)bytes, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        return PMSZ_OK;
+    }
+    CopyRing& r = copy_ring();
+    std::lock_guard<std::mutex> lk(r.m);
+    CUDA_TRY(copy_ring_ready(r));
+    cudaEvent_t start;
+    CUDA_TRY(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventRecord(start, s));                 // the producer of src is ordered first
+    CUDA_TRY(cudaStreamWaitEvent(r.st, start, 0));
+    cudaEventDestroy(start);
+    HostPool& pool = HostPool::get();
+    const size_t total = (size_t)bytes;
+    const int64_t nch = (int64_t)((total + r.chunk - 1) / r.chunk);
+    // DMA up to r.n chunks ahead of the host copy-out
+    auto issue = [&](int64_t c) -> cudaError_t {
+        const size_t o = (size_t)c * r.chunk, len = std::min(r.chunk, total - o);
+        cudaError_t e = cudaMemcpyAsync(r.buf + (size_t)(c % r.n) * r.chunk, (const char*)src_dev + o, len,
+                                        cudaMemcpyDeviceToHost, r.st);
+        return e == cudaSuccess ? cudaEventRecord(r.ev[c % r.n], r.st) : e;
+    };
+    for (int64_t c = 0; c < std::min<int64_t>(nch, r.n); ++c) CUDA_TRY(issue(c));
+    for (int64_t c = 0; c < nch; ++c) {
+        const size_t o = (size_t)c * r.chunk, len = std::min(r.chunk, total - o);
+        const char* pin = r.buf + (size_t)(c % r.n) * r.chunk;
+        CUDA_TRY(cudaEventSynchronize(r.ev[c % r.n]));
+        pool.run([&](int t, int nt) {
+            size_t a, b;
+            share_at((uintptr_t)dst_host + o, len, t, nt, (size_t)2 << 20, &a, &b);
+            nt_copy((char*)dst_host + o + a, nullptr, pin + a, b - a);
+            _mm_sfence();
+        });
+        if (c + r.n < nch) CUDA_TRY(issue(c + r.n));   // the slot is free again
+    }
+    return PMSZ_OK;
+}
+
 // ---- topology -------------------------------------------------------------
 static Dom whole_dom(int64_t nx, int64_t ny, int64_t nz) {
     pmsz_desc d{};

@@ -25,7 +25,8 @@ import torch
 
 from . import _native as N
 from .correction import CorrectionConfig, CorrectionResult, EditSet
-from .engine import (BoundViolationError, ConvergenceError, DomainPlan, DomainSpec, as_device_f64, narrow_if_exact,
+from .engine import (BoundViolationError, ConvergenceError, DomainPlan, DomainSpec, as_device_f64,
+                     as_device_narrowed, narrow_if_exact,
                      to_host_f64,
                      raise_for)
 from .grid import ScalarField
@@ -325,17 +326,21 @@ def run_parallel(original: ScalarField, decompressed: ScalarField, config: Corre
         raise ValueError(f"dims differ: {original.dims} vs {decompressed.dims}")
     dims = original.dims
     dev = torch.device("cuda", torch.cuda.current_device())
-    f = as_device_f64(original.values, dev)
+    # f32-exact originals (f32 files, codec.py:86-87) are narrowed on the host
+    # while staged and run the f32 K0 everywhere; others go up as f64
+    f = as_device_narrowed(original.values, dev)
+    f32 = f is not None
+    if not f32:
+        f = as_device_f64(original.values, dev)
     fh = as_device_f64(decompressed.values, dev)
     # validate_error_bound + global f-code for the final verification
     gplan = DomainPlan(DomainSpec.whole(dims), config.xi_abs, config.tau, config.max_outer_iterations,
-                       incremental=False)
+                       incremental=False, f32_original=f32)
     scratch = torch.empty_like(fh)
     st, res = gplan.prepare(f, fh, scratch)
     raise_for(st, res, original.values, decompressed.values, config.xi_abs)
     decomp = decompose(dims, block_grid)
-    f32 = narrow_if_exact(f)   # f32-exact originals run the f32 K0 in every block
-    blocks = [_DevBlock(b, dims, config, f if f32 is None else f32, fh) for b in decomp.blocks]
+    blocks = [_DevBlock(b, dims, config, f, fh) for b in decomp.blocks]
     lockstep = strategy is SyncStrategy.LOCKSTEP
     rounds = syncs = 0
     totals: list[int] = []
@@ -388,8 +393,10 @@ def run_parallel(original: ScalarField, decompressed: ScalarField, config: Corre
         raise ConvergenceError("corrected field escaped the error bound")
     if any(gplan.verify(out)):
         raise ConvergenceError("distortions survived at termination")
-    corrected = ScalarField._owned(dims, to_host_f64(out))
-    edits = EditSet.diff(decompressed, corrected)
+    corrected = ScalarField._owned(dims, to_host_f64(out, recycle=True))
+    # EditSet.diff (correction.py:363-369) on the device: ascending ids where g != fhat
+    ids_d = torch.nonzero(out != fh).reshape(-1)
+    edits = EditSet._owned(ids_d.cpu().numpy(), out[ids_d].cpu().numpy(), original.vertex_count)
     result = CorrectionResult(corrected=corrected, edits=edits,
                               iterations=max(b.iterations for b in blocks),
                               edits_per_iteration=tuple(totals),

@@ -258,3 +258,49 @@ def test_dropin_at_slab_size_matches_device():
     for r in (second, third):
         assert np.array_equal(r.corrected.values, ref_g)
         assert np.array_equal(r.edits.ids, ref.edit_ids.cpu().numpy())
+
+
+@pytest.mark.parametrize("n", [1, 1000, (32 << 20) // 8 + 3, 3 * (32 << 20) // 8 + 77])
+def test_staged_host_device_copies(n):
+    """pmsz_host_to_device / pmsz_device_to_host on pageable numpy arrays
+    (pinned ring, host threads, streaming stores): exact bytes both ways for
+    sizes around the 32 MiB ring chunk, and the f64 -> f32 narrowing reports
+    a value that does not survive the round trip."""
+    import ctypes
+    import torch
+    from paper_2601_01787_b200 import _native as N
+    rng = np.random.default_rng(n)
+    src = rng.standard_normal(n)
+    dev = torch.empty(n, dtype=torch.float64, device="cuda")
+    N.check(N.lib().pmsz_host_to_device(N.ptr(dev), src.ctypes.data, src.nbytes, 0, None, None), "h2d")
+    assert np.array_equal(dev.cpu().numpy(), src)
+    back = np.empty(n)
+    N.check(N.lib().pmsz_device_to_host(back.ctypes.data, N.ptr(dev), back.nbytes, None), "d2h")
+    assert np.array_equal(back, src)
+    exact = src.astype(np.float32).astype(np.float64)
+    d32 = torch.empty(n, dtype=torch.float32, device="cuda")
+    bad = ctypes.c_int64(-1)
+    N.check(N.lib().pmsz_host_to_device(N.ptr(d32), exact.ctypes.data, n, 1, ctypes.byref(bad), None), "narrow")
+    assert bad.value == 0 and np.array_equal(d32.cpu().numpy(), exact.astype(np.float32))
+    exact[n // 2] += 2.0 ** -40 * (1 + abs(exact[n // 2]))
+    N.check(N.lib().pmsz_host_to_device(N.ptr(d32), exact.ctypes.data, n, 1, ctypes.byref(bad), None), "narrow")
+    assert bad.value == 1
+
+
+def test_run_parallel_dropin_staged_matches_device():
+    """run_parallel(ScalarField, ...) above the staging threshold: the original
+    is narrowed while staged, the result comes back through the staged copy
+    into a recycled array -- equal to the single-domain device run (lockstep)
+    and bit-identical across two calls."""
+    import paper_2601_01787_b200 as pm
+    dims = (128, 96, 130)
+    f32, fh, cfg = _slab_case(dims, seed=11)
+    ref = pm.run_correction_device(f32, fh, dims, cfg)
+    f = pm.ScalarField(dims, f32.double().cpu().numpy())
+    fhat = pm.ScalarField(dims, fh.cpu().numpy())
+    a, sa = pm.run_parallel(f, fhat, cfg, (1, 2, 2), pm.SyncStrategy.LOCKSTEP)
+    b, sb = pm.run_parallel(f, fhat, cfg, (1, 2, 2), pm.SyncStrategy.LOCKSTEP)
+    assert np.array_equal(a.corrected.values, ref.corrected.cpu().numpy())
+    assert np.array_equal(a.edits.ids, ref.edit_ids.cpu().numpy())
+    assert np.array_equal(a.edits.values, ref.edit_values.cpu().numpy())
+    assert np.array_equal(b.corrected.values, a.corrected.values) and sa.rounds == sb.rounds
