@@ -239,12 +239,51 @@ __device__ __forceinline__ uint4 load_words4(const uint32_t* bits, int64_t w, in
 
 // Chunk of the bitmap -> ascending ids (bits cleared on the way when `clear`).
 // A round covers 4 x 256 words: thread t owns the four consecutive words
-// 4 t .. 4 t + 3 (one vector load), one block scan per round.
+// 4 t .. 4 t + 3 (one vector load), one block scan per round.  The round's
+// ids are staged in shared memory at their scanned positions and written out
+// by consecutive threads (coalesced), unless the round holds more than
+// kStageIds of them (then each thread writes its own, as the bits come).
+constexpr int kStageIds = 4096;
+
+template <class Out>
+__device__ __forceinline__ void compact_round(const uint4 v, int64_t w, unsigned long long pos0, uint32_t* stage,
+                                              unsigned* wt, unsigned& total, Out&& out) {
+    const unsigned before = block_exclusive_scan(__popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w), wt, total);
+    const uint32_t m4[4] = {v.x, v.y, v.z, v.w};
+    if (total <= (unsigned)kStageIds) {
+        unsigned k = before;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            uint32_t m = m4[q];
+            while (m) {
+                const int b = __ffs(m) - 1;
+                m &= m - 1;
+                stage[k++] = (uint32_t)((w + q) * 32 + b);   // ids < 2^32 (plan limit)
+            }
+        }
+        __syncthreads();
+        for (unsigned e = threadIdx.x; e < total; e += kCompactThreads) out(pos0 + e, (int64_t)stage[e]);
+        __syncthreads();   // stage is reused by the next round
+    } else {
+        unsigned long long pos = pos0 + before;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            uint32_t m = m4[q];
+            while (m) {
+                const int b = __ffs(m) - 1;
+                m &= m - 1;
+                out(pos++, (w + q) * 32 + b);
+            }
+        }
+    }
+}
+
 template <typename IdT>
 __global__ void __launch_bounds__(kCompactThreads) k_chunk_list(uint32_t* __restrict__ bits, Chunks c,
                                                                 const unsigned long long* __restrict__ offs,
                                                                 IdT* __restrict__ list, int clear) {
     __shared__ unsigned wt[kCompactThreads / 32];
+    __shared__ uint32_t stage[kStageIds];
     const int64_t w0 = (int64_t)blockIdx.x * c.chunk, w1 = min(w0 + c.chunk, c.nwords);
     unsigned long long pos0 = offs[blockIdx.x];
     uint4 nxt = load_words4(bits, w0 + 4 * threadIdx.x, w1);
@@ -259,18 +298,8 @@ __global__ void __launch_bounds__(kCompactThreads) k_chunk_list(uint32_t* __rest
                 for (int q = 0; q < 4 && w + q < w1; ++q) bits[w + q] = 0u;
         }
         unsigned total;
-        const unsigned before = block_exclusive_scan(__popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w), wt, total);
-        unsigned long long pos = pos0 + before;
-        const uint32_t m4[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            uint32_t m = m4[q];
-            while (m) {
-                const int b = __ffs(m) - 1;
-                m &= m - 1;
-                list[pos++] = (IdT)((w + q) * 32 + b);
-            }
-        }
+        compact_round(v, w, pos0, stage, wt, total,
+                      [&](unsigned long long pos, int64_t id) { list[pos] = (IdT)id; });
         pos0 += total;
     }
 }
@@ -281,6 +310,7 @@ __global__ void __launch_bounds__(kCompactThreads) k_chunk_write(const uint32_t*
                                                                  const double* __restrict__ g, int64_t* ids,
                                                                  double* vals, int64_t cap) {
     __shared__ unsigned wt[kCompactThreads / 32];
+    __shared__ uint32_t stage[kStageIds];
     const int64_t w0 = (int64_t)blockIdx.x * c.chunk, w1 = min(w0 + c.chunk, c.nwords);
     unsigned long long pos0 = offs[blockIdx.x];
     uint4 nxt = load_words4(bits, w0 + 4 * threadIdx.x, w1);
@@ -289,23 +319,12 @@ __global__ void __launch_bounds__(kCompactThreads) k_chunk_write(const uint32_t*
         const uint4 v = nxt;
         nxt = load_words4(bits, w + 4 * kCompactThreads, w1);
         unsigned total;
-        const unsigned before = block_exclusive_scan(__popc(v.x) + __popc(v.y) + __popc(v.z) + __popc(v.w), wt, total);
-        long long pos = (long long)(pos0 + before);
-        const uint32_t m4[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            uint32_t m = m4[q];
-            while (m) {
-                const int b = __ffs(m) - 1;
-                m &= m - 1;
-                const int64_t id = (w + q) * 32 + b;
-                if (id < n && pos < cap) {
-                    ids[pos] = id;
-                    vals[pos] = g[id];
-                }
-                ++pos;
+        compact_round(v, w, pos0, stage, wt, total, [&](unsigned long long pos, int64_t id) {
+            if (id < n && (long long)pos < cap) {
+                ids[pos] = id;
+                vals[pos] = g[id];
             }
-        }
+        });
         pos0 += total;
     }
 }
