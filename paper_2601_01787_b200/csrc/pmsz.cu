@@ -202,6 +202,67 @@ __global__ void __launch_bounds__(kCompactThreads) k_chunk_count(const uint32_t*
     }
 }
 
+// k_chunk_count and k_chunk_scan in one launch: the last CTA to finish (a
+// ticket in *done, reset by that CTA) scans the per-chunk counts.
+__global__ void __launch_bounds__(kCompactThreads) k_chunk_count_scan(const uint32_t* __restrict__ bits, Chunks c,
+                                                                      unsigned long long* counts,
+                                                                      unsigned long long* total, unsigned* done) {
+    __shared__ unsigned long long ws[kCompactThreads / 32];
+    __shared__ bool last;
+    const int64_t w0 = (int64_t)blockIdx.x * c.chunk, w1 = min(w0 + c.chunk, c.nwords);
+    unsigned t = 0;
+    for (int64_t w = w0 + threadIdx.x; w < w1; w += kCompactThreads) t += __popc(__ldg(bits + w));
+    t = __reduce_add_sync(0xffffffffu, t);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) ws[wid] = t;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long sum = 0;
+        for (int q = 0; q < kCompactThreads / 32; ++q) sum += ws[q];
+        counts[blockIdx.x] = sum;
+        __threadfence();
+        last = atomicAdd(done, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    // exclusive scan of counts[0 .. n), n <= 1024 = 4 per thread
+    const int n = (int)gridDim.x;
+    unsigned long long v[4], mine = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int i = 4 * threadIdx.x + k;
+        v[k] = i < n ? __ldcg(counts + i) : 0ull;
+        mine += v[k];
+    }
+    unsigned long long sc = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(0xffffffffu, sc, o);
+        if (lane >= o) sc += y;
+    }
+    __syncthreads();   // ws is reused
+    if (lane == 31) ws[wid] = sc;
+    __syncthreads();
+    unsigned long long before = 0, all = 0;
+#pragma unroll
+    for (int q = 0; q < kCompactThreads / 32; ++q) {
+        before += q < wid ? ws[q] : 0ull;
+        all += ws[q];
+    }
+    unsigned long long pos = before + sc - mine;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int i = 4 * threadIdx.x + k;
+        if (i < n) counts[i] = pos;
+        pos += v[k];
+    }
+    if (threadIdx.x == 0) {
+        if (total) *total = all;
+        *done = 0u;
+    }
+}
+
 // counts[0..n) -> exclusive offsets in place; the total -> *total (n <= 1024).
 __global__ void __launch_bounds__(kMaxChunks) k_chunk_scan(unsigned long long* counts, int n,
                                                            unsigned long long* total) {
@@ -696,9 +757,8 @@ pmsz_status reset_iter(pmsz_plan* p, cudaStream_t s, int nxt) {
 // lands in *dst on the device.
 void launch_bits_total(pmsz_plan* p, const uint32_t* bits, unsigned long long* dst, cudaStream_t s) {
     p->offsets_of = bits;
-    k_chunk_count<<<(unsigned)p->ch.n, kCompactThreads, 0, s>>>(bits, p->ch, p->block_counts);
-    LAUNCHED();
-    k_chunk_scan<<<1, kMaxChunks, 0, s>>>(p->block_counts, p->ch.n, dst);
+    k_chunk_count_scan<<<(unsigned)p->ch.n, kCompactThreads, 0, s>>>(bits, p->ch, p->block_counts, dst,
+                                                                     (unsigned*)(p->block_counts + kMaxChunks));
     LAUNCHED();
 }
 
@@ -1301,7 +1361,7 @@ pmsz_status pmsz_plan_create(const pmsz_desc* desc, pmsz_plan** out) {
               alloc((void**)&p->w.touched, p->nwords * 4) && alloc((void**)&p->w.detbits, p->nwords * 4) &&
               alloc((void**)&p->w.code, n) && alloc((void**)&p->frag, p->nwords * 4) &&
               alloc((void**)&p->ctr, sizeof(DevCounters)) &&
-              alloc((void**)&p->block_counts, kMaxChunks * 8);
+              alloc((void**)&p->block_counts, (kMaxChunks + 1) * 8);   // + the count/scan ticket
     if (ok && p->w.incremental)
         ok = alloc((void**)&p->w.actbits, p->nwords * 4) && alloc((void**)&p->w.act[0], p->w.act_cap * 4) &&
              alloc((void**)&p->w.act[1], p->w.act_cap * 4) && alloc((void**)&p->w.iteredit, p->nwords * 4) &&
@@ -1349,6 +1409,7 @@ pmsz_status pmsz_plan_create(const pmsz_desc* desc, pmsz_plan** out) {
     memset(p->hctr, 0, sizeof(DevCounters));
     if (cudaMemset(p->w.prop, 0xff, n * 8) != cudaSuccess || cudaMemset(p->ctr, 0, sizeof(DevCounters)) != cudaSuccess ||
         cudaMemset(p->w.touched, 0, p->nwords * 4) != cudaSuccess || cudaMemset(p->w.detbits, 0, p->nwords * 4) != cudaSuccess ||
+        cudaMemset(p->block_counts, 0, (kMaxChunks + 1) * 8) != cudaSuccess ||
         cudaDeviceSynchronize() != cudaSuccess) {
         pmsz_plan_destroy(p);
         return fail(PMSZ_ERR_CUDA, "plan initialisation failed");
