@@ -152,8 +152,16 @@ class HostPool {
    private:
     HostPool() : pid_(getpid()) {
         const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-        nt_ = (int)std::min(16u, hw);
-        for (int t = 1; t < nt_; ++t) std::thread([this, t] { loop(t); }).detach();
+        const int want = (int)std::min(16u, hw);
+        nt_ = 1;
+        for (int t = 1; t < want; ++t) {   // (a thread that cannot start just shrinks the pool)
+            try {
+                std::thread([this, t] { loop(t); }).detach();
+            } catch (...) {
+                break;
+            }
+            nt_ = t + 1;
+        }
     }
     void loop(int t) {
         uint64_t seen = 0;

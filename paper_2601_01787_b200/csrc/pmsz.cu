@@ -2055,10 +2055,16 @@ pmsz_status pmsz_run_correction_host(pmsz_plan* p, const void* f_host, const dou
         }
         int dev = 0;
         CUDA_TRY(cudaGetDevice(&dev));
-        p->feed = new StageFeed();
         if (g_pin && !p->d2h_stream) CUDA_TRY(cudaStreamCreateWithFlags(&p->d2h_stream, cudaStreamNonBlocking));
-        feeder = std::thread(feed_slabs, p, p->feed, dev, (const char*)f_host, f_pin, narrow, fh_host, h_pin, (char*)f, g,
-                             g_fill, g_pin ? g_host : nullptr, plane);
+        try {   // (no exception may cross the C ABI)
+            p->feed = new StageFeed();
+            feeder = std::thread(feed_slabs, p, p->feed, dev, (const char*)f_host, f_pin, narrow, fh_host, h_pin, (char*)f,
+                                 g, g_fill, g_pin ? g_host : nullptr, plane);
+        } catch (const std::exception& e) {
+            delete p->feed;
+            p->feed = nullptr;
+            return fail(PMSZ_ERR_CUDA, std::string("host staging thread: ") + e.what());
+        }
     }
     // Pinned field out: g equals fhat except at the edits, so the host copy
     // is streamed back slab by slab as soon as each fhat slab has landed --
