@@ -155,7 +155,10 @@ struct Chunks {
 inline Chunks make_chunks(int64_t nwords, int sms) {
     Chunks c;
     c.nwords = nwords;
-    int64_t want = std::min<int64_t>(kMaxChunks, std::max<int64_t>(1, (int64_t)sms * 6));
+    // six chunks per SM (measured: 16 or 27 per SM, i.e. shorter chains of
+    // rounds per CTA, are 0.01 ms slower per step at 512^3)
+    static const int per_sm = getenv("PMSZ_COMPACT_PER_SM") ? std::max(1, atoi(getenv("PMSZ_COMPACT_PER_SM"))) : 6;
+    int64_t want = std::min<int64_t>(kMaxChunks, std::max<int64_t>(1, (int64_t)sms * per_sm));
     int64_t per = (nwords + want - 1) / want;
     constexpr int64_t kRound = 4 * kCompactThreads;   // words per round of the list / write kernels
     per = std::max<int64_t>(kRound, (per + kRound - 1) / kRound * kRound);
@@ -186,24 +189,8 @@ __device__ __forceinline__ unsigned block_exclusive_scan(unsigned v, unsigned* w
     return before + s - v;
 }
 
-__global__ void __launch_bounds__(kCompactThreads) k_chunk_count(const uint32_t* __restrict__ bits, Chunks c,
-                                                                 unsigned long long* counts) {
-    __shared__ unsigned long long ws[kCompactThreads / 32];
-    const int64_t w0 = (int64_t)blockIdx.x * c.chunk, w1 = min(w0 + c.chunk, c.nwords);
-    unsigned long long t = 0;
-    for (int64_t w = w0 + threadIdx.x; w < w1; w += kCompactThreads) t += __popc(__ldg(bits + w));
-    t = __reduce_add_sync(0xffffffffu, (unsigned)t);
-    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = t;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned long long s = 0;
-        for (int q = 0; q < kCompactThreads / 32; ++q) s += ws[q];
-        counts[blockIdx.x] = s;
-    }
-}
-
-// k_chunk_count and k_chunk_scan in one launch: the last CTA to finish (a
-// ticket in *done, reset by that CTA) scans the per-chunk counts.
+// Per-chunk set-bit counts and their exclusive scan in one launch: the last
+// CTA to finish (a ticket in *done, reset by that CTA) scans the counts.
 __global__ void __launch_bounds__(kCompactThreads) k_chunk_count_scan(const uint32_t* __restrict__ bits, Chunks c,
                                                                       unsigned long long* counts,
                                                                       unsigned long long* total, unsigned* done) {
@@ -226,12 +213,13 @@ __global__ void __launch_bounds__(kCompactThreads) k_chunk_count_scan(const uint
     __syncthreads();
     if (!last) return;
     __threadfence();
-    // exclusive scan of counts[0 .. n), n <= 1024 = 4 per thread
+    // exclusive scan of counts[0 .. n), n <= kMaxChunks = kPer per thread
+    constexpr int kPer = kMaxChunks / kCompactThreads;
     const int n = (int)gridDim.x;
-    unsigned long long v[4], mine = 0;
+    unsigned long long v[kPer], mine = 0;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        const int i = 4 * threadIdx.x + k;
+    for (int k = 0; k < kPer; ++k) {
+        const int i = kPer * threadIdx.x + k;
         v[k] = i < n ? __ldcg(counts + i) : 0ull;
         mine += v[k];
     }
@@ -252,8 +240,8 @@ __global__ void __launch_bounds__(kCompactThreads) k_chunk_count_scan(const uint
     }
     unsigned long long pos = before + sc - mine;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        const int i = 4 * threadIdx.x + k;
+    for (int k = 0; k < kPer; ++k) {
+        const int i = kPer * threadIdx.x + k;
         if (i < n) counts[i] = pos;
         pos += v[k];
     }
@@ -261,29 +249,6 @@ __global__ void __launch_bounds__(kCompactThreads) k_chunk_count_scan(const uint
         if (total) *total = all;
         *done = 0u;
     }
-}
-
-// counts[0..n) -> exclusive offsets in place; the total -> *total (n <= 1024).
-__global__ void __launch_bounds__(kMaxChunks) k_chunk_scan(unsigned long long* counts, int n,
-                                                           unsigned long long* total) {
-    __shared__ unsigned long long wt[32];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const unsigned long long v = threadIdx.x < n ? counts[threadIdx.x] : 0ull;
-    unsigned long long s = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const unsigned long long y = __shfl_up_sync(0xffffffffu, s, o);
-        if (lane >= o) s += y;
-    }
-    if (lane == 31) wt[wid] = s;
-    __syncthreads();
-    unsigned long long before = 0, all = 0;
-    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) {
-        before += q < wid ? wt[q] : 0ull;
-        all += wt[q];
-    }
-    if (threadIdx.x < n) counts[threadIdx.x] = before + s - v;
-    if (threadIdx.x == 0 && total) *total = all;
 }
 
 // Four consecutive bitmap words w .. w + 3 of [.., w1) (one 16-byte load when whole).
@@ -2642,13 +2607,13 @@ pmsz_status pmsz_bits_to_ids(const uint32_t* bits, int64_t nbits, int64_t* ids, 
     }
     const Chunks ch = make_chunks(nwords, num_sms());
     unsigned long long* bc = nullptr;
-    CUDA_TRY(cudaMallocAsync((void**)&bc, (kMaxChunks + 1) * 8, s));
-    k_chunk_count<<<(unsigned)ch.n, kCompactThreads, 0, s>>>(bits, ch, bc);
-    LAUNCHED();
-    k_chunk_scan<<<1, kMaxChunks, 0, s>>>(bc, ch.n, bc + kMaxChunks);
+    CUDA_TRY(cudaMallocAsync((void**)&bc, (kMaxChunks + 2) * 8, s));
+    CUDA_TRY(cudaMemsetAsync(bc + kMaxChunks, 0, 8, s));   // the ticket
+    k_chunk_count_scan<<<(unsigned)ch.n, kCompactThreads, 0, s>>>(bits, ch, bc, bc + kMaxChunks + 1,
+                                                                  (unsigned*)(bc + kMaxChunks));
     LAUNCHED();
     unsigned long long total = 0;
-    CUDA_TRY(cudaMemcpyAsync(&total, bc + kMaxChunks, 8, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemcpyAsync(&total, bc + kMaxChunks + 1, 8, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
     *count = (int64_t)total;
     if (ids && (int64_t)total <= cap && total > 0) {
