@@ -353,6 +353,10 @@ pmsz_status pmsz_minmax(const void* values_dev, int32_t is_f32, int64_t n, doubl
 /* quantize (quantizer.py:122-154): recon = origin + code*(2 xi) with the ulp repair. */
 pmsz_status pmsz_quantize(const void* f_dev, int32_t is_f32, int64_t n, double origin, double xi,
                           double* recon_dev, int64_t* max_code_out, void* stream);
+/* The same with the integer codes of the payload (QuantizedPayload.codes,
+ * quantizer.py:146-153) into codes_dev (u64[n]). */
+pmsz_status pmsz_quantize_codes(const void* f_dev, int32_t is_f32, int64_t n, double origin, double xi,
+                                double* recon_dev, uint64_t* codes_dev, int64_t* max_code_out, void* stream);
 /* Seeded bounded noise fhat = clamp(f + xi*u, f - xi, f + xi), u in [-1,1) from a
  * counter hash of (seed, global id); ids are global so blocks agree. */
 pmsz_status pmsz_bounded_noise(const void* f_dev, int32_t is_f32, int64_t nx, int64_t ny,

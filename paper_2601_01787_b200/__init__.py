@@ -17,6 +17,6 @@ from .parallel import (Block, BlockDecomposition, ParallelStats, SyncStrategy, b
                        local_converge, run_parallel, sync_ghosts)
 from .codec import (FormatError, decode_edits, decode_edits_meta, encode_edits, read_field, read_labels,
                     write_field, write_labels)
-from .inputs import NoiseSpec, PeakSpec
+from .inputs import NoiseSpec, PeakSpec, QuantizedPayload, perlin, quantize, reconstruct, relative_to_absolute
 
 __version__ = "0.1.0"

@@ -128,6 +128,7 @@ SIGNATURES = {
     "pmsz_host_to_device": (i32, [vp, vp, i64, i32, i64p, vp]),
     "pmsz_device_to_host": (i32, [vp, vp, i64, vp]),
     "pmsz_quantize": (i32, [vp, i32, i64, ctypes.c_double, ctypes.c_double, vp, i64p, vp]),
+    "pmsz_quantize_codes": (i32, [vp, i32, i64, ctypes.c_double, ctypes.c_double, vp, vp, i64p, vp]),
     "pmsz_bounded_noise": (i32, [vp, i32, i64, i64, i64, i64p, i64p, ctypes.c_double, u64, vp, vp]),
     "pmsz_box_extract": (i32, [i64p, vp, i32, i64p, i64p, vp, vp]),
     "pmsz_segmentation": (i32, [i64, i64, i64, vp, i32, vp, vp, vp]),

@@ -106,7 +106,8 @@ __global__ void __launch_bounds__(256) k_minmax(const FT* __restrict__ v, int64_
 template <typename FT>
 __global__ void __launch_bounds__(256) k_quantize(const FT* __restrict__ f, int64_t n, double origin,
                                                  double xi, double two_xi, double* __restrict__ recon,
-                                                 unsigned long long* maxcode, unsigned long long* fails) {
+                                                 unsigned long long* maxcode, unsigned long long* fails,
+                                                 unsigned long long* __restrict__ codes) {
     unsigned long long my_max = 0, my_fail = 0;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -118,6 +119,7 @@ __global__ void __launch_bounds__(256) k_quantize(const FT* __restrict__ f, int6
         r = origin + (double)code * two_xi;
         if (fabs(fv - r) > xi || code < 0) ++my_fail;                   // quantizer.py:142-145
         recon[i] = r;
+        if (codes) codes[i] = (unsigned long long)code;                  // QuantizedPayload.codes
         my_max = max(my_max, (unsigned long long)(code < 0 ? 0 : code));
     }
     for (int o = 16; o; o >>= 1) {

@@ -2461,6 +2461,11 @@ pmsz_status pmsz_minmax(const void* v, int32_t is_f32, int64_t n, double* mn, do
 
 pmsz_status pmsz_quantize(const void* f, int32_t is_f32, int64_t n, double origin, double xi, double* recon,
                           int64_t* max_code, void* stream) {
+    return pmsz_quantize_codes(f, is_f32, n, origin, xi, recon, nullptr, max_code, stream);
+}
+
+pmsz_status pmsz_quantize_codes(const void* f, int32_t is_f32, int64_t n, double origin, double xi, double* recon,
+                                uint64_t* codes, int64_t* max_code, void* stream) {
     if (!f || !recon || n < 1 || !(xi > 0)) return fail(PMSZ_ERR_INVALID, "bad arguments");
     cudaStream_t s = S(stream);
     unsigned long long* k = nullptr;
@@ -2468,9 +2473,11 @@ pmsz_status pmsz_quantize(const void* f, int32_t is_f32, int64_t n, double origi
     CUDA_TRY(cudaMemsetAsync(k, 0, 16, s));
     const double two_xi = 2.0 * xi;
     if (is_f32)
-        k_quantize<float><<<grid_for(n, 256, 16), 256, 0, s>>>((const float*)f, n, origin, xi, two_xi, recon, k, k + 1);
+        k_quantize<float><<<grid_for(n, 256, 16), 256, 0, s>>>((const float*)f, n, origin, xi, two_xi, recon, k, k + 1,
+                                                               (unsigned long long*)codes);
     else
-        k_quantize<double><<<grid_for(n, 256, 16), 256, 0, s>>>((const double*)f, n, origin, xi, two_xi, recon, k, k + 1);
+        k_quantize<double><<<grid_for(n, 256, 16), 256, 0, s>>>((const double*)f, n, origin, xi, two_xi, recon, k, k + 1,
+                                                                (unsigned long long*)codes);
     LAUNCHED();
     unsigned long long out[2];
     CUDA_TRY(cudaMemcpyAsync(out, k, 16, cudaMemcpyDeviceToHost, s));

@@ -134,3 +134,68 @@ def gaussian_peaks_device(spec: PeakSpec, *, lo=(0, 0, 0), ext=None, f32: bool =
     N.check(N.lib().pmsz_gaussian_peaks(N.ivec(gd), N.ivec(lo), N.ivec(e), int(spec.seed) & (2**64 - 1), int(f32),
                                         N.ptr(out), N.stream_handle()), "pmsz_gaussian_peaks")
     return out
+
+
+# ---- the reference's host-facing generators (drop-in names) -----------------
+@dataclass(frozen=True, eq=False)
+class QuantizedPayload:
+    """quantizer.QuantizedPayload (quantizer.py:28-44): the quantizer's codes
+    and what reconstructs the field from them.  (The bit-packed byte form,
+    to_bytes / from_bytes, is the codec -- out of scope.)"""
+    dims: tuple[int, int, int]
+    xi_abs: float
+    origin: float
+    bit_width: int
+    codes: np.ndarray
+    payload_bytes: int
+
+
+def perlin(spec: NoiseSpec):
+    """synth.perlin (synth.py:83-100): the field as a ScalarField, generated on
+    the device bit for bit."""
+    from .engine import to_host_f64
+    from .grid import ScalarField
+    return ScalarField._owned(spec.dims, to_host_f64(perlin_device(spec)))
+
+
+def relative_to_absolute(field, eb_rel: float) -> float:
+    """quantizer.relative_to_absolute (quantizer.py:99-113)."""
+    v = field.values
+    return relative_to_absolute_range(float(v.min()), float(v.max()), eb_rel)
+
+
+def quantize(field, xi_abs: float):
+    """quantizer.quantize (quantizer.py:122-154) -> (QuantizedPayload, ScalarField):
+    codes and reconstruction computed on the device (with the ulp repair)."""
+    from .engine import as_device_f64, to_host_f64
+    from .grid import ScalarField
+    if not (xi_abs > 0 and np.isfinite(xi_abs)):
+        raise ValueError(f"absolute error bound must be positive, got {xi_abs}")
+    f = field.values
+    origin, fmax = float(f.min()), float(f.max())
+    if (fmax - origin) / (2.0 * xi_abs) > 2.0 ** 53:
+        raise ValueError("error bound too small for the field's value range")
+    fd = as_device_f64(f, torch.device("cuda", torch.cuda.current_device()))
+    recon = torch.empty(fd.numel(), dtype=torch.float64, device=fd.device)
+    codes = torch.empty(fd.numel(), dtype=torch.int64, device=fd.device)
+    mc = ctypes.c_int64()
+    st = N.lib().pmsz_quantize_codes(N.ptr(fd), 0, fd.numel(), origin, float(xi_abs), N.ptr(recon), N.ptr(codes),
+                                     ctypes.byref(mc), N.stream_handle())
+    if st != N.PMSZ_OK:
+        raise AssertionError(N.last_error())
+    codes_h = codes.cpu().numpy().view(np.uint64)
+    codes_h.setflags(write=False)
+    bit_width = max(1, int(mc.value).bit_length())
+    ndims = 2 if field.dims[2] == 1 else 3
+    n = field.vertex_count
+    size = 25 + 8 * ndims + (n * bit_width + 7) // 8 + 4
+    payload = QuantizedPayload(dims=field.dims, xi_abs=float(xi_abs), origin=origin, bit_width=bit_width,
+                               codes=codes_h, payload_bytes=size)
+    return payload, ScalarField._owned(field.dims, to_host_f64(recon))
+
+
+def reconstruct(payload: QuantizedPayload):
+    """quantizer.reconstruct (quantizer.py:157-159): origin + code * (2 xi)."""
+    from .grid import ScalarField
+    values = payload.origin + payload.codes.astype(np.float64) * (2.0 * payload.xi_abs)
+    return ScalarField(payload.dims, values)

@@ -77,10 +77,12 @@ def main():
                                    ((20, 17, 9), 7, 4.0, 3), ((64, 64, 64), 0, 4.0, 3), ((33, 5, 7), 123456789, 2.5, 4)]:
         f = tc.perlin(tc.NoiseSpec(dims=dims, seed=seed, frequency=freq, octaves=octv))
         xi = tc.relative_to_absolute(f, 1e-3)
-        _, recon = tc.quantize(f, xi)
+        payload, recon = tc.quantize(f, xi)
         perl.append({"dims": list(dims), "seed": seed, "frequency": freq, "octaves": octv,
                      "sha256": sha(f.values), "xi_rel_1e-3": xi, "quantized_sha256": sha(recon.values),
-                     "f32_sha256": sha(f.values.astype(np.float32))})
+                     "f32_sha256": sha(f.values.astype(np.float32)),
+                     "payload": {"origin": payload.origin, "bit_width": payload.bit_width,
+                                 "payload_bytes": payload.payload_bytes, "codes_sha256": sha(payload.codes)}})
     meta["perlin"] = perl
 
     # ---- _iterate_array trajectories (test_correction.py:215-235)

@@ -546,3 +546,23 @@ def test_residual_and_bound_detection_on_crafted_fields():
     bad[idx[2:]] = f[idx[2:]] - 2 * xi     # below L
     assert plan.bounds_violations(fd, torch.from_numpy(bad).to(DEV)) == 4
     plan.close()
+
+
+def test_host_generators_match_reference(golden):
+    """The reference's host-facing names (synth.perlin, quantizer.relative_to_absolute,
+    quantize -> (QuantizedPayload, ScalarField), reconstruct) on the device
+    generators: field, bound, codes, bit width and payload size as the reference's."""
+    meta, _ = golden
+    for p in meta["perlin"]:
+        dims = tuple(p["dims"]) if len(p["dims"]) == 3 else (*p["dims"], 1)
+        f = pm.perlin(pm.NoiseSpec(dims, p["seed"], p["frequency"], p["octaves"]))
+        assert isinstance(f, pm.ScalarField) and sha(f.values) == p["sha256"]
+        xi = pm.relative_to_absolute(f, 1e-3)
+        assert xi == p["xi_rel_1e-3"]
+        payload, recon = pm.quantize(f, xi)
+        assert sha(recon.values) == p["quantized_sha256"]
+        q = p["payload"]
+        assert (payload.origin, payload.bit_width, payload.payload_bytes) == (q["origin"], q["bit_width"],
+                                                                              q["payload_bytes"])
+        assert payload.codes.dtype == np.uint64 and sha(payload.codes) == q["codes_sha256"]
+        assert np.array_equal(pm.reconstruct(payload).values, recon.values)
