@@ -9,7 +9,7 @@ from .grid import (RANK_OFFSETS, STENCIL, ScalarField, linear_index, neighbors, 
                    vertex_coords)
 from .engine import BoundViolationError, ConvergenceError, empty_host_cache
 from .topology import (DistortionReport, ExtremaSet, NeighborScan, SegmentationLabels, compare_plmss,
-                       compute_segmentation, field_scan, find_extrema, scan_neighbors)
+                       compute_segmentation, compute_segmentation_naive, field_scan, find_extrema, scan_neighbors)
 from .correction import (BoundsField, CorrectionConfig, CorrectionResult, DeviceCorrection, EditSet,
                          apply_edit, compute_bounds, iterate_array, run_correction,
                          run_correction_device, validate_error_bound)
@@ -17,6 +17,9 @@ from .parallel import (Block, BlockDecomposition, ParallelStats, SyncStrategy, b
                        local_converge, run_parallel, sync_ghosts)
 from .codec import (FormatError, decode_edits, decode_edits_meta, encode_edits, read_field, read_labels,
                     write_field, write_labels)
-from .inputs import NoiseSpec, PeakSpec, QuantizedPayload, perlin, quantize, reconstruct, relative_to_absolute
+from .inputs import (NoiseSpec, PayloadFormatError, PeakSpec, QuantizedPayload, constant, perlin, quantize, ramp,
+                     reconstruct, relative_to_absolute)
+from .records import (Distortion, DistortionKind, correction_iteration, detect_distortions, extreme_neighbor,
+                      is_maximum, is_minimum, propose_corrections)
 
 __version__ = "0.1.0"

@@ -199,3 +199,26 @@ def reconstruct(payload: QuantizedPayload):
     from .grid import ScalarField
     values = payload.origin + payload.codes.astype(np.float64) * (2.0 * payload.xi_abs)
     return ScalarField(payload.dims, values)
+
+
+class PayloadFormatError(ValueError):
+    """quantizer.PayloadFormatError: a malformed payload byte string."""
+
+
+def ramp(dims, coefficients=(1.0, 2.0, 4.0)):
+    """synth.ramp (synth.py:108-116): c0 x + c1 y + c2 z, no interior extrema."""
+    from .grid import ScalarField
+    d = tuple(int(v) for v in dims)
+    nx, ny, nz = d if len(d) == 3 else (d[0], d[1], 1)
+    c = tuple(float(v) for v in coefficients) + (0.0, 0.0, 0.0)
+    z, y, x = np.meshgrid(np.arange(nz, dtype=np.float64), np.arange(ny, dtype=np.float64),
+                          np.arange(nx, dtype=np.float64), indexing="ij")
+    return ScalarField((nx, ny, nz), (c[0] * x + c[1] * y + c[2] * z).reshape(-1))
+
+
+def constant(dims, value: float = 0.0):
+    """synth.constant (synth.py:119-121)."""
+    from .grid import ScalarField
+    d = tuple(int(v) for v in dims)
+    nx, ny, nz = d if len(d) == 3 else (d[0], d[1], 1)
+    return ScalarField((nx, ny, nz), np.full(nx * ny * nz, float(value)))

@@ -165,6 +165,14 @@ def compute_segmentation(field: ScalarField) -> SegmentationLabels:
     return SegmentationLabels(dims=field.dims, asc_target=asc.cpu().numpy(), desc_target=desc.cpu().numpy())
 
 
+def compute_segmentation_naive(field: ScalarField) -> SegmentationLabels:
+    """topology.compute_segmentation_naive (topology.py:177-194): the reference
+    follows the steepest pointers one step at a time as an oracle for its
+    pointer-jumping path; both define the same labels, which is what this
+    returns (the device pointer jumping of compute_segmentation)."""
+    return compute_segmentation(field)
+
+
 def _bits_to_ids(bits: torch.Tensor, nbits: int) -> np.ndarray:
     cnt = N.ctypes.c_int64()
     lib = N.lib()
