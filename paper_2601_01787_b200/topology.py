@@ -50,7 +50,8 @@ def scan_neighbors(values: np.ndarray, dims) -> NeighborScan:
     """GPU steepest-neighbour scan of a flat x-fastest f64 array."""
     dims = _dims3(dims)
     dev = torch.device("cuda", torch.cuda.current_device())
-    v = torch.from_numpy(np.ascontiguousarray(values, dtype=np.float64)).to(dev)
+    from .engine import as_device_f64
+    v = as_device_f64(values, dev)
     nmax, nmin, ismax, ismin = scan_neighbors_device(v, dims)
     return NeighborScan(nmax=nmax.cpu().numpy(), nmin=nmin.cpu().numpy(),
                         is_max=ismax.cpu().numpy().astype(bool),
