@@ -52,7 +52,13 @@ __device__ __forceinline__ void ring_from_smem(const double* dn, const double* c
     vc = ct[cell];
 }
 
-constexpr int kQSlots = 6;
+#ifndef PMSZ_QSLOTS
+#define PMSZ_QSLOTS 6   // plane slots of the ring (3 in use + look-ahead)
+#endif
+#ifndef PMSZ_QMINB
+#define PMSZ_QMINB 3    // resident CTAs per SM
+#endif
+constexpr int kQSlots = PMSZ_QSLOTS;
 constexpr int kQConsumers = kQY / kQRowsPerThread;   // consumer warps (4 rows x 32 columns each)
 constexpr int kQThreads = (kQConsumers + 1) * 32;     // + one producer warp
 struct QSmem {
@@ -80,7 +86,7 @@ __device__ __forceinline__ void mbar_arrive(unsigned bar) {
 // with the g plane as one more TMA box (needs x0 % 16 == 0 and nx % 16 == 0;
 // launch_qsweep falls back to tiles.cuh otherwise).
 template <bool kCount, bool kMasked, bool kExtrema>
-__global__ void __launch_bounds__(kQThreads, 3) k_qsweep_tma(Dom d, const __grid_constant__ CUtensorMap tm,
+__global__ void __launch_bounds__(kQThreads, PMSZ_QMINB) k_qsweep_tma(Dom d, const __grid_constant__ CUtensorMap tm,
                                                              const __grid_constant__ CUtensorMap tmc,
                                                              const __grid_constant__ CUtensorMap tmd,
                                                              DetectOp<kCount, kMasked, kExtrema> op, int zchunk) {
