@@ -243,12 +243,13 @@ def run_correction_device(f: torch.Tensor, fhat: torch.Tensor, dims, config: Cor
         plan = _plan_for(dims, config, incremental=incremental, extrema_only=extrema_only,
                          f32_original=f32)
     g = out if out is not None else torch.empty_like(fhat)
-    st, res, hist = plan.run(f, fhat, g, stream=stream)
-    raise_for(st, res, None, None, config.xi_abs, f_dev=f, fhat_dev=fhat)
-    if export_edits:
-        ids, vals = plan.export_edits(g, stream=stream)
-    else:
-        ids = vals = torch.empty(0, device=g.device)
+    with plan.lock:
+        st, res, hist = plan.run(f, fhat, g, stream=stream)
+        raise_for(st, res, None, None, config.xi_abs, f_dev=f, fhat_dev=fhat)
+        if export_edits:
+            ids, vals = plan.export_edits(g, stream=stream)
+        else:
+            ids = vals = torch.empty(0, device=g.device)
     return DeviceCorrection(corrected=g, edit_ids=ids, edit_values=vals,
                             iterations=int(res.iterations), edits_per_iteration=tuple(hist),
                             max_vertex_edits=int(res.max_vertex_edits),
@@ -277,7 +278,8 @@ def run_correction(original: ScalarField, decompressed: ScalarField, config: Cor
     for narrow in (True, False):
         plan = _plan_for(dims, config, incremental=incremental, extrema_only=False,
                          f32_original=narrow, host_f64=narrow)
-        st, res, hist, ids, vals = plan.run_host(f, fh, g)
+        with plan.lock:
+            st, res, hist, ids, vals = plan.run_host(f, fh, g)
         if st != N.PMSZ_ERR_INEXACT:
             break
     raise_for(st, res, original.values, decompressed.values, config.xi_abs)

@@ -85,6 +85,8 @@ class DomainPlan:
         N.check(st, "pmsz_plan_create")
         self.handle = h
         self.n = spec.dims[0] * spec.dims[1] * spec.dims[2]
+        import threading
+        self.lock = threading.RLock()   # a plan runs one correction at a time (cached plans are shared)
 
     def close(self):
         if getattr(self, "handle", None):
@@ -290,9 +292,11 @@ class HostFieldCache:
 
     def __init__(self, max_idle: int = 2):
         import os
+        import threading
         self.enabled = os.environ.get("PMSZ_HOST_CACHE", "1") != "0"
         self.max_idle = max_idle
         self.arrays: list[np.ndarray] = []
+        self._lock = threading.Lock()   # two threads must not both take one idle array
 
     def _idle(self, i: int) -> bool:
         import sys
@@ -302,6 +306,10 @@ class HostFieldCache:
     def take(self, n: int) -> np.ndarray:
         if not self.enabled:
             return np.empty(n, dtype=np.float64)
+        with self._lock:
+            return self._take(n)
+
+    def _take(self, n: int) -> np.ndarray:
         hit = next((i for i in range(len(self.arrays)) if self.arrays[i].size == n and self._idle(i)), None)
         if hit is not None:
             self.arrays.append(self.arrays.pop(hit))     # most recently used last
@@ -315,8 +323,9 @@ class HostFieldCache:
         return self.arrays[-1]
 
     def clear(self):
-        keep = [i for i in range(len(self.arrays)) if not self._idle(i)]
-        self.arrays = [self.arrays[i] for i in keep]
+        with self._lock:
+            keep = [i for i in range(len(self.arrays)) if not self._idle(i)]
+            self.arrays = [self.arrays[i] for i in keep]
 
 
 HOST_FIELDS = HostFieldCache()
