@@ -304,3 +304,18 @@ def test_run_parallel_dropin_staged_matches_device():
     assert np.array_equal(a.edits.ids, ref.edit_ids.cpu().numpy())
     assert np.array_equal(a.edits.values, ref.edit_values.cpu().numpy())
     assert np.array_equal(b.corrected.values, a.corrected.values) and sa.rounds == sb.rounds
+
+
+@pytest.mark.parametrize("dims", [(2048, 1024, 3), (3000, 2000, 1), (1024, 64, 65)])
+def test_dropin_staging_odd_slab_layouts(dims):
+    """The staged host path where the z-slabs are single planes (nz = 3),
+    where there is one plane (2-D: one slab), and with a chunk size that does
+    not divide the slabs -- equal to the device run."""
+    import paper_2601_01787_b200 as pm
+    f32, fh, cfg = _slab_case(dims, seed=13)
+    ref = pm.run_correction_device(f32, fh, dims, cfg)
+    out = pm.run_correction(pm.ScalarField(dims, f32.double().cpu().numpy()),
+                            pm.ScalarField(dims, fh.cpu().numpy()), cfg)
+    assert np.array_equal(out.corrected.values, ref.corrected.cpu().numpy())
+    assert np.array_equal(out.edits.ids, ref.edit_ids.cpu().numpy())
+    assert out.edits_per_iteration == ref.edits_per_iteration
