@@ -18,6 +18,18 @@
 
 namespace pmsz {
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per call site and
+// device (it is per device, and a host call per launch costs the launch
+// path several microseconds): `done` is the call site's device bitmask.
+template <typename F>
+inline void smem_attr_once(F* fn, int bytes, unsigned long long& done) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (done & bit) return;
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) == cudaSuccess) done |= bit;
+}
+
 // Offsets in ascending-id (rank) order, packed 2 bits per rank (value + 1) so
 // a run-time rank costs a shift and a mask, no memory table:
 //   dx: -1 0 -1 0 | -1 0 -1 1 0 1 | 0 1 0 1

@@ -986,11 +986,8 @@ pmsz_status launch_tail(pmsz_plan* p, const void* f, double* g, cudaStream_t s, 
 // Small dirty sets: the one-CTA shared-memory tail (k_tail1, tail.cuh).
 template <typename FT>
 pmsz_status launch_tail1(pmsz_plan* p, const void* f, double* g, cudaStream_t s, long long budget, int chained) {
-    static bool attr = false;
-    if (!attr) {
-        CUDA_TRY(cudaFuncSetAttribute(k_tail1<FT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kT1SmemBytes));
-        attr = true;
-    }
+    static unsigned long long attr = 0;
+    smem_attr_once(k_tail1<FT>, (int)kT1SmemBytes, attr);
     static const bool trace = getenv("PMSZ_TAIL_TRACE") != nullptr;
     static unsigned long long* trace_buf = nullptr;
     unsigned long long* tr = nullptr;
@@ -1080,17 +1077,50 @@ void tail_result(pmsz_plan* p, pmsz_result* r, int64_t k) {
     r->sparse_sweeps += k;
 }
 
-pmsz_status reset_run_state(pmsz_plan* p, cudaStream_t s) {
+// The per-run resets in one launch (instead of a memset call each: the host
+// side of those calls delayed K0 by ~40 us per run).  Buffers are cudaMalloc'd
+// (16-byte aligned); the counters are reset by one thread, which then sets
+// bound_first to all-ones.
+struct ZeroList {
+    void* p[8];
+    unsigned long long bytes[8];
+    int k;
+};
+__global__ void __launch_bounds__(256) k_zero_many(ZeroList z, DevCounters* ctr) {
+    const unsigned long long t = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    if (t == 0) {
+        unsigned long long* c = reinterpret_cast<unsigned long long*>(ctr);
+        for (size_t i = 0; i < sizeof(DevCounters) / 8; ++i) c[i] = 0ull;
+        ctr->bound_first = ~0ull;
+    }
+    for (int b = 0; b < z.k; ++b) {
+        uint4* q = reinterpret_cast<uint4*>(z.p[b]);
+        const unsigned long long n16 = z.bytes[b] / 16;
+        for (unsigned long long i = t; i < n16; i += stride) q[i] = make_uint4(0u, 0u, 0u, 0u);
+        unsigned char* tail = reinterpret_cast<unsigned char*>(z.p[b]);
+        for (unsigned long long i = n16 * 16 + t; i < z.bytes[b]; i += stride) tail[i] = 0;
+    }
+}
+
+pmsz_status reset_run_state(pmsz_plan* p, cudaStream_t s, uint32_t* extra0 = nullptr, uint32_t* extra1 = nullptr) {
     p->edits_cached = -1;
     p->mark_deferred = false;
-    CUDA_TRY(cudaMemsetAsync(p->ctr, 0, sizeof(DevCounters), s));
-    CUDA_TRY(cudaMemsetAsync(&p->ctr->bound_first, 0xff, sizeof(unsigned long long), s));
-    CUDA_TRY(cudaMemsetAsync(p->w.editbits, 0, p->nwords * 4, s));
-    CUDA_TRY(cudaMemsetAsync(p->w.counts, 0, p->n * (p->w.counts32 ? 4 : 2), s));
+    ZeroList z{};
+    auto add = [&](void* ptr, unsigned long long bytes) {
+        if (ptr && bytes) { z.p[z.k] = ptr; z.bytes[z.k] = bytes; ++z.k; }
+    };
+    add(p->w.editbits, p->nwords * 4);
+    add(p->w.counts, p->n * (p->w.counts32 ? 4 : 2));
     if (p->w.incremental) {
-        CUDA_TRY(cudaMemsetAsync(p->w.actbits, 0, p->nwords * 4, s));
-        CUDA_TRY(cudaMemsetAsync(p->w.iteredit, 0, p->nwords * 4, s));
+        add(p->w.actbits, p->nwords * 4);
+        add(p->w.iteredit, p->nwords * 4);
     }
+    add(extra0, p->nwords * 4);   // (prep: the fragile and detection bitmaps)
+    add(extra1, p->nwords * 4);
+    k_zero_many<<<num_sms() * 4, 256, 0, s>>>(z, p->ctr);
+    LAUNCHED();
+    CUDA_TRY(cudaGetLastError());
     p->cur = 0;
     p->next_mode = kFull;
     p->pending = 0;
@@ -1111,15 +1141,14 @@ pmsz_status restore_prop(pmsz_plan* p, cudaStream_t s) {
 // reads them with the first iteration's counters (one synchronisation less)
 // and must call prep_checks() before trusting anything else.
 pmsz_status prep(pmsz_plan* p, const void* f, const double* fh, double* g, cudaStream_t s, bool sync = true) {
-    pmsz_status st = reset_run_state(p, s);
+    // K0 also runs the first detection sweep (g = fhat) unless told otherwise;
+    // the fragile and detection bitmaps are cleared with the run state
+    uint32_t* det = p->fuse_on ? p->w.detbits : nullptr;
+    pmsz_status st = reset_run_state(p, s, p->robust_on ? p->frag : nullptr, det);
     if (st) return st;
     {
         ProfScope ps(p, s, PMSZ_K_PREP);
         p->w.frag = p->robust_on ? p->frag : nullptr;
-        if (p->robust_on) CUDA_TRY(cudaMemsetAsync(p->frag, 0, p->nwords * 4, s));
-        // K0 also runs the first detection sweep (g = fhat) unless told otherwise
-        uint32_t* det = p->fuse_on ? p->w.detbits : nullptr;
-        if (det) CUDA_TRY(cudaMemsetAsync(det, 0, p->nwords * 4, s));
         bool queued = false;
         const size_t nsl = p->stage_pending ? p->stage_z.size() - 1 : 0;
         if (p->qprep_on && nsl > 0) {

@@ -475,9 +475,12 @@ inline bool launch_prep_q(const Dom& d, const FT* f, const double* fh, double* g
     const dim3 grid((unsigned)((d.nx + kQX - 1) / kQX), (unsigned)((d.ny + kQY - 1) / kQY), (unsigned)chunks);
     const dim3 block(kQX, kQY / kQRowsPerThread, 1);
     const size_t smem = sizeof(PrepSmem<FT>);
-#define PMSZ_LAUNCH_PREP(R, D)                                                                          \
-    cudaFuncSetAttribute(k_prep_q<FT, R, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-    k_prep_q<FT, R, D><<<grid, block, smem, s>>>(all, tf, th, a, zchunk)
+#define PMSZ_LAUNCH_PREP(R, D)                                                    \
+    {                                                                             \
+        static unsigned long long attr = 0;                                      \
+        smem_attr_once(k_prep_q<FT, R, D>, (int)smem, attr);                     \
+        k_prep_q<FT, R, D><<<grid, block, smem, s>>>(all, tf, th, a, zchunk);    \
+    }
     if (frag && det) { PMSZ_LAUNCH_PREP(true, true); }
     else if (frag) { PMSZ_LAUNCH_PREP(true, false); }
     else if (det) { PMSZ_LAUNCH_PREP(false, true); }

@@ -253,8 +253,8 @@ inline bool launch_qsweep(const Dom& d, const double* g, const Work& w, cudaStre
     Op op{w, dirty, 0};
     const dim3 block(kQX, kQConsumers + 1, 1);
     auto kern = k_qsweep_tma<kCount, kMasked, kExtrema>;
-    static bool attr = false;
-    if (!attr) attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kQSmemBytes) == cudaSuccess;
+    static unsigned long long attr = 0;
+    smem_attr_once(kern, (int)kQSmemBytes, attr);
     kern<<<grid, block, kQSmemBytes, s>>>(d, tm, tmc, tmd, op, zchunk);
     return true;
 }

@@ -20,7 +20,7 @@ for _ in range(3):
     pm.run_correction_device(f32, fh, dims, cfg, out=out)
 torch.cuda.synchronize()
 from torch.profiler import profile, ProfilerActivity
-with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
+with profile(activities=[ProfilerActivity.CUDA]) as prof:
     pm.run_correction_device(f32, fh, dims, cfg, out=out)
     torch.cuda.synchronize()
 path = "gpurun_out/gap_trace.json"
