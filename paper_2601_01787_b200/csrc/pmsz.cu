@@ -573,6 +573,8 @@ struct pmsz_plan {
     Work w{};
     DevCounters* ctr = nullptr;
     DevCounters* hctr = nullptr;   // pinned mirror
+    volatile unsigned long long* hflag = nullptr;   // pinned: the last k_publish sequence number
+    unsigned long long sync_seq = 0;
     unsigned long long* block_counts = nullptr;
     Chunks ch{};              // bitmap compaction layout
     int64_t scratch_bytes = 0;
@@ -704,7 +706,43 @@ struct ProfScope {
     ~ProfScope() { prof_end(p, s, tok, cls); }
 };
 
+// The counters reach the host by a one-CTA kernel writing them into the
+// pinned (mapped) mirror and then a sequence number into a pinned flag the
+// host spins on: no copy-engine round trip and no stream synchronisation on
+// the ~5 host decisions of a run (each cost the device ~25 us idle).  The
+// kernel is the last operation of the stream, so the flag also means every
+// earlier operation has completed.
+__global__ void k_publish(const DevCounters* __restrict__ c, DevCounters* h, volatile unsigned long long* flag,
+                          unsigned long long seq) {
+    const unsigned long long* src = reinterpret_cast<const unsigned long long*>(c);
+    unsigned long long* dst = reinterpret_cast<unsigned long long*>(h);
+    for (int i = threadIdx.x; i < (int)(sizeof(DevCounters) / 8); i += blockDim.x) dst[i] = __ldcg(src + i);
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) *flag = seq;
+}
+
 pmsz_status sync_counters(pmsz_plan* p, cudaStream_t s) {
+    static const bool by_kernel = !(getenv("PMSZ_SYNC_KERNEL") && atoi(getenv("PMSZ_SYNC_KERNEL")) == 0);
+    if (by_kernel && p->hflag) {
+        const unsigned long long seq = ++p->sync_seq;
+        k_publish<<<1, 64, 0, s>>>(p->ctr, p->hctr, p->hflag, seq);
+        CUDA_TRY(cudaGetLastError());
+        for (unsigned long long i = 1;; ++i) {
+            if (*p->hflag == seq) break;
+            if ((i & 4095) == 0) {   // a failed stream would never set the flag
+                const cudaError_t q = cudaStreamQuery(s);
+                if (q != cudaSuccess && q != cudaErrorNotReady) {
+                    cudaGetLastError();
+                    return fail(PMSZ_ERR_CUDA, std::string("CUDA: ") + cudaGetErrorString(q));
+                }
+                if (q == cudaSuccess && *p->hflag != seq) return fail(PMSZ_ERR_CUDA, "counter publish lost");
+            }
+        }
+        std::atomic_thread_fence(std::memory_order_acquire);
+        prof_flush(p);
+        return PMSZ_OK;
+    }
     CUDA_TRY(cudaMemcpyAsync(p->hctr, p->ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
     prof_flush(p);
@@ -1365,6 +1403,11 @@ pmsz_status pmsz_plan_create(const pmsz_desc* desc, pmsz_plan** out) {
     const int64_t hist_n = std::min<int64_t>(std::max<int64_t>(d.max_iterations, 1), 4096);
     p->hist_chunk = hist_n;
     if (ok) ok = alloc((void**)&p->tail, sizeof(TailState)) && alloc((void**)&p->thist, hist_n * 8);
+    if (ok) {
+        unsigned long long* fl = nullptr;
+        ok = cudaMallocHost((void**)&fl, 64) == cudaSuccess;
+        if (ok) { *fl = 0; p->hflag = fl; }
+    }
     if (ok) ok = cudaMallocHost((void**)&p->hctr, sizeof(DevCounters)) == cudaSuccess &&
                  cudaMallocHost((void**)&p->htail, sizeof(TailState)) == cudaSuccess &&
                  cudaMallocHost((void**)&p->hthist, hist_n * 8) == cudaSuccess;
@@ -1419,6 +1462,7 @@ void pmsz_plan_destroy(pmsz_plan* p) {
     cudaFree(p->w.actbits); cudaFree(p->w.act[0]); cudaFree(p->w.act[1]); cudaFree(p->w.iteredit);
     cudaFree(p->w.elist);
     if (p->hctr) cudaFreeHost(p->hctr);
+    if (p->hflag) cudaFreeHost((void*)p->hflag);
     cudaFree(p->tail); cudaFree(p->thist);
     if (p->htail) cudaFreeHost(p->htail);
     if (p->hthist) cudaFreeHost(p->hthist);
