@@ -162,6 +162,14 @@ pmsz_status pmsz_run_correction(pmsz_plan* plan, const void* f_dev, const double
                                 double* g_dev, int64_t* history_host, int64_t history_cap,
                                 pmsz_result* result, void* stream);
 
+/* pmsz_run_correction followed by pmsz_edits_export into device buffers of
+ * capacity cap (the first min(cap, count) edits) with no return to the caller
+ * in between; result->edit_count is the full count. */
+pmsz_status pmsz_run_correction_export(pmsz_plan* plan, const void* f_dev, const double* fhat_dev,
+                                       double* g_dev, int64_t* history_host, int64_t history_cap,
+                                       pmsz_result* result, int64_t* ids_dev, double* vals_dev,
+                                       int64_t cap, void* stream);
+
 /*
  * The same call with HOST buffers (the end-to-end drop-in): copies f and fhat
  * in, runs, and writes the corrected field and the edit set back to the host.

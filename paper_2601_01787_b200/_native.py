@@ -99,6 +99,7 @@ SIGNATURES = {
     "pmsz_profile": (i32, [vp, i32]),
     "pmsz_profile_read": (i32, [vp, dp, i64p, i32]),
     "pmsz_run_correction": (i32, [vp, vp, vp, vp, i64p, i64, ctypes.POINTER(PmszResult), vp]),
+    "pmsz_run_correction_export": (i32, [vp, vp, vp, vp, i64p, i64, ctypes.POINTER(PmszResult), vp, vp, i64, vp]),
     "pmsz_run_correction_host": (i32, [vp, vp, vp, vp, vp, vp, i64, i64p, i64,
                                        ctypes.POINTER(PmszResult), vp]),
     "pmsz_edits_export": (i32, [vp, vp, vp, vp, i64, i64p, vp]),

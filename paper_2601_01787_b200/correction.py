@@ -244,11 +244,12 @@ def run_correction_device(f: torch.Tensor, fhat: torch.Tensor, dims, config: Cor
                          f32_original=f32)
     g = out if out is not None else torch.empty_like(fhat)
     with plan.lock:
-        st, res, hist = plan.run(f, fhat, g, stream=stream)
-        raise_for(st, res, None, None, config.xi_abs, f_dev=f, fhat_dev=fhat)
         if export_edits:
-            ids, vals = plan.export_edits(g, stream=stream)
+            st, res, hist, ids, vals = plan.run_export(f, fhat, g, stream=stream)
+            raise_for(st, res, None, None, config.xi_abs, f_dev=f, fhat_dev=fhat)
         else:
+            st, res, hist = plan.run(f, fhat, g, stream=stream)
+            raise_for(st, res, None, None, config.xi_abs, f_dev=f, fhat_dev=fhat)
             ids = vals = torch.empty(0, device=g.device)
     return DeviceCorrection(corrected=g, edit_ids=ids, edit_values=vals,
                             iterations=int(res.iterations), edits_per_iteration=tuple(hist),

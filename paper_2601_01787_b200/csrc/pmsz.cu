@@ -1929,6 +1929,17 @@ pmsz_status pmsz_edits_export(pmsz_plan* p, const double* g, int64_t* ids, doubl
     return PMSZ_OK;
 }
 
+pmsz_status pmsz_run_correction_export(pmsz_plan* p, const void* f, const double* fh, double* g, int64_t* history,
+                                       int64_t history_cap, pmsz_result* r, int64_t* ids, double* vals, int64_t cap,
+                                       void* stream) {
+    pmsz_status st = pmsz_run_correction(p, f, fh, g, history, history_cap, r, stream);
+    if (st) return st;
+    int64_t count = 0;
+    st = pmsz_edits_export(p, g, ids, vals, cap, &count, stream);
+    if (st == PMSZ_OK && r) r->edit_count = count;
+    return st;
+}
+
 namespace {
 // Staging thread of a host run with pageable buffers (hoststage.h): per z-slab,
 // the f and fhat bytes go pageable -> pinned ring slot (all pool threads) ->

@@ -132,6 +132,31 @@ class DomainPlan:
             return st, res, [int(hist[i]) for i in range(n_hist)]
         return st, res, self.history()
 
+    def run_export(self, f: torch.Tensor, fhat: torch.Tensor, g: torch.Tensor, stream=None):
+        """pmsz_run_correction + the edit export in one C call (no host gap
+        before the export): the record lands in tensors sized by the last
+        run's count (+5 %); a larger record is exported again at its size.
+        Returns (status, PmszResult, history, ids, vals)."""
+        cap = min(self.max_iterations, self.HIST_BUF)
+        hist = (ctypes.c_int64 * cap)()
+        res = N.PmszResult()
+        ecap = getattr(self, "_ecap", 0)
+        ids = torch.empty(ecap, dtype=torch.int64, device=g.device)
+        vals = torch.empty(ecap, dtype=torch.float64, device=g.device)
+        st = self.lib.pmsz_run_correction_export(self.handle, N.ptr(f), N.ptr(fhat), N.ptr(g), hist, cap,
+                                                 ctypes.byref(res), N.ptr(ids) if ecap else None,
+                                                 N.ptr(vals) if ecap else None, ecap, N.stream_handle(stream))
+        n_hist = int(res.iterations)
+        history = [int(hist[i]) for i in range(n_hist)] if n_hist <= cap else self.history()
+        if st != N.PMSZ_OK:
+            return st, res, history, None, None
+        m = int(res.edit_count)
+        self._ecap = m + m // 20 + 1024
+        if m <= ecap:
+            return st, res, history, ids[:m], vals[:m]
+        ids, vals = self.export_edits(g, stream=stream)
+        return st, res, history, ids, vals
+
     def run_host(self, f: np.ndarray, fhat: np.ndarray, g: np.ndarray | None):
         """pmsz_run_correction_host on host arrays (pageable or pinned): f (f64,
         or f32 with f32_original; f64 with host_f64), fhat f64, g the f64
