@@ -495,8 +495,10 @@ struct SigArgs {
     unsigned long long* sums[PMSZ_MAX_RANKS];    // each rank's sum slots [2][world][4]
     unsigned long long* flags[PMSZ_MAX_RANKS];   // each rank's arrival epochs [world]
     unsigned long long v[4];
-    unsigned long long* out;                     // device: the 4 sums over ranks
+    unsigned long long* out;                     // the 4 sums over ranks (mapped pinned memory)
     unsigned long long epoch;
+    volatile unsigned long long* flag;           // then seq here (the host spins on it)
+    unsigned long long seq;
     int world, rank;
 };
 
@@ -525,6 +527,11 @@ __global__ void __launch_bounds__(PMSZ_MAX_RANKS) k_signal(SigArgs a) {
         unsigned long long t = 0;
         for (int r = 0; r < a.world; ++r) t += a.sums[a.rank][((size_t)par * a.world + r) * 4 + q];
         a.out[q] = t;
+    }
+    if (a.flag) {
+        __threadfence_system();
+        __syncthreads();
+        if (q == 0) *a.flag = a.seq;
     }
 }
 
@@ -722,24 +729,35 @@ __global__ void k_publish(const DevCounters* __restrict__ c, DevCounters* h, vol
     if (threadIdx.x == 0) *flag = seq;
 }
 
+bool sync_by_kernel() {
+    static const bool on = !(getenv("PMSZ_SYNC_KERNEL") && atoi(getenv("PMSZ_SYNC_KERNEL")) == 0);
+    return on;
+}
+
+// Spin until the stream's last kernel has written `seq` into the plan's flag.
+pmsz_status spin_flag(pmsz_plan* p, cudaStream_t s, unsigned long long seq) {
+    CUDA_TRY(cudaGetLastError());
+    for (unsigned long long i = 1;; ++i) {
+        if (*p->hflag == seq) break;
+        if ((i & 4095) == 0) {   // a failed stream would never set the flag
+            const cudaError_t q = cudaStreamQuery(s);
+            if (q != cudaSuccess && q != cudaErrorNotReady) {
+                cudaGetLastError();
+                return fail(PMSZ_ERR_CUDA, std::string("CUDA: ") + cudaGetErrorString(q));
+            }
+            if (q == cudaSuccess && *p->hflag != seq) return fail(PMSZ_ERR_CUDA, "counter publish lost");
+        }
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);
+    return PMSZ_OK;
+}
+
 pmsz_status sync_counters(pmsz_plan* p, cudaStream_t s) {
-    static const bool by_kernel = !(getenv("PMSZ_SYNC_KERNEL") && atoi(getenv("PMSZ_SYNC_KERNEL")) == 0);
-    if (by_kernel && p->hflag) {
+    if (sync_by_kernel() && p->hflag) {
         const unsigned long long seq = ++p->sync_seq;
         k_publish<<<1, 64, 0, s>>>(p->ctr, p->hctr, p->hflag, seq);
-        CUDA_TRY(cudaGetLastError());
-        for (unsigned long long i = 1;; ++i) {
-            if (*p->hflag == seq) break;
-            if ((i & 4095) == 0) {   // a failed stream would never set the flag
-                const cudaError_t q = cudaStreamQuery(s);
-                if (q != cudaSuccess && q != cudaErrorNotReady) {
-                    cudaGetLastError();
-                    return fail(PMSZ_ERR_CUDA, std::string("CUDA: ") + cudaGetErrorString(q));
-                }
-                if (q == cudaSuccess && *p->hflag != seq) return fail(PMSZ_ERR_CUDA, "counter publish lost");
-            }
-        }
-        std::atomic_thread_fence(std::memory_order_acquire);
+        const pmsz_status st = spin_flag(p, s, seq);
+        if (st) return st;
         prof_flush(p);
         return PMSZ_OK;
     }
@@ -1692,10 +1710,18 @@ static pmsz_status rounds_signal(pmsz_plan* p, pmsz_rounds_desc* rd, const unsig
         a.flags[r] = (unsigned long long*)rd->bufs[r] + rd->flags_off;
     }
     for (int k = 0; k < 4; ++k) a.v[k] = v[k];
-    a.out = p->dsig;
     a.epoch = ++rd->epoch;
     a.world = rd->world;
     a.rank = rd->rank;
+    if (sync_by_kernel() && p->hflag) {   // sums straight into the pinned mirror, then the flag
+        a.out = p->hsig;
+        a.flag = p->hflag;
+        a.seq = ++p->sync_seq;
+        k_signal<<<1, PMSZ_MAX_RANKS, 0, s>>>(a);
+        LAUNCHED();
+        return spin_flag(p, s, a.seq);
+    }
+    a.out = p->dsig;
     k_signal<<<1, PMSZ_MAX_RANKS, 0, s>>>(a);
     LAUNCHED();
     CUDA_TRY(cudaMemcpyAsync(p->hsig, p->dsig, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
