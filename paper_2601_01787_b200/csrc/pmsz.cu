@@ -719,11 +719,20 @@ struct ProfScope {
 // the ~5 host decisions of a run (each cost the device ~25 us idle).  The
 // kernel is the last operation of the stream, so the flag also means every
 // earlier operation has completed.
+// (tail: also the tail state and its per-iteration edit counts, k words of
+// them where k = the state's iteration count, capped at hist_cap)
 __global__ void k_publish(const DevCounters* __restrict__ c, DevCounters* h, volatile unsigned long long* flag,
-                          unsigned long long seq) {
+                          unsigned long long seq, const unsigned long long* __restrict__ ts, unsigned long long* hts,
+                          int ts_words, const unsigned long long* __restrict__ hist, unsigned long long* hhist,
+                          long long hist_cap) {
     const unsigned long long* src = reinterpret_cast<const unsigned long long*>(c);
     unsigned long long* dst = reinterpret_cast<unsigned long long*>(h);
     for (int i = threadIdx.x; i < (int)(sizeof(DevCounters) / 8); i += blockDim.x) dst[i] = __ldcg(src + i);
+    if (ts) {
+        for (int i = threadIdx.x; i < ts_words; i += blockDim.x) hts[i] = __ldcg(ts + i);
+        const long long k = min((long long)__ldcg(ts), hist_cap);   // TailState::iterations
+        for (long long i = threadIdx.x; i < k; i += blockDim.x) hhist[i] = __ldcg(hist + i);
+    }
     __threadfence_system();
     __syncthreads();
     if (threadIdx.x == 0) *flag = seq;
@@ -755,7 +764,7 @@ pmsz_status spin_flag(pmsz_plan* p, cudaStream_t s, unsigned long long seq) {
 pmsz_status sync_counters(pmsz_plan* p, cudaStream_t s) {
     if (sync_by_kernel() && p->hflag) {
         const unsigned long long seq = ++p->sync_seq;
-        k_publish<<<1, 64, 0, s>>>(p->ctr, p->hctr, p->hflag, seq);
+        k_publish<<<1, 64, 0, s>>>(p->ctr, p->hctr, p->hflag, seq, nullptr, nullptr, 0, nullptr, nullptr, 0);
         const pmsz_status st = spin_flag(p, s, seq);
         if (st) return st;
         prof_flush(p);
@@ -1097,10 +1106,20 @@ pmsz_status tail_step(pmsz_plan* p, const void* f, double* g, cudaStream_t s, lo
         launch_bits_total(p, p->w.detbits, &p->ctr->scratch[1], s);
         launch_bits_total(p, p->w.editbits, &p->ctr->scratch[2], s);
     }
-    CUDA_TRY(cudaMemcpyAsync(p->htail, p->tail, sizeof(TailState), cudaMemcpyDeviceToHost, s));
-    CUDA_TRY(cudaMemcpyAsync(p->hthist, p->thist, sizeof(unsigned long long) * budget, cudaMemcpyDeviceToHost, s));
-    st = sync_counters(p, s);
-    if (st) return st;
+    if (sync_by_kernel() && p->hflag) {   // state + history + counters in one publish
+        const unsigned long long seq = ++p->sync_seq;
+        k_publish<<<1, 128, 0, s>>>(p->ctr, p->hctr, p->hflag, seq, (const unsigned long long*)p->tail,
+                                    (unsigned long long*)p->htail, (int)(sizeof(TailState) / 8), p->thist, p->hthist,
+                                    budget);
+        st = spin_flag(p, s, seq);
+        if (st) return st;
+        prof_flush(p);
+    } else {
+        CUDA_TRY(cudaMemcpyAsync(p->htail, p->tail, sizeof(TailState), cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaMemcpyAsync(p->hthist, p->thist, sizeof(unsigned long long) * budget, cudaMemcpyDeviceToHost, s));
+        st = sync_counters(p, s);
+        if (st) return st;
+    }
     const TailState& ts = *p->htail;
     if (totals && ts.exit == kTailConverged) {
         p->totals_ready = true;
