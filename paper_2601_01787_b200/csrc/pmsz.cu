@@ -748,6 +748,10 @@ pmsz_status spin_flag(pmsz_plan* p, cudaStream_t s, unsigned long long seq) {
     CUDA_TRY(cudaGetLastError());
     for (unsigned long long i = 1;; ++i) {
         if (*p->hflag == seq) break;
+        // short waits spin; long ones (a host run's K0 waiting for its input)
+        // yield the core to the staging threads
+        if (i < 4096) _mm_pause();
+        else std::this_thread::yield();
         if ((i & 4095) == 0) {   // a failed stream would never set the flag
             const cudaError_t q = cudaStreamQuery(s);
             if (q != cudaSuccess && q != cudaErrorNotReady) {
