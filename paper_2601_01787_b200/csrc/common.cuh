@@ -15,8 +15,36 @@
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <cstdlib>
 
 namespace pmsz {
+
+// Programmatic dependent launch (sm_90+): a kernel of the loop is launched
+// with programmatic stream serialisation, so its launch is processed while
+// the previous kernel drains; every such kernel waits here, first thing,
+// until the previous grid has completed and its writes are visible (a no-op
+// when it was launched the ordinary way).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline void pdl_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+    static const bool on = !(getenv("PMSZ_PDL") && atoi(getenv("PMSZ_PDL")) == 0);
+    if (!on) {
+        kern<<<grid, block, smem, s>>>(args...);
+        return;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
 
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per call site and
 // device (it is per device, and a host call per launch costs the launch

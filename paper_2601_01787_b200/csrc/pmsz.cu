@@ -194,6 +194,7 @@ __device__ __forceinline__ unsigned block_exclusive_scan(unsigned v, unsigned* w
 __global__ void __launch_bounds__(kCompactThreads) k_chunk_count_scan(const uint32_t* __restrict__ bits, Chunks c,
                                                                       unsigned long long* counts,
                                                                       unsigned long long* total, unsigned* done) {
+    pdl_wait();   // (programmatic dependent launch)
     __shared__ unsigned long long ws[kCompactThreads / 32];
     __shared__ bool last;
     const int64_t w0 = (int64_t)blockIdx.x * c.chunk, w1 = min(w0 + c.chunk, c.nwords);
@@ -308,6 +309,7 @@ template <typename IdT>
 __global__ void __launch_bounds__(kCompactThreads) k_chunk_list(uint32_t* __restrict__ bits, Chunks c,
                                                                 const unsigned long long* __restrict__ offs,
                                                                 IdT* __restrict__ list, int clear) {
+    pdl_wait();   // (programmatic dependent launch)
     __shared__ unsigned wt[kCompactThreads / 32];
     __shared__ uint32_t stage[kStageIds];
     const int64_t w0 = (int64_t)blockIdx.x * c.chunk, w1 = min(w0 + c.chunk, c.nwords);
@@ -335,6 +337,7 @@ __global__ void __launch_bounds__(kCompactThreads) k_chunk_write(const uint32_t*
                                                                  int64_t n, const unsigned long long* __restrict__ offs,
                                                                  const double* __restrict__ g, int64_t* ids,
                                                                  double* vals, int64_t cap) {
+    pdl_wait();   // (programmatic dependent launch)
     __shared__ unsigned wt[kCompactThreads / 32];
     __shared__ uint32_t stage[kStageIds];
     const int64_t w0 = (int64_t)blockIdx.x * c.chunk, w1 = min(w0 + c.chunk, c.nwords);
@@ -725,6 +728,7 @@ __global__ void k_publish(const DevCounters* __restrict__ c, DevCounters* h, vol
                           unsigned long long seq, const unsigned long long* __restrict__ ts, unsigned long long* hts,
                           int ts_words, const unsigned long long* __restrict__ hist, unsigned long long* hhist,
                           long long hist_cap) {
+    pdl_wait();   // (programmatic dependent launch)
     const unsigned long long* src = reinterpret_cast<const unsigned long long*>(c);
     unsigned long long* dst = reinterpret_cast<unsigned long long*>(h);
     for (int i = threadIdx.x; i < (int)(sizeof(DevCounters) / 8); i += blockDim.x) dst[i] = __ldcg(src + i);
@@ -768,7 +772,8 @@ pmsz_status spin_flag(pmsz_plan* p, cudaStream_t s, unsigned long long seq) {
 pmsz_status sync_counters(pmsz_plan* p, cudaStream_t s) {
     if (sync_by_kernel() && p->hflag) {
         const unsigned long long seq = ++p->sync_seq;
-        k_publish<<<1, 64, 0, s>>>(p->ctr, p->hctr, p->hflag, seq, nullptr, nullptr, 0, nullptr, nullptr, 0);
+        pdl_launch(k_publish, 1, 64, 0, s, p->ctr, p->hctr, p->hflag, seq, (const unsigned long long*)nullptr,
+                   (unsigned long long*)nullptr, 0, (const unsigned long long*)nullptr, (unsigned long long*)nullptr, 0LL);
         const pmsz_status st = spin_flag(p, s, seq);
         if (st) return st;
         prof_flush(p);
@@ -791,8 +796,8 @@ pmsz_status reset_iter(pmsz_plan* p, cudaStream_t s, int nxt) {
 // lands in *dst on the device.
 void launch_bits_total(pmsz_plan* p, const uint32_t* bits, unsigned long long* dst, cudaStream_t s) {
     p->offsets_of = bits;
-    k_chunk_count_scan<<<(unsigned)p->ch.n, kCompactThreads, 0, s>>>(bits, p->ch, p->block_counts, dst,
-                                                                     (unsigned*)(p->block_counts + kMaxChunks));
+    pdl_launch(k_chunk_count_scan, (unsigned)p->ch.n, kCompactThreads, 0, s, bits, p->ch, p->block_counts, dst,
+               (unsigned*)(p->block_counts + kMaxChunks));
     LAUNCHED();
 }
 
@@ -804,8 +809,8 @@ int sort_pending(pmsz_plan* p, cudaStream_t s) {
     p->bits_only = false;
     ProfScope ps(p, s, PMSZ_K_COMPACT);
     launch_bits_total(p, p->w.actbits, &p->ctr->nact[p->cur], s);
-    k_chunk_list<uint32_t><<<(unsigned)p->ch.n, kCompactThreads, 0, s>>>(p->w.actbits, p->ch, p->block_counts,
-                                                                      p->w.act[p->cur], 1);
+    pdl_launch(k_chunk_list<uint32_t>, (unsigned)p->ch.n, kCompactThreads, 0, s, p->w.actbits, p->ch,
+               (const unsigned long long*)p->block_counts, p->w.act[p->cur], 1);
     LAUNCHED();
     return 1;
 }
@@ -817,8 +822,8 @@ pmsz_status launch_apply(pmsz_plan* p, const void* f, double* g, cudaStream_t s,
         // touched bitmap -> ascending target list (load-balanced apply)
         ProfScope ps(p, s, PMSZ_K_COMPACT);
         launch_bits_total(p, p->w.touched, &p->ctr->nwork, s);
-        k_chunk_list<uint32_t><<<(unsigned)p->ch.n, kCompactThreads, 0, s>>>(p->w.touched, p->ch, p->block_counts,
-                                                                      p->w.work, 1);
+        pdl_launch(k_chunk_list<uint32_t>, (unsigned)p->ch.n, kCompactThreads, 0, s, p->w.touched, p->ch,
+                   (const unsigned long long*)p->block_counts, p->w.work, 1);
         LAUNCHED();
     }
     ProfScope ps(p, s, PMSZ_K_APPLY);
@@ -827,11 +832,11 @@ pmsz_status launch_apply(pmsz_plan* p, const void* f, double* g, cudaStream_t s,
     static const int apply_per_sm = getenv("PMSZ_APPLY_PER_SM") ? atoi(getenv("PMSZ_APPLY_PER_SM")) : 1;
     Work w = p->w;
     w.first_apply = p->iterations == 0 ? 1 : 0;   // nothing edited yet: no counts / editbits reads
-    k_apply_list<FT><<<grid_for(bound, 256, apply_per_sm), 256, 0, s>>>(p->dom, (const FT*)f, g, w, nxt);
+    pdl_launch(k_apply_list<FT>, grid_for(bound, 256, apply_per_sm), 256, 0, s, p->dom, (const FT*)f, g, w, nxt);
     LAUNCHED();
     if (p->w.incremental) {   // list-mode ring marking (no-op when the edits went to the bitmap)
-        k_mark_list<<<grid_for(std::min<int64_t>(15 * bound, (int64_t)p->w.mark_limit), 256, 4), 256, 0, s>>>(
-            p->dom, p->w, nxt, (unsigned long long)p->sort_min);
+        pdl_launch(k_mark_list, grid_for(std::min<int64_t>(15 * bound, (int64_t)p->w.mark_limit), 256, 4), 256, 0, s,
+                   p->dom, p->w, nxt, (unsigned long long)p->sort_min);
         LAUNCHED();
     }
     return PMSZ_OK;
@@ -922,8 +927,8 @@ pmsz_status iterate_once(pmsz_plan* p, const void* f, double* g, cudaStream_t s)
             {
                 ProfScope ps(p, s, PMSZ_K_COMPACT);
                 launch_bits_total(p, p->w.actbits, &p->ctr->ndefer, s);
-                k_chunk_list<uint32_t><<<(unsigned)p->ch.n, kCompactThreads, 0, s>>>(p->w.actbits, p->ch, p->block_counts,
-                                                                      p->w.work, 1);
+                pdl_launch(k_chunk_list<uint32_t>, (unsigned)p->ch.n, kCompactThreads, 0, s, p->w.actbits, p->ch,
+                           (const unsigned long long*)p->block_counts, p->w.work, 1);
                 LAUNCHED();
             }
             if (nonempty) {
@@ -933,7 +938,8 @@ pmsz_status iterate_once(pmsz_plan* p, const void* f, double* g, cudaStream_t s)
                 // (0.12 vs 0.25 ms at 512^3); PMSZ_LIST_SWEEP=0 selects k_gather
                 static const int list_per_sm = getenv("PMSZ_LIST_SWEEP") ? atoi(getenv("PMSZ_LIST_SWEEP")) : 4;
                 if (list_per_sm > 0)
-                    k_sweep_list<<<num_sms() * list_per_sm, 256, 0, s>>>(d, g, p->w, p->w.work, &p->ctr->ndefer);
+                    pdl_launch(k_sweep_list, num_sms() * list_per_sm, 256, 0, s, d, g, p->w,
+                               (const uint32_t*)p->w.work, (const unsigned long long*)&p->ctr->ndefer);
                 else
                     k_gather<false><<<num_sms() * 2, kGWarps * 32, kGatherSmem, s>>>(d, g, p->w, p->w.work,
                                                                                      &p->ctr->ndefer);
@@ -954,14 +960,14 @@ pmsz_status iterate_once(pmsz_plan* p, const void* f, double* g, cudaStream_t s)
         {
             ProfScope ps(p, s, PMSZ_K_COMPACT);
             launch_bits_total(p, p->w.detbits, &p->ctr->ndefer, s);
-            k_chunk_list<uint32_t><<<(unsigned)p->ch.n, kCompactThreads, 0, s>>>(p->w.detbits, p->ch, p->block_counts,
-                                                                      p->w.work, 0);
+            pdl_launch(k_chunk_list<uint32_t>, (unsigned)p->ch.n, kCompactThreads, 0, s, p->w.detbits, p->ch,
+                       (const unsigned long long*)p->block_counts, p->w.work, 0);
             LAUNCHED();
         }
         ProfScope ps(p, s, PMSZ_K_DEFER);
         // two CTAs per SM measured best (the same L2-window effect as the apply)
         static const int defer_per_sm = getenv("PMSZ_DEFER_PER_SM") ? atoi(getenv("PMSZ_DEFER_PER_SM")) : 2;
-        k_defer<<<grid_for(p->n, 256, defer_per_sm), 256, 0, s>>>(d, g, p->w);
+        pdl_launch(k_defer, grid_for(p->n, 256, defer_per_sm), 256, 0, s, d, g, p->w);
         LAUNCHED();
     }
     if (mode == kList) {
@@ -1970,7 +1976,8 @@ pmsz_status pmsz_edits_export(pmsz_plan* p, const double* g, int64_t* ids, doubl
     if (count_out) *count_out = count;
     if (ids && vals && cap > 0 && count > 0) {
         ProfScope ps(p, s, PMSZ_K_COMPACT);
-        k_chunk_write<<<(unsigned)p->ch.n, kCompactThreads, 0, s>>>(p->w.editbits, p->ch, p->n, p->block_counts, g, ids,
+        pdl_launch(k_chunk_write, (unsigned)p->ch.n, kCompactThreads, 0, s, (const uint32_t*)p->w.editbits, p->ch, p->n,
+                   (const unsigned long long*)p->block_counts, g, ids,
                                                                    vals, cap);
         LAUNCHED();
         CUDA_TRY(cudaGetLastError());

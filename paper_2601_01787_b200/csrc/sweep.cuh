@@ -185,6 +185,7 @@ __device__ __forceinline__ void rules(const Dom& d, const Work& w, const Scan& s
 // Rule evaluation of the centres a tiled sweep found mismatching (their ids are
 // in w.work[0 .. ndefer)); one thread per centre, neighbours gathered from g.
 __global__ void __launch_bounds__(256) k_defer(Dom d, const double* __restrict__ g, Work w) {
+    pdl_wait();   // (programmatic dependent launch)
     const unsigned long long n = w.ctr->ndefer;
     for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (unsigned long long)gridDim.x * blockDim.x) {
@@ -241,6 +242,7 @@ __device__ __forceinline__ void sweep_sparse_range(const Dom& d, const double* _
 __global__ void __launch_bounds__(256) k_sweep_list(Dom d, const double* __restrict__ g, Work w,
                                                     const uint32_t* __restrict__ list,
                                                     const unsigned long long* __restrict__ count) {
+    pdl_wait();   // (programmatic dependent launch)
     const unsigned long long n = *count;
     unsigned ndet = 0;
     for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -434,6 +436,7 @@ __device__ __forceinline__ void apply_range(const Dom& d, const FT* __restrict__
 template <typename FT>
 __global__ void __launch_bounds__(256) k_apply_list(Dom d, const FT* __restrict__ f, double* __restrict__ g,
                                                     Work w, int nxt) {
+    pdl_wait();   // (programmatic dependent launch)
     const int mark = apply_marks(w);
     apply_range<8>(d, f, g, w, nxt, mark, (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x,
                 (unsigned long long)gridDim.x * blockDim.x);
@@ -474,6 +477,7 @@ __device__ __forceinline__ void mark_list_range(const Dom& d, const Work& w, int
 }
 
 __global__ void __launch_bounds__(256) k_mark_list(Dom d, Work w, int nxt, unsigned long long list_limit) {
+    pdl_wait();   // (programmatic dependent launch)
     mark_list_range(d, w, nxt, mark_appends(w, list_limit), (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x,
                     (unsigned long long)gridDim.x * blockDim.x);
 }
