@@ -975,7 +975,7 @@ pmsz_status iterate_once(pmsz_plan* p, const void* f, double* g, cudaStream_t s)
         ProfScope ps(p, s, PMSZ_K_SWEEP_SPARSE);
         p->w.track = 1;
         const int64_t m = std::min<int64_t>(p->pending, (int64_t)p->w.act_cap);
-        k_sweep_sparse<<<grid_for(m, 256, 8), 256, 0, s>>>(d, g, p->w, p->cur, sorted);
+        pdl_launch(k_sweep_sparse, grid_for(m, 256, 8), 256, 0, s, d, g, p->w, p->cur, sorted);
         LAUNCHED();
         apply_bound = std::min<int64_t>(p->n, 15 * m + 32);
     }
@@ -1172,6 +1172,7 @@ struct ZeroList {
     int k;
 };
 __global__ void __launch_bounds__(256) k_zero_many(ZeroList z, DevCounters* ctr) {
+    pdl_wait();   // (programmatic dependent launch)
     const unsigned long long t = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
     const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
     if (t == 0) {
@@ -1203,7 +1204,7 @@ pmsz_status reset_run_state(pmsz_plan* p, cudaStream_t s, uint32_t* extra0 = nul
     }
     add(extra0, p->nwords * 4);   // (prep: the fragile and detection bitmaps)
     add(extra1, p->nwords * 4);
-    k_zero_many<<<num_sms() * 4, 256, 0, s>>>(z, p->ctr);
+    pdl_launch(k_zero_many, num_sms() * 4, 256, 0, s, z, p->ctr);
     LAUNCHED();
     CUDA_TRY(cudaGetLastError());
     p->cur = 0;
@@ -1244,9 +1245,9 @@ pmsz_status prep(pmsz_plan* p, const void* f, const double* fh, double* g, cudaS
                 if (p->feed && !p->feed->wait((int)j + 1)) break;   // staged on the host: enqueued yet?
                 CUDA_TRY(cudaStreamWaitEvent(s, p->stage_ev[1 + j], 0));
                 queued = p->f32 ? launch_prep_q<float>(p->dom, (const float*)f, fh, g, p->w.code, p->frag_out(), p->ctr,
-                                                       det, s, p->stage_z[c], p->stage_z[c + 1])
+                                                       det, s, p->stage_z[c], p->stage_z[c + 1], false)
                                 : launch_prep_q<double>(p->dom, (const double*)f, fh, g, p->w.code, p->frag_out(),
-                                                        p->ctr, det, s, p->stage_z[c], p->stage_z[c + 1]);
+                                                        p->ctr, det, s, p->stage_z[c], p->stage_z[c + 1], false);
                 if (!queued) break;   // no tensor map for this field: nothing was launched
                 if (c + 1 < nsl) LAUNCHED();
             }

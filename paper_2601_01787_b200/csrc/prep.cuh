@@ -191,6 +191,7 @@ struct PrepArgs {
 template <typename FT, bool kScreen, bool kDetect>
 __global__ void __launch_bounds__(256, sizeof(FT) == 4 ? PMSZ_PREP_MINB : 2) k_prep_q(Dom d, const __grid_constant__ CUtensorMap tf,
                                                    const __grid_constant__ CUtensorMap th, PrepArgs a, int zchunk) {
+    pdl_wait();   // (programmatic dependent launch)
     using G = PrepGeo<FT>;
     extern __shared__ __align__(1024) unsigned char praw[];
     PrepSmem<FT>& S = *reinterpret_cast<PrepSmem<FT>*>(praw);
@@ -432,7 +433,8 @@ __global__ void __launch_bounds__(256, sizeof(FT) == 4 ? PMSZ_PREP_MINB : 2) k_p
 // the shared-fold K0 of tiles.cuh).
 template <typename FT>
 inline bool launch_prep_q(const Dom& d, const FT* f, const double* fh, double* g, uint8_t* code, uint32_t* frag,
-                          DevCounters* ctr, uint32_t* det, cudaStream_t s, int64_t z0 = 0, int64_t z1 = -1) {
+                          DevCounters* ctr, uint32_t* det, cudaStream_t s, int64_t z0 = 0, int64_t z1 = -1,
+                          bool pdl = true) {
     if (z1 < 0) z1 = d.nz;
     using G = PrepGeo<FT>;
     CUtensorMap tf, th;
@@ -479,7 +481,10 @@ inline bool launch_prep_q(const Dom& d, const FT* f, const double* fh, double* g
     {                                                                             \
         static unsigned long long attr = 0;                                      \
         smem_attr_once(k_prep_q<FT, R, D>, (int)smem, attr);                     \
-        k_prep_q<FT, R, D><<<grid, block, smem, s>>>(all, tf, th, a, zchunk);    \
+        if (pdl)   /* (the slab launches wait on copy events: ordinary launches) */             \
+            pdl_launch(k_prep_q<FT, R, D>, grid, block, smem, s, all, tf, th, a, zchunk);         \
+        else                                                                                       \
+            k_prep_q<FT, R, D><<<grid, block, smem, s>>>(all, tf, th, a, zchunk);                 \
     }
     if (frag && det) { PMSZ_LAUNCH_PREP(true, true); }
     else if (frag) { PMSZ_LAUNCH_PREP(true, false); }

@@ -90,6 +90,7 @@ __global__ void __launch_bounds__(kQThreads, PMSZ_QMINB) k_qsweep_tma(Dom d, con
                                                              const __grid_constant__ CUtensorMap tmc,
                                                              const __grid_constant__ CUtensorMap tmd,
                                                              DetectOp<kCount, kMasked, kExtrema> op, int zchunk) {
+    pdl_wait();   // (programmatic dependent launch)
     using Op = DetectOp<kCount, kMasked, kExtrema>;
     extern __shared__ __align__(1024) unsigned char qraw[];   // TMA destinations: 128-B aligned slots
     QSmem& S = *reinterpret_cast<QSmem*>(qraw);
@@ -255,7 +256,7 @@ inline bool launch_qsweep(const Dom& d, const double* g, const Work& w, cudaStre
     auto kern = k_qsweep_tma<kCount, kMasked, kExtrema>;
     static unsigned long long attr = 0;
     smem_attr_once(kern, (int)kQSmemBytes, attr);
-    kern<<<grid, block, kQSmemBytes, s>>>(d, tm, tmc, tmd, op, zchunk);
+    pdl_launch(kern, grid, block, kQSmemBytes, s, d, tm, tmc, tmd, op, zchunk);
     return true;
 }
 

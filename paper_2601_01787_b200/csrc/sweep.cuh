@@ -272,6 +272,7 @@ __global__ void __launch_bounds__(256) k_sweep_list(Dom d, const double* __restr
 
 __global__ void __launch_bounds__(256) k_sweep_sparse(Dom d, const double* __restrict__ g, Work w, int cur,
                                                      int sorted) {
+    pdl_wait();   // (programmatic dependent launch)
     sweep_sparse_range(d, g, w, cur, sorted != 0, (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x,
                        (unsigned long long)gridDim.x * blockDim.x);
 }
