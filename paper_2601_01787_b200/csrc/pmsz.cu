@@ -376,6 +376,7 @@ __device__ __forceinline__ int64_t box_off(const Box& b, int64_t i) {
 }
 
 __global__ void __launch_bounds__(256) k_box_pack(Box b, const double* __restrict__ src, double* __restrict__ buf) {
+    pdl_wait();   // (programmatic dependent launch)
     const int64_t n = b.ext[0] * b.ext[1] * b.ext[2];
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -411,6 +412,7 @@ __device__ __forceinline__ void mark_changed(const Dom& d, const Work& w, int64_
 
 __global__ void __launch_bounds__(256) k_box_mark(Dom d, Work w, Box b, const double* __restrict__ before,
                                                   const double* __restrict__ g, int cur, int bits) {
+    pdl_wait();   // (programmatic dependent launch)
     const int64_t n = b.ext[0] * b.ext[1] * b.ext[2];
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -424,6 +426,7 @@ __global__ void __launch_bounds__(256) k_box_mark(Dom d, Work w, Box b, const do
 __global__ void __launch_bounds__(256) k_box_merge(Dom d, Work w, Box b, double* __restrict__ g,
                                                    const double* __restrict__ buf, int cur, int mode,
                                                    unsigned long long* changed) {
+    pdl_wait();   // (programmatic dependent launch)
     const int64_t n = b.ext[0] * b.ext[1] * b.ext[2];
     unsigned mine = 0;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -443,6 +446,7 @@ __global__ void __launch_bounds__(256) k_box_merge(Dom d, Work w, Box b, double*
 
 __global__ void __launch_bounds__(256) k_mark_ids(Dom d, Work w, const uint32_t* __restrict__ ids, int64_t n, int cur,
                                                   int bits) {
+    pdl_wait();   // (programmatic dependent launch)
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
         mark_changed(d, w, ids[i], cur, bits);
@@ -517,6 +521,7 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
 // Thread q publishes this rank's values into rank q's slot of this epoch's
 // parity and raises this rank's epoch there; then waits for q's epoch here.
 __global__ void __launch_bounds__(PMSZ_MAX_RANKS) k_signal(SigArgs a) {
+    pdl_wait();   // (programmatic dependent launch)
     const int q = threadIdx.x;
     const int par = (int)(a.epoch & 1);
     if (q < a.world) {
@@ -1071,8 +1076,8 @@ pmsz_status launch_tail1(pmsz_plan* p, const void* f, double* g, cudaStream_t s,
         tr = trace_buf;
         CUDA_TRY(cudaMemsetAsync(tr, 0, 2 * 8 * 4096, s));
     }
-    k_tail1<FT><<<1, kT1Threads, kT1SmemBytes, s>>>(p->dom, (const FT*)f, g, p->w, p->cur, budget, p->thist, p->tail, tr,
-                                                     chained);
+    pdl_launch(k_tail1<FT>, 1, kT1Threads, kT1SmemBytes, s, p->dom, (const FT*)f, g, p->w, p->cur, budget, p->thist,
+               p->tail, tr, chained);
     LAUNCHED();
     if (trace) {
         std::vector<unsigned long long> h2(2 * 4096);
@@ -1675,8 +1680,8 @@ pmsz_status pmsz_mark_dirty_ids(pmsz_plan* p, const uint32_t* ids, int64_t count
     drop_k0(p, S(stream));   // g may change before the first iteration: K0's detections are stale
     if (!p->w.incremental || p->next_mode == kFull || count <= 0) return PMSZ_OK;
     cudaStream_t s = S(stream);
-    k_mark_ids<<<grid_for(count, 256), 256, 0, s>>>(p->dom, p->w, ids, count, p->cur,
-                                                   p->next_mode == kMasked || p->next_mode == kMaskedQ);
+    pdl_launch(k_mark_ids, grid_for(count, 256), 256, 0, s, p->dom, p->w, ids, count, p->cur,
+               p->next_mode == kMasked || p->next_mode == kMaskedQ);
     LAUNCHED();
     return after_mark(p, s);
 }
@@ -1692,8 +1697,8 @@ pmsz_status pmsz_box_mark_changed(pmsz_plan* p, const int64_t lo[3], const int64
     b.mx = div_magic((uint64_t)b.ext[0]);
     const int64_t n = b.ext[0] * b.ext[1] * b.ext[2];
     if (n <= 0) return PMSZ_OK;
-    k_box_mark<<<grid_for(n, 256), 256, 0, s>>>(p->dom, p->w, b, before, g, p->cur,
-                                                p->next_mode == kMasked || p->next_mode == kMaskedQ);
+    pdl_launch(k_box_mark, grid_for(n, 256), 256, 0, s, p->dom, p->w, b, before, g, p->cur,
+               p->next_mode == kMasked || p->next_mode == kMaskedQ);
     LAUNCHED();
     return after_mark(p, s);
 }
@@ -1718,7 +1723,7 @@ pmsz_status pmsz_box_merge_min(pmsz_plan* p, double* g, const int64_t lo[3], con
                          : ((p->next_mode == kMasked || p->next_mode == kMaskedQ) ? 1
                             : ((p->next_mode == kList || p->next_mode == kMaskedList) ? 2 : 0));
         ProfScope ps(p, s, PMSZ_K_OTHER);
-        k_box_merge<<<grid_for(n, 256), 256, 0, s>>>(p->dom, p->w, b, g, buf, p->cur, mode, &p->ctr->changed);
+        pdl_launch(k_box_merge, grid_for(n, 256), 256, 0, s, p->dom, p->w, b, g, buf, p->cur, mode, &p->ctr->changed);
         LAUNCHED();
     }
     if (!changed_out) {   // the counters are read at the next iteration
@@ -1747,7 +1752,7 @@ static pmsz_status rounds_signal(pmsz_plan* p, pmsz_rounds_desc* rd, const unsig
         a.out = p->hsig;
         a.flag = p->hflag;
         a.seq = ++p->sync_seq;
-        k_signal<<<1, PMSZ_MAX_RANKS, 0, s>>>(a);
+        pdl_launch(k_signal, 1, PMSZ_MAX_RANKS, 0, s, a);
         LAUNCHED();
         return spin_flag(p, s, a.seq);
     }
@@ -1791,7 +1796,7 @@ pmsz_status pmsz_rounds(pmsz_plan* p, const void* f, double* g, pmsz_rounds_desc
             const Box& b = boxes[x];
             const int64_t n = b.ext[0] * b.ext[1] * b.ext[2];
             if (n == 0) continue;
-            k_box_pack<<<grid_for(n, 256), 256, 0, s>>>(b, g, mine + rd->ex_off[x]);
+            pdl_launch(k_box_pack, grid_for(n, 256), 256, 0, s, b, (const double*)g, mine + rd->ex_off[x]);
             LAUNCHED();
         }
         const unsigned long long v[4] = {(unsigned long long)e, rr.shared_dirty ? 1ull : 0ull, 0ull, 0ull};

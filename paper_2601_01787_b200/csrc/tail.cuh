@@ -401,6 +401,7 @@ __global__ void __launch_bounds__(kT1Threads, 1) k_tail1(Dom d, const FT* __rest
                                                          long long budget, unsigned long long* __restrict__ hist,
                                                          TailState* ts, unsigned long long* __restrict__ trace,
                                                          int chained) {
+    pdl_wait();   // (programmatic dependent launch)
     extern __shared__ __align__(16) unsigned char t1raw[];
     T1Smem& S = *reinterpret_cast<T1Smem*>(t1raw);
     const int tid = threadIdx.x;
