@@ -94,6 +94,23 @@ __device__ __forceinline__ bool robust2_narrowed(const T2<float>& a, float thr32
     return a.sx < __fsub_rd(__fsub_rd(a.mx, thr32), sx) && a.sn > __fadd_ru(__fadd_ru(a.mn, thr32), sn);
 }
 
+// Extrema-only mode compares the extremum flags alone, so a side
+// is also robust when the centre c trails the ring's largest (smallest)
+// member by more than 2 xi: c can then never be the maximum (minimum) for any
+// g in [f - xi, f + xi].  Per side: the ordinary lead test OR that one.
+__device__ __forceinline__ bool robust_extrema(const T2<float>& a, float fc, float thr) {
+    const float hi = __fsub_rd(a.mx, thr), lo = __fadd_ru(a.mn, thr);
+    return fminf(a.sx, fc) < hi && fmaxf(a.sn, fc) > lo;
+}
+// (f64 fields screened in f32: the slack of robust2_narrowed, over c too)
+__device__ __forceinline__ bool robust_extrema_narrowed(const T2<float>& a, float fc, float thr32) {
+    const float afc = fabsf(fc);
+    const float sx = __fadd_ru(__fmul_ru(0x1p-22f, fmaxf(fmaxf(fabsf(a.mx), fabsf(a.sx)), afc)), 0x1p-120f);
+    const float sn = __fadd_ru(__fmul_ru(0x1p-22f, fmaxf(fmaxf(fabsf(a.mn), fabsf(a.sn)), afc)), 0x1p-120f);
+    return fminf(a.sx, fc) < __fsub_rd(__fsub_rd(a.mx, thr32), sx) &&
+           fmaxf(a.sn, fc) > __fadd_ru(__fadd_ru(a.mn, thr32), sn);
+}
+
 // Exact f-code of a queued centre (fold_scan / tree_scan on V values; NaN =
 // outside the field, only in the fold).
 template <typename V>
@@ -188,7 +205,7 @@ struct PrepArgs {
     int z0, z1;         // centre planes of this launch (z-slab launches overlap the input copy)
 };
 
-template <typename FT, bool kScreen, bool kDetect>
+template <typename FT, bool kScreen, bool kDetect, bool kExtrema>
 __global__ void __launch_bounds__(256, sizeof(FT) == 4 ? PMSZ_PREP_MINB : 2) k_prep_q(Dom d, const __grid_constant__ CUtensorMap tf,
                                                    const __grid_constant__ CUtensorMap th, PrepArgs a, int zchunk) {
     pdl_wait();   // (programmatic dependent launch)
@@ -304,8 +321,13 @@ __global__ void __launch_bounds__(256, sizeof(FT) == 4 ? PMSZ_PREP_MINB : 2) k_p
                          [&](int r, const T2<SV>& lb, const T2<SV>& rb, const P2<SV>& rp, SV leaf) {
                 merge2(acc[r], rb);   // U group: the ring of centre r is complete
                 const uint32_t c = cz + r * sy;
-                const bool robust = kScreen && (sizeof(FT) == 4 ? robust2(acc[r], thr32, a.xi)
-                                                                : robust2_narrowed(acc[r], thr32));
+                bool robust = kScreen && (sizeof(FT) == 4 ? robust2(acc[r], thr32, a.xi)
+                                                          : robust2_narrowed(acc[r], thr32));
+                if (kExtrema && kScreen && !robust) {
+                    const SV fcv = (SV)ctr_plane[(row0 + r + 1) * G::kPX + col + 1];
+                    robust = sizeof(FT) == 4 ? robust_extrema(acc[r], fcv, thr32)
+                                             : robust_extrema_narrowed(acc[r], fcv, thr32);
+                }
                 want[r] = live[r] && !robust;
                 if (live[r]) {
                     // validation (correction.py:52-60), hazard H6, g <- fhat
@@ -480,16 +502,18 @@ inline bool launch_prep_q(const Dom& d, const FT* f, const double* fh, double* g
 #define PMSZ_LAUNCH_PREP(R, D)                                                    \
     {                                                                             \
         static unsigned long long attr = 0;                                      \
-        smem_attr_once(k_prep_q<FT, R, D>, (int)smem, attr);                     \
+        smem_attr_once(k_prep_q<FT, R, D, E>, (int)smem, attr);                  \
         if (pdl)   /* (the slab launches wait on copy events: ordinary launches) */             \
-            pdl_launch(k_prep_q<FT, R, D>, grid, block, smem, s, all, tf, th, a, zchunk);         \
+            pdl_launch(k_prep_q<FT, R, D, E>, grid, block, smem, s, all, tf, th, a, zchunk);      \
         else                                                                                       \
-            k_prep_q<FT, R, D><<<grid, block, smem, s>>>(all, tf, th, a, zchunk);                 \
+            k_prep_q<FT, R, D, E><<<grid, block, smem, s>>>(all, tf, th, a, zchunk);              \
     }
-    if (frag && det) { PMSZ_LAUNCH_PREP(true, true); }
-    else if (frag) { PMSZ_LAUNCH_PREP(true, false); }
-    else if (det) { PMSZ_LAUNCH_PREP(false, true); }
-    else { PMSZ_LAUNCH_PREP(false, false); }
+    if (frag && det && d.extrema_only) { constexpr bool E = true; PMSZ_LAUNCH_PREP(true, true); }
+    else if (frag && d.extrema_only) { constexpr bool E = true; PMSZ_LAUNCH_PREP(true, false); }
+    else if (frag && det) { constexpr bool E = false; PMSZ_LAUNCH_PREP(true, true); }
+    else if (frag) { constexpr bool E = false; PMSZ_LAUNCH_PREP(true, false); }
+    else if (det) { constexpr bool E = false; PMSZ_LAUNCH_PREP(false, true); }
+    else { constexpr bool E = false; PMSZ_LAUNCH_PREP(false, false); }
 #undef PMSZ_LAUNCH_PREP
     return true;
 }
