@@ -43,7 +43,10 @@ inline void pdl_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+    if (cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...) != cudaSuccess) {
+        cudaGetLastError();   // (a driver without programmatic launch: the ordinary one)
+        kern<<<grid, block, smem, s>>>(args...);
+    }
 }
 
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per call site and
