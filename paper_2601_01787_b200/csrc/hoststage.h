@@ -13,7 +13,12 @@
 // Host-only C++ (no device code); included by pmsz.cu.
 #pragma once
 #include <cuda_runtime.h>
+#if defined(__x86_64__) || defined(_M_X64)
 #include <emmintrin.h>
+#define PMSZ_HOST_SSE2 1
+#else
+#define PMSZ_HOST_SSE2 0
+#endif
 #include <unistd.h>
 
 #include <algorithm>
@@ -46,7 +51,24 @@ inline bool host_pinned(const void* ptr) {
 // destination line (~2.7 GB of extra DRAM reads at 512^3) is pure waste.
 // SSE2 only (the x86-64 baseline); the caller fences (_mm_sfence) before the
 // DMA is issued.  Unaligned destinations fall back to memcpy.
+// store fence after streaming stores / spin-wait hint (no-ops off x86-64)
+inline void host_sfence() {
+#if PMSZ_HOST_SSE2
+    _mm_sfence();
+#endif
+}
+inline void host_pause() {
+#if PMSZ_HOST_SSE2
+    _mm_pause();
+#endif
+}
+
 inline void nt_copy(char* d1, char* d2, const char* src, size_t bytes) {
+#if !PMSZ_HOST_SSE2
+    memcpy(d1, src, bytes);
+    if (d2) memcpy(d2, src, bytes);
+    return;
+#else
     if ((((uintptr_t)d1 | (uintptr_t)(d2 ? d2 : d1)) & 15) != 0) {
         memcpy(d1, src, bytes);
         if (d2) memcpy(d2, src, bytes);
@@ -84,12 +106,15 @@ inline void nt_copy(char* d1, char* d2, const char* src, size_t bytes) {
         memcpy(d1 + i, src + i, bytes - i);
         if (d2) memcpy(d2 + i, src + i, bytes - i);
     }
+#endif
 }
 
 // f64 -> f32 with streaming stores; true when some value does not survive the
 // round trip (NaN compares unequal, an overflow becomes inf != v).
 inline bool nt_narrow(float* dst, const double* src, size_t n) {
     size_t i = 0;
+    bool nb = false;
+#if PMSZ_HOST_SSE2
     __m128d bad = _mm_setzero_pd();
     if (((uintptr_t)dst & 15) == 0) {
         for (; i + 4 <= n; i += 4) {
@@ -100,7 +125,8 @@ inline bool nt_narrow(float* dst, const double* src, size_t n) {
             bad = _mm_or_pd(bad, _mm_cmpneq_pd(_mm_cvtps_pd(fb), b));
         }
     }
-    bool nb = _mm_movemask_pd(bad) != 0;
+    nb = _mm_movemask_pd(bad) != 0;
+#endif
     for (; i < n; ++i) {
         const float v = (float)src[i];
         dst[i] = v;
@@ -222,7 +248,7 @@ inline void pool_memcpy(void* dst, const void* src, size_t bytes) {
         size_t a, b;
         share_at((uintptr_t)dst, bytes, t, nt, (size_t)2 << 20, &a, &b);
         nt_copy((char*)dst + a, nullptr, (const char*)src + a, b - a);
-        _mm_sfence();
+        host_sfence();
     });
 }
 

@@ -759,7 +759,7 @@ pmsz_status spin_flag(pmsz_plan* p, cudaStream_t s, unsigned long long seq) {
         if (*p->hflag == seq) break;
         // short waits spin; long ones (a host run's K0 waiting for its input)
         // yield the core to the staging threads
-        if (i < 4096) _mm_pause();
+        if (i < 4096) host_pause();
         else std::this_thread::yield();
         if ((i & 4095) == 0) {   // a failed stream would never set the flag
             const cudaError_t q = cudaStreamQuery(s);
@@ -2047,7 +2047,7 @@ void feed_slabs(pmsz_plan* p, StageFeed* fd, int dev, const char* fsrc, bool f_p
                 } else {
                     nt_copy(pin + x0, fill ? (char*)fill + o + x0 : nullptr, src + o + x0, x1 - x0);
                 }
-                _mm_sfence();   // the streaming stores are visible before the DMA is issued
+                host_sfence();   // the streaming stores are visible before the DMA is issued
             }, want);
             if (trace) {
                 const double tc = now();
@@ -2392,7 +2392,7 @@ pmsz_status pmsz_host_to_device(void* dst_dev, const void* src_host, int64_t n, 
             } else {
                 nt_copy(pin + a, nullptr, (const char*)src_host + o + a, b - a);
             }
-            _mm_sfence();
+            host_sfence();
         });
         if (nb.load()) bad = true;
         CUDA_TRY(cudaMemcpyAsync((char*)dst_dev + o, pin, len, cudaMemcpyHostToDevice, r.st));
@@ -2439,7 +2439,7 @@ pmsz_status pmsz_device_to_host(void* dst_host, const void* src_dev, int64_t byt
             size_t a, b;
             share_at((uintptr_t)dst_host + o, len, t, nt, (size_t)2 << 20, &a, &b);
             nt_copy((char*)dst_host + o + a, nullptr, pin + a, b - a);
-            _mm_sfence();
+            host_sfence();
         });
         if (c + r.n < nch) CUDA_TRY(issue(c + r.n));   // the slot is free again
     }
