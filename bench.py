@@ -487,9 +487,9 @@ def e2e_host(args, plan, f32, fh, dims, nvox, dev_res) -> dict:
 
 
 def main():
-    # NCCL prints its version banner on stdout at the first communicator
-    # unless told otherwise: the contract is one JSON line on stdout
-    os.environ.setdefault("NCCL_DEBUG", "WARN")
+    # NCCL's debug output (the image sets NCCL_DEBUG=VERSION: a banner at the
+    # first communicator) goes to stderr: the contract is one JSON line on stdout
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if args.impl == "reference":
