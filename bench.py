@@ -487,8 +487,11 @@ def e2e_host(args, plan, f32, fh, dims, nvox, dev_res) -> dict:
 
 
 def main():
-    # NCCL's debug output (the image sets NCCL_DEBUG=VERSION: a banner at the
-    # first communicator) goes to stderr: the contract is one JSON line on stdout
+    # The image sets NCCL_DEBUG=VERSION, which prints a banner on stdout at the
+    # first communicator; the contract is one JSON line on stdout (an explicit
+    # INFO / TRACE setting is kept, its output sent to stderr)
+    if os.environ.get("NCCL_DEBUG", "").upper() == "VERSION":
+        os.environ["NCCL_DEBUG"] = "WARN"
     os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
