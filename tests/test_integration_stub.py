@@ -255,7 +255,8 @@ def test_dropin_at_slab_size_matches_device():
     assert id(second.corrected.values.base) != base
     del held
     third = pm.run_correction(f, fhat, cfg)
-    assert (id(third.corrected.values.base) == base) == HOST_FIELDS.enabled   # (PMSZ_HOST_CACHE=0: fresh arrays)
+    if HOST_FIELDS.enabled:   # (PMSZ_HOST_CACHE=0: fresh arrays)
+        assert id(third.corrected.values.base) == base
     for r in (second, third):
         assert np.array_equal(r.corrected.values, ref_g)
         assert np.array_equal(r.edits.ids, ref.edit_ids.cpu().numpy())
